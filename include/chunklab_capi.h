@@ -1,0 +1,249 @@
+/*
+ * chunklab_capi.h -- C-ABI of the B200-native COREY hot path (libchunklab_b200.so).
+ *
+ * The reference boundary is the header-only C++ API in
+ * /root/reference/proj/include/chunklab (namespace chunklab).  This C-ABI is
+ * what that API compiles down to in this repo: include/chunklab/*.hpp are
+ * drop-in replacements for the reference headers implemented on top of the
+ * entry points below, and every compute entry point runs on the GPU
+ * (sm_100a kernels in paper_2604_10597_b200/csrc/).  There is no CPU path.
+ *
+ * Conventions
+ *   - Every function returns int status: CL_OK (0) or a CL_E_* code; the
+ *     message is available from cl_last_error(ctx) and, for CL_E_INVALID,
+ *     is byte-identical to the reference's chunklab::invalid_input what().
+ *   - "d_" pointers are device pointers, "h_" pointers are host pointers.
+ *     Buffers are caller-owned; scratch belongs to the context.
+ *   - Device-path functions (cl_minmax_f32 ... cl_selective_scan_f32) are
+ *     asynchronous on the given cudaStream_t (passed as void*) and never
+ *     synchronise with the host.  Errors only the device can see
+ *     (non-finite input, negative signal) are written into the device-side
+ *     cl_decision.status word and surface at cl_decision_check().
+ *   - Host-path functions (suffix _host) take host buffers, synchronise, and
+ *     are the building blocks of the drop-in C++ headers.
+ *   - Multi-GPU: the caller runs the stages on each rank and
+ *     performs two collectives between them: MAX-allreduce of the 4-double
+ *     range buffer after cl_minmax_*, SUM-allreduce of the uint64 counts
+ *     after cl_histogram_*.  Every rank then derives the identical decision.
+ */
+#ifndef CHUNKLAB_CAPI_H
+#define CHUNKLAB_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CL_ABI_VERSION 1
+
+enum cl_status {
+  CL_OK = 0,
+  CL_E_INVALID = 1, /* chunklab::invalid_input (message verbatim)            */
+  CL_E_CUDA = 2,    /* CUDA runtime / launch failure                          */
+  CL_E_DEVICE = 3,  /* device-detected error surfaced by cl_decision_check()  */
+  CL_E_NOMEM = 4
+};
+
+/* Device-side error codes carried in cl_decision.status (0 = ok). */
+enum cl_device_error {
+  CL_DEV_OK = 0,
+  CL_DEV_NON_FINITE = 1, /* "non-finite input"    entropy.hpp:42 / :110        */
+  CL_DEV_NO_SAMPLES = 2, /* "no samples"          entropy.hpp:115              */
+  CL_DEV_SIGNAL = 3      /* "signal must be >= 0" chunk.hpp:72 (constant input) */
+};
+
+typedef struct cl_ctx cl_ctx;
+
+/* ------------------------------------------------------------------------ */
+/* Context                                                                   */
+/* ------------------------------------------------------------------------ */
+int cl_ctx_create(int device, cl_ctx** out);
+int cl_ctx_destroy(cl_ctx* ctx);
+const char* cl_last_error(const cl_ctx* ctx);
+int cl_abi_version(void);
+/* Number of kernel launches this context has issued (bench evidence). */
+uint64_t cl_launch_count(const cl_ctx* ctx);
+
+/* ------------------------------------------------------------------------ */
+/* Specs (POD mirrors of the reference structs)                              */
+/* ------------------------------------------------------------------------ */
+enum { CL_RANGE_DYNAMIC = 0, CL_RANGE_FIXED = 1 };
+
+/* HistogramSpec, entropy.hpp:47-54 (defaults K=256, eps=1e-8, Dynamic, stride 1). */
+typedef struct {
+  int bin_count;
+  double epsilon;
+  int range_mode;
+  double fixed_lo, fixed_hi;
+  uint64_t sample_stride;
+} cl_hist_spec;
+
+/* Policy kinds (chunk.hpp:101-142, the on-device subset). */
+enum {
+  CL_POL_STATIC = 0,
+  CL_POL_MIDPOINT = 1,
+  CL_POL_FULL_HIST = 2,
+  CL_POL_SAMPLED_HIST = 3,
+  CL_POL_LEARNED_TABLE = 4,
+  CL_POL_GUARDED = 5,
+  CL_POL_RULE = 6 /* bare select_chunk (chunk.hpp:68-89), no bucket snap */
+};
+
+/* Source tags (ChunkDecision::source_policy, chunk.hpp:265-368):
+ * 0 "static", 1 "no_entropy_midpoint", 2 "full_histogram", 3 "sampled_histogram",
+ * 4 "learned_table", 6 "rule"; 16+k "guarded[<k>]"; 32 "guarded[fallback]". */
+enum { CL_SRC_GUARDED = 16, CL_SRC_GUARDED_FALLBACK = 32 };
+
+/* ChunkBounds (chunk.hpp:29-32) + CalibrationRef (chunk.hpp:42-59) + SchedulerPolicy. */
+typedef struct {
+  int kind;
+  int static_chunk;          /* StaticPolicy::chunk */
+  int inner_kind;            /* GuardedPolicy::inner (non-guarded kind) */
+  int inner_static_chunk;
+  int safe_chunk;            /* GuardedPolicy::safe_chunk (512) */
+  int min_delta_buckets;     /* GuardedPolicy::min_delta_buckets (2) */
+  uint64_t threshold_tokens; /* LearnedTablePolicy (50, 128, 512) */
+  int short_chunk, long_chunk;
+  int n_buckets;             /* SchedulerPolicy::bucket_set, <= 16 */
+  int buckets[16];
+  int c_min, c_max;          /* ChunkBounds */
+  double h_ref_nats;         /* CalibrationRef::h_ref_nats (log K or legacy) */
+} cl_rule_spec;
+
+/* Decision record written by the device (ChunkDecision + EntropyEstimate + Histogram scalars). */
+typedef struct {
+  int32_t status;        /* cl_device_error */
+  int32_t chunk;         /* ChunkDecision::chunk */
+  int32_t source;        /* source tag */
+  int32_t bin_count;
+  double r;              /* ChunkDecision::r */
+  double signal_nats;    /* ChunkDecision::signal_nats */
+  double raw_nats;       /* EntropyEstimate::raw_nats */
+  double normalized;     /* EntropyEstimate::normalized */
+  double lo, hi;         /* Histogram::lo/hi */
+  uint64_t sample_count; /* Histogram::sample_count */
+  double margin;         /* |log2(target) - (e - 0.5)|: knife-edge diagnostic */
+} cl_decision;
+
+/* ------------------------------------------------------------------------ */
+/* Device path (async, stream-ordered; the prefill hot path)                 */
+/* ------------------------------------------------------------------------ */
+/* Stage 1 (entropy.hpp:108-114): strided min/max over the samples whose GLOBAL
+ * flat index (global_offset + i) is a multiple of stride, and a finite check
+ * over EVERY element (entropy.hpp:42).  d_range (4 doubles, MAX-allreducible):
+ * {-lo, hi, nonfinite(0/1), 0}.  Initialise with cl_range_init. */
+int cl_range_init(cl_ctx* ctx, double* d_range, void* stream);
+int cl_minmax_f32(cl_ctx* ctx, const float* d_values, uint64_t n, uint64_t global_offset,
+                  uint64_t stride, double* d_range, void* stream);
+int cl_minmax_f64(cl_ctx* ctx, const double* d_values, uint64_t n, uint64_t global_offset,
+                  uint64_t stride, double* d_range, void* stream);
+
+/* Stage 2 (entropy.hpp:116-126): accumulate K uint64 counts of the strided
+ * samples, binned exactly as detail::bin_index (entropy.hpp:87-94) over the
+ * (global) range in d_range, or the spec's fixed range.  d_counts must be
+ * zeroed first (cl_counts_zero) when starting a new histogram. */
+int cl_counts_zero(cl_ctx* ctx, uint64_t* d_counts, int bin_count, void* stream);
+int cl_histogram_f32(cl_ctx* ctx, const float* d_values, uint64_t n, uint64_t global_offset,
+                     const cl_hist_spec* spec, const double* d_range, uint64_t* d_counts,
+                     void* stream);
+int cl_histogram_f64(cl_ctx* ctx, const double* d_values, uint64_t n, uint64_t global_offset,
+                     const cl_hist_spec* spec, const double* d_range, uint64_t* d_counts,
+                     void* stream);
+
+/* Stage 3 (entropy.hpp:149-164 + chunk.hpp:68-89/256-368): masses, entropy,
+ * rule, bucket snap, guarded / learned-table policy -> d_decision.
+ * n_samples_total = number of samples over all ranks (ceil(N_global/stride)).
+ * seq_len feeds the learned-table policy. */
+int cl_decide(cl_ctx* ctx, const uint64_t* d_counts, const double* d_range,
+              const cl_hist_spec* spec, uint64_t n_samples_total, const cl_rule_spec* rule,
+              uint64_t seq_len, cl_decision* d_decision, void* stream);
+
+/* Stage 4: fused Mamba-1 selective scan (fp32), chunk read from d_decision.
+ * Layouts (mamba_ssm selective_scan_fn): u, delta, z, out: (batch, dim, L)
+ * row-major; A: (dim, N); B, C: (batch, N, L); D, delta_bias: (dim) or NULL;
+ * z NULL -> no gate; h0 NULL -> zeros; h_last (batch, dim, N) or NULL.
+ * N must be 16 on the TMA fast path, <= 64 in general. */
+typedef struct {
+  const float* u;
+  const float* delta;
+  const float* A;
+  const float* B;
+  const float* C;
+  const float* D;
+  const float* z;
+  const float* delta_bias;
+  const float* h0;
+  float* out;
+  float* h_last;
+  uint64_t batch, dim, seq_len, d_state;
+  int delta_softplus;
+} cl_mamba1_args;
+
+/* Scan variants: CL_SCAN_AUTO picks by shape. */
+enum { CL_SCAN_AUTO = 0, CL_SCAN_ROWSEQ_TMA = 1, CL_SCAN_GENERIC = 2 };
+int cl_selective_scan_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_decision* d_decision,
+                          int fixed_chunk /* used when d_decision == NULL */, int variant,
+                          void* stream);
+
+/* Single-GPU convenience: range_init -> minmax -> histogram -> decide -> scan,
+ * all on one stream, no host sync.  d_counts: K uint64 scratch; d_range: 4 doubles. */
+int cl_prefill_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_hist_spec* spec,
+                   const cl_rule_spec* rule, uint64_t* d_counts, double* d_range,
+                   cl_decision* d_decision, void* stream);
+
+/* Sync point: copy the decision to the host and convert a device error into
+ * CL_E_DEVICE with the reference's message. */
+int cl_decision_check(cl_ctx* ctx, const cl_decision* d_decision, cl_decision* h_out,
+                      void* stream);
+
+/* fp64 reference-mode recurrence on device (scan.hpp:77-136), bit-identical
+ * to chunklab::scan_sequential / scan_chunked: h = a*h + b*x; out += c*h;
+ * y = out + d*x, no FMA contraction, state order s = 0..N-1.
+ * a: d*N (constant) or L*d*N [t][c][s]; b, c: N or L*N [t][s]; d: channels;
+ * x: [c][t].  h0 NULL -> zeros.  chunk 0 -> sequential. */
+typedef struct {
+  uint64_t channels, state_dim, seq_len;
+  const double *a, *b, *c, *d, *x;
+  uint64_t a_len, b_len, c_len, d_len, x_len;
+} cl_scan_params_f64;
+int cl_scan_f64(cl_ctx* ctx, const cl_scan_params_f64* d_params, const double* d_h0,
+                uint64_t chunk, double* d_y, double* d_h, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Host path (synchronous; used by include/chunklab/*.hpp)                    */
+/* ------------------------------------------------------------------------ */
+/* validate_spec (entropy.hpp:56-62), validate_bounds (chunk.hpp:34-40). */
+int cl_validate_hist_spec(cl_ctx* ctx, const cl_hist_spec* spec);
+int cl_validate_rule(cl_ctx* ctx, const cl_rule_spec* rule);
+
+/* compute_histogram(span, spec) (entropy.hpp:101-138) on the GPU. */
+int cl_compute_histogram_host(cl_ctx* ctx, const double* h_values, uint64_t n,
+                              const cl_hist_spec* spec, uint64_t* h_counts, double* h_masses,
+                              double* h_lo, double* h_hi, uint64_t* h_sample_count);
+/* estimate_entropy(hist, eps) (entropy.hpp:149-164) on the GPU. */
+int cl_estimate_entropy_host(cl_ctx* ctx, const double* h_masses, int bin_count, double epsilon,
+                             double* h_raw, double* h_normalized);
+
+/* Scheduler::decide for pre-computed host features (chunk.hpp:256-368), on the GPU.
+ * has_* flags mirror std::optional presence (chunk.hpp:185-193). */
+typedef struct {
+  int has_full_entropy;
+  double full_entropy_nats;
+  int has_sampled_entropy;
+  double sampled_entropy_nats;
+  int has_seq_len;
+  uint64_t seq_len;
+} cl_features;
+int cl_schedule_host(cl_ctx* ctx, const cl_rule_spec* rule, const cl_features* features,
+                     cl_decision* h_out);
+
+/* scan_sequential / scan_chunked (scan.hpp:113-136) on the GPU (fp64, bit-exact). */
+int cl_scan_f64_host(cl_ctx* ctx, const cl_scan_params_f64* h_params, const double* h_h0,
+                     uint64_t chunk, double* h_y, double* h_h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHUNKLAB_CAPI_H */

@@ -1,0 +1,63 @@
+// cl_internal.h -- internal declarations shared by the C-ABI implementation and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "chunklab_capi.h"
+
+struct cl_ctx {
+  int device = 0;
+  int num_sms = 148;
+  std::string last_error;
+  uint64_t launches = 0;
+  // device scratch owned by the context
+  double* d_scratch_range = nullptr;   // 4 doubles
+  uint64_t* d_scratch_counts = nullptr;  // up to kMaxBinsScratch
+  cl_decision* d_scratch_decision = nullptr;
+  unsigned int* d_work = nullptr;  // scan work counters / flags (grown on demand)
+  size_t work_bytes = 0;
+  float* d_carry = nullptr;  // scan segment carry (grown on demand)
+  size_t carry_bytes = 0;
+  cudaStream_t own_stream = nullptr;
+};
+
+namespace cl {
+
+constexpr int kMaxBinsScratch = 1 << 16;
+
+// Set the error message and return the code.
+int fail(cl_ctx* ctx, int code, const std::string& msg);
+int cuda_fail(cl_ctx* ctx, cudaError_t e, const char* where);
+
+// ---- kernel launchers (defined in the .cu files) ----
+// entropy.cu
+cudaError_t launch_range_init(double* d_range, cudaStream_t s);
+cudaError_t launch_minmax_f32(const float* v, uint64_t n, uint64_t g0, uint64_t stride,
+                              double* d_range, int num_sms, cudaStream_t s, int* launches);
+cudaError_t launch_minmax_f64(const double* v, uint64_t n, uint64_t g0, uint64_t stride,
+                              double* d_range, int num_sms, cudaStream_t s, int* launches);
+cudaError_t launch_histogram_f32(const float* v, uint64_t n, uint64_t g0,
+                                 const cl_hist_spec& spec, const double* d_range,
+                                 uint64_t* d_counts, int num_sms, cudaStream_t s,
+                                 int* launches);
+cudaError_t launch_histogram_f64(const double* v, uint64_t n, uint64_t g0,
+                                 const cl_hist_spec& spec, const double* d_range,
+                                 uint64_t* d_counts, int num_sms, cudaStream_t s,
+                                 int* launches);
+cudaError_t launch_decide(const uint64_t* d_counts, const double* d_range,
+                          const cl_hist_spec& spec, uint64_t n_samples, const cl_rule_spec& rule,
+                          uint64_t seq_len, const cl_features* features_or_null,
+                          cl_decision* d_out, cudaStream_t s);
+cudaError_t launch_entropy_from_masses(const double* d_masses, int k, double eps, double* d_out,
+                                       cudaStream_t s);
+// scan_f64.cu
+cudaError_t launch_scan_f64(const cl_scan_params_f64& p, const double* d_h0, uint64_t chunk,
+                            double* d_y, double* d_h, cudaStream_t s);
+// scan_mamba1.cu
+int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decision,
+                int fixed_chunk, int variant, cudaStream_t s);
+
+}  // namespace cl

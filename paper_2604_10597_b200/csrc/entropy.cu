@@ -1,0 +1,848 @@
+// entropy.cu -- sm_100a kernels for the K-bin activation-entropy estimator and the
+// on-device chunk rule (reference: proj/include/chunklab/entropy.hpp, chunk.hpp).
+//
+//   minmax      entropy.hpp:108-114  strided min/max + all-element finite check
+//   histogram   entropy.hpp:116-126  exact detail::bin_index binning (bit-exact counts)
+//   decide      entropy.hpp:130-164 + chunk.hpp:68-89, 206-218, 256-368
+//
+// Bit-exactness of the fp32 histogram: the reference bins in fp64 with
+// floor((v-lo)/(hi-lo)*K).  The kernel bins in fp32 with a proven error bound
+// delta on x = (v-lo_f)*s_f; whenever x lies within delta of an interior bin
+// boundary (probability ~2*delta per sample) it recomputes the bin with the
+// reference's exact fp64 operation sequence.  Away from boundaries floor(x) equals
+// the reference's bin, so counts are bit-exact by construction.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+
+#include "cl_internal.h"
+
+namespace cl {
+namespace {
+
+constexpr int kThreads = 256;
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ bool finite_f32(float x) {
+  return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u;
+}
+__device__ __forceinline__ bool finite_f64(double x) {
+  return (__double_as_longlong(x) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;
+}
+
+__device__ __forceinline__ void atomic_max_f64(double* addr, double v) {
+  unsigned long long* a = reinterpret_cast<unsigned long long*>(addr);
+  unsigned long long old = *a;
+  while (__longlong_as_double(static_cast<long long>(old)) < v) {
+    const unsigned long long assumed = old;
+    old = atomicCAS(a, assumed, static_cast<unsigned long long>(__double_as_longlong(v)));
+    if (old == assumed) break;
+  }
+}
+
+// detail::bin_index (entropy.hpp:87-94), operation-for-operation in fp64.  The
+// int conversion reproduces x86-64 cvttsd2si (out-of-range -> INT_MIN), which is
+// what the reference's static_cast<int> does on its build target; it only
+// matters for Fixed-range outliers more than 2^31 bins away.
+__device__ __forceinline__ int bin_index_exact(double v, double lo, double width, int k) {
+  if (!(width > 0.0)) return 0;
+  const double x = __dmul_rn(__ddiv_rn(__dsub_rn(v, lo), width), static_cast<double>(k));
+  const double f = floor(x);
+  int idx;
+  if (!(f >= -2147483648.0 && f < 2147483648.0))
+    idx = INT_MIN;
+  else
+    idx = static_cast<int>(f);
+  if (idx < 0) idx = 0;
+  if (idx >= k) idx = k - 1;
+  return idx;
+}
+
+// Per-launch binning parameters, derived on device from the (allreduced) range.
+struct BinParams {
+  double lo, width;  // exact fp64 range
+  float lo_f, s_f;   // fast-path fp32 affine map x = (v - lo_f) * s_f
+  float delta;       // error bound on x; < 0 -> always take the exact path
+  int k;
+};
+
+__device__ BinParams make_bin_params(const double* d_range, int range_mode, double fixed_lo,
+                                     double fixed_hi, int k) {
+  BinParams p;
+  double lo, hi;
+  if (range_mode == CL_RANGE_FIXED) {
+    lo = fixed_lo;
+    hi = fixed_hi;
+  } else {
+    lo = -d_range[0];
+    hi = d_range[1];
+  }
+  p.lo = lo;
+  p.width = __dsub_rn(hi, lo);
+  p.k = k;
+  if (!(p.width > 0.0)) {  // degenerate range: everything in bin 0 (entropy.hpp:89)
+    p.lo_f = 0.f;
+    p.s_f = 0.f;
+    p.delta = 0.f;
+    return p;
+  }
+  const double S = static_cast<double>(k) / p.width;
+  p.lo_f = static_cast<float>(lo);
+  p.s_f = static_cast<float>(S);
+  const double u = 5.9604644775390625e-08;  // 2^-24
+  // |x - X| <= |X|*((1+u)^3-1) + |lo-lo_f|*S*(1+u)^3 for |X| <= k (see header);
+  // take twice that, plus room for the fp64 reference's own rounding.
+  const double err = static_cast<double>(k) * 3.0001 * u +
+                     fabs(lo - static_cast<double>(p.lo_f)) * S * 1.0001;
+  const double delta = 2.0 * err + static_cast<double>(k) * 1e-12;
+  const bool ok = isfinite(p.lo_f) && isfinite(p.s_f) && p.s_f > 0.f && delta < 0.25;
+  p.delta = ok ? static_cast<float>(delta) * 1.0001f : -1.f;
+  return p;
+}
+
+// Fast fp32 bin with exact fallback.  Returns the reference bin for v.
+__device__ __forceinline__ int bin_f32(float v, const BinParams& p) {
+  const float x = (v - p.lo_f) * p.s_f;
+  const float xc = fminf(fmaxf(x, -1.0f), static_cast<float>(p.k) + 1.0f);
+  const float t = xc + 12582912.0f;  // 1.5*2^23: round-to-nearest into the mantissa
+  const float rn = t - 12582912.0f;
+  const int n = __float_as_int(t) - 0x4B400000;
+  const int fl = n - (xc < rn ? 1 : 0);
+  const bool near = fabsf(xc - rn) <= p.delta && n >= 1 && n <= p.k - 1;
+  const bool slow = near || p.delta < 0.f || !(fabsf(x) < 1e9f);
+  if (__builtin_expect(slow, 0))
+    return bin_index_exact(static_cast<double>(v), p.lo, p.width, p.k);
+  return fl < 0 ? 0 : (fl >= p.k ? p.k - 1 : fl);
+}
+
+// ---------------------------------------------------------------------------
+// Stage 1: min/max + finite
+// ---------------------------------------------------------------------------
+template <typename T>
+struct Vec4;
+template <>
+struct Vec4<float> {
+  using type = float4;
+};
+template <>
+struct Vec4<double> {
+  using type = double2;  // 16 bytes
+};
+
+template <int MODE>
+__device__ __forceinline__ bool sampled(uint64_t gi, uint64_t stride) {
+  if (MODE == 0) return true;
+  if (MODE == 1) return (gi & (stride - 1)) == 0;
+  return gi % stride == 0;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) minmax_f32_kernel(const float* __restrict__ v,
+                                                              uint64_t n, uint64_t g0,
+                                                              uint64_t stride, double* range) {
+  float lo = FLT_MAX, hi = -FLT_MAX;
+  bool any = false;
+  bool bad = false;
+  const uint64_t head = umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
+  const uint64_t n4 = (n - head) / 4;
+  const uint64_t tail0 = head + n4 * 4;
+  auto visit = [&](float x, uint64_t i) {
+    bad |= !finite_f32(x);
+    if (sampled<MODE>(g0 + i, stride)) {
+      lo = fminf(lo, x);
+      hi = fmaxf(hi, x);
+      any = true;
+    }
+  };
+  if (blockIdx.x == 0) {
+    for (uint64_t i = threadIdx.x; i < head; i += blockDim.x) visit(v[i], i);
+    for (uint64_t i = tail0 + threadIdx.x; i < n; i += blockDim.x) visit(v[i], i);
+  }
+  const float4* v4 = reinterpret_cast<const float4*>(v + head);
+  const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint64_t i4 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i4 + 3 * T < n4; i4 += 4 * T) {
+    float4 q[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) q[j] = __ldcs(v4 + i4 + j * T);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t i = head + (i4 + j * T) * 4;
+      visit(q[j].x, i);
+      visit(q[j].y, i + 1);
+      visit(q[j].z, i + 2);
+      visit(q[j].w, i + 3);
+    }
+  }
+  for (; i4 < n4; i4 += T) {
+    const float4 q = __ldcs(v4 + i4);
+    const uint64_t i = head + i4 * 4;
+    visit(q.x, i);
+    visit(q.y, i + 1);
+    visit(q.z, i + 2);
+    visit(q.w, i + 3);
+  }
+  // block reduce
+  for (int o = 16; o; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  any = __any_sync(0xffffffffu, any);
+  bad = __any_sync(0xffffffffu, bad);
+  __shared__ float s_lo[kThreads / 32], s_hi[kThreads / 32];
+  __shared__ int s_any[kThreads / 32], s_bad[kThreads / 32];
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (l == 0) {
+    s_lo[w] = lo;
+    s_hi[w] = hi;
+    s_any[w] = any;
+    s_bad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < kThreads / 32; ++k) {
+      lo = fminf(lo, s_lo[k]);
+      hi = fmaxf(hi, s_hi[k]);
+      any |= s_any[k] != 0;
+      bad |= s_bad[k] != 0;
+    }
+    if (any) {
+      atomic_max_f64(range + 0, -static_cast<double>(lo));
+      atomic_max_f64(range + 1, static_cast<double>(hi));
+    }
+    if (bad) atomic_max_f64(range + 2, 1.0);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) minmax_f64_kernel(const double* __restrict__ v,
+                                                              uint64_t n, uint64_t g0,
+                                                              uint64_t stride, double* range) {
+  double lo = DBL_MAX, hi = -DBL_MAX;
+  bool any = false, bad = false;
+  const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += T) {
+    const double x = v[i];
+    bad |= !finite_f64(x);
+    if (sampled<MODE>(g0 + i, stride)) {
+      // std::min(lo, x) keeps lo unless x < lo (entropy.hpp:111-112)
+      lo = x < lo ? x : lo;
+      hi = hi < x ? x : hi;
+      any = true;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const double h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = l2 < lo ? l2 : lo;
+    hi = hi < h2 ? h2 : hi;
+  }
+  any = __any_sync(0xffffffffu, any);
+  bad = __any_sync(0xffffffffu, bad);
+  __shared__ double s_lo[kThreads / 32], s_hi[kThreads / 32];
+  __shared__ int s_any[kThreads / 32], s_bad[kThreads / 32];
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (l == 0) {
+    s_lo[w] = lo;
+    s_hi[w] = hi;
+    s_any[w] = any;
+    s_bad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < kThreads / 32; ++k) {
+      lo = s_lo[k] < lo ? s_lo[k] : lo;
+      hi = hi < s_hi[k] ? s_hi[k] : hi;
+      any |= s_any[k] != 0;
+      bad |= s_bad[k] != 0;
+    }
+    if (any) {
+      atomic_max_f64(range + 0, -lo);
+      atomic_max_f64(range + 1, hi);
+    }
+    if (bad) atomic_max_f64(range + 2, 1.0);
+  }
+}
+
+__global__ void range_init_kernel(double* range) {
+  range[0] = -INFINITY;
+  range[1] = -INFINITY;
+  range[2] = 0.0;
+  range[3] = 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Stage 2: histogram.  K <= 256: lane-private 16-bit counters laid out
+// [bin/2][lane] per warp, so a warp's 32 increments hit 32 distinct banks
+// whatever the bins (no atomics, no conflicts).  Input is streamed through a
+// 4-stage shared-memory ring filled by cp.async.bulk (TMA bulk copies) issued
+// by a dedicated producer warp.
+// ---------------------------------------------------------------------------
+constexpr int kHistWarps = 8;                     // consumer warps
+constexpr int kHistThreads = (kHistWarps + 1) * 32;  // + producer warp
+constexpr int kStages = 4;
+constexpr int kChunkFloats = 4096;                // 16 KB per stage
+constexpr int kChunkBytes = kChunkFloats * 4;
+constexpr int kLaneWords = 128;                   // 256 bins / 2 per word
+constexpr size_t kHistSmem =
+    size_t(kHistWarps) * kLaneWords * 32 * 4 + size_t(kStages) * kChunkBytes + 2 * kStages * 8 + 64;
+constexpr int kFlushChunks = 4000;  // 16 samples/lane/chunk * 4000 < 65536
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void flush_lane_counters(uint32_t* cnt, int lane, int k,
+                                                    unsigned long long* d_counts) {
+  __syncwarp();
+  const int words = (k + 1) / 2;
+  for (int p = lane; p < words; p += 32) {
+    uint32_t lo = 0, hi = 0;
+#pragma unroll 8
+    for (int s = 0; s < 32; ++s) {
+      const int col = (lane + s) & 31;  // rotated: 32 lanes hit 32 banks
+      const uint32_t w = cnt[p * 32 + col];
+      lo += w & 0xffffu;
+      hi += w >> 16;
+    }
+    if (lo) atomicAdd(d_counts + 2 * p, static_cast<unsigned long long>(lo));
+    if (hi && 2 * p + 1 < k) atomicAdd(d_counts + 2 * p + 1, static_cast<unsigned long long>(hi));
+  }
+  __syncwarp();
+  for (int i = lane; i < words * 32; i += 32) cnt[i] = 0;
+  __syncwarp();
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kHistThreads, 1)
+    hist_f32_lane_kernel(const float* __restrict__ v, uint64_t n, uint64_t g0, uint64_t stride,
+                         int range_mode, double fixed_lo, double fixed_hi, int k,
+                         const double* __restrict__ d_range, unsigned long long* d_counts) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t* counters = reinterpret_cast<uint32_t*>(smem);
+  unsigned char* ring = smem + size_t(kHistWarps) * kLaneWords * 32 * 4;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(kStages) * kChunkBytes);
+  uint64_t* empty = full + kStages;
+  __shared__ BinParams sp;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    sp = make_bin_params(d_range, range_mode, fixed_lo, fixed_hi, k);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kHistWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < kHistWarps * kLaneWords * 32; i += blockDim.x) counters[i] = 0;
+  __syncthreads();
+  const BinParams p = sp;
+
+  // Body = 16B-aligned span of v; head/tail (< 4 elements each) go to block 0.
+  const uint64_t head =
+      umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
+  const uint64_t body_n = ((n - head) / 4) * 4;
+  const float* body = v + head;
+  const uint64_t n_chunks = (body_n + kChunkFloats - 1) / kChunkFloats;
+
+  if (warp == kHistWarps) {
+    // ---------------- producer warp ----------------
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+        const int s = it % kStages;
+        const uint32_t phase = (it / kStages) & 1;
+        if (it >= kStages) mbar_wait(empty + s, phase ^ 1);
+        const uint64_t off = c * kChunkFloats;
+        const uint32_t bytes =
+            static_cast<uint32_t>(umin64(kChunkFloats, body_n - off) * 4);
+        mbar_expect_tx(full + s, bytes);
+        bulk_g2s(ring + size_t(s) * kChunkBytes, body + off, bytes, full + s);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  uint32_t* cnt = counters + warp * kLaneWords * 32;
+  auto count = [&](int bin) { cnt[(bin >> 1) * 32 + lane] += 1u << ((bin & 1) << 4); };
+
+  if (blockIdx.x == 0 && warp == 0) {
+    for (uint64_t i = lane; i < head; i += 32)
+      if (sampled<MODE>(g0 + i, stride)) count(bin_f32(v[i], p));
+    for (uint64_t i = head + body_n + lane; i < n; i += 32)
+      if (sampled<MODE>(g0 + i, stride)) count(bin_f32(v[i], p));
+  }
+
+  uint32_t it = 0, since_flush = 0;
+  for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+    const int s = it % kStages;
+    const uint32_t phase = (it / kStages) & 1;
+    mbar_wait(full + s, phase);
+    const float4* tile = reinterpret_cast<const float4*>(ring + size_t(s) * kChunkBytes);
+    const uint64_t off = c * kChunkFloats;
+    const int valid4 = static_cast<int>(umin64(kChunkFloats, body_n - off) / 4);
+    float4 q[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = j * (kHistWarps * 32) + warp * 32 + lane;
+      q[j] = idx < valid4 ? tile[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = j * (kHistWarps * 32) + warp * 32 + lane;
+      if (idx < valid4) {
+        const uint64_t gi = g0 + head + off + static_cast<uint64_t>(idx) * 4;
+        if (sampled<MODE>(gi, stride)) count(bin_f32(q[j].x, p));
+        if (sampled<MODE>(gi + 1, stride)) count(bin_f32(q[j].y, p));
+        if (sampled<MODE>(gi + 2, stride)) count(bin_f32(q[j].z, p));
+        if (sampled<MODE>(gi + 3, stride)) count(bin_f32(q[j].w, p));
+      }
+    }
+    if (++since_flush == kFlushChunks) {
+      flush_lane_counters(cnt, lane, k, d_counts);
+      since_flush = 0;
+    }
+  }
+  flush_lane_counters(cnt, lane, k, d_counts);
+}
+
+// K > 256 (or f64 input): shared-memory atomics on a CTA histogram.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kThreads)
+    hist_atomic_kernel(const T* __restrict__ v, uint64_t n, uint64_t g0, uint64_t stride,
+                       int range_mode, double fixed_lo, double fixed_hi, int k,
+                       const double* __restrict__ d_range, unsigned long long* d_counts,
+                       int use_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);
+  __shared__ BinParams sp;
+  if (threadIdx.x == 0) sp = make_bin_params(d_range, range_mode, fixed_lo, fixed_hi, k);
+  if (use_smem)
+    for (int i = threadIdx.x; i < k; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const BinParams p = sp;
+  const uint64_t nthr = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += nthr) {
+    if (!sampled<MODE>(g0 + i, stride)) continue;
+    int b;
+    if constexpr (sizeof(T) == 4)
+      b = bin_f32(v[i], p);
+    else
+      b = bin_index_exact(v[i], p.lo, p.width, k);
+    if (use_smem)
+      atomicAdd(hist + b, 1u);
+    else
+      atomicAdd(d_counts + b, 1ull);
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += blockDim.x)
+      if (hist[i]) atomicAdd(d_counts + i, static_cast<unsigned long long>(hist[i]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage 3: entropy + rule + policy (one CTA).
+// ---------------------------------------------------------------------------
+struct DecideArgs {
+  const unsigned long long* counts;  // may be null (host-features mode)
+  const double* range;
+  int k;
+  double epsilon;
+  int range_mode;
+  double fixed_lo, fixed_hi;
+  uint64_t n_samples;
+  cl_rule_spec rule;
+  uint64_t seq_len;
+  int features_mode;  // 0: entropy from counts; 1: host features
+  cl_features f;
+};
+
+__device__ __forceinline__ int ilog2_pow2(int v) { return 31 - __clz(v); }
+
+// select_chunk (chunk.hpp:68-89) in fp64.  Returns 0 or CL_DEV_SIGNAL.
+__device__ int device_select_chunk(double signal, int c_min, int c_max, double h_ref, int* chunk,
+                                   double* r_out, double* margin) {
+  if (!(signal >= 0.0)) return CL_DEV_SIGNAL;
+  double r = __ddiv_rn(signal, h_ref);
+  if (1.0 < r) r = 1.0;
+  const double target = __dadd_rn(static_cast<double>(c_min),
+                                  __dmul_rn(r, static_cast<double>(c_max - c_min)));
+  const double l2 = log2(target);
+  const double e = floor(__dadd_rn(l2, 0.5));  // round_half_up (common.hpp:35)
+  const double frac = __dsub_rn(__dadd_rn(l2, 0.5), e);
+  *margin = fmin(frac, 1.0 - frac);
+  const double pow2 = exp2(e);
+  int c = static_cast<int>(pow2);
+  c = c < c_min ? c_min : (c > c_max ? c_max : c);
+  *chunk = c;
+  *r_out = r;
+  return 0;
+}
+
+// snap_to_buckets (chunk.hpp:206-218): nearest by |log2| distance, ties toward
+// the larger bucket.  All operands are powers of two, so log2 is exact.
+__device__ int device_snap(int chunk, const cl_rule_spec& rule) {
+  int best = rule.buckets[0];
+  int best_dist = INT_MAX;
+  const int lc = ilog2_pow2(chunk);
+  for (int i = 0; i < rule.n_buckets; ++i) {
+    const int b = rule.buckets[i];
+    int d = ilog2_pow2(b) - lc;
+    d = d < 0 ? -d : d;
+    if (d < best_dist || (d == best_dist && b > best)) {
+      best = b;
+      best_dist = d;
+    }
+  }
+  return best;
+}
+
+__device__ int decide_simple(const DecideArgs& a, int kind, int static_chunk, double entropy,
+                             cl_decision& out) {
+  const cl_rule_spec& rule = a.rule;
+  out.r = 0.0;
+  out.signal_nats = 0.0;
+  switch (kind) {
+    case CL_POL_STATIC:
+      out.chunk = static_chunk;
+      out.source = 0;
+      return 0;
+    case CL_POL_MIDPOINT: {
+      const int n = rule.n_buckets;
+      int idx = (n + 1) / 2;
+      if (idx > n - 1) idx = n - 1;
+      out.chunk = rule.buckets[idx];
+      out.source = 1;
+      return 0;
+    }
+    case CL_POL_FULL_HIST:
+    case CL_POL_SAMPLED_HIST:
+    case CL_POL_RULE: {
+      int c;
+      double r;
+      const int st = device_select_chunk(entropy, rule.c_min, rule.c_max, rule.h_ref_nats, &c,
+                                         &r, &out.margin);
+      if (st) return st;
+      out.chunk = kind == CL_POL_RULE ? c : device_snap(c, rule);
+      out.r = r;
+      out.signal_nats = entropy;
+      out.source = kind == CL_POL_RULE ? 6 : (kind == CL_POL_FULL_HIST ? 2 : 3);
+      return 0;
+    }
+    case CL_POL_LEARNED_TABLE: {
+      const uint64_t L = a.features_mode ? a.f.seq_len : a.seq_len;
+      out.chunk = L < rule.threshold_tokens ? rule.short_chunk : rule.long_chunk;
+      out.signal_nats = static_cast<double>(L);
+      out.source = 4;
+      return 0;
+    }
+  }
+  return 0;
+}
+
+__global__ void __launch_bounds__(kThreads) decide_kernel(DecideArgs a, cl_decision* d_out) {
+  __shared__ double terms[kThreads];
+  cl_decision out = {};
+  out.margin = 1.0;
+  double entropy = 0.0;
+  int status = 0;
+  if (a.features_mode == 0) {
+    const bool bad = a.range[2] != 0.0;
+    // masses[b] = counts[b] * (1/n) (entropy.hpp:130-133); terms p*log(p+eps)
+    const double inv_n = __ddiv_rn(1.0, static_cast<double>(a.n_samples));
+    double raw = 0.0;
+    for (int base = 0; base < a.k; base += kThreads) {
+      const int b = base + threadIdx.x;
+      double t = 0.0;
+      if (b < a.k) {
+        const double pm = __dmul_rn(static_cast<double>(a.counts[b]), inv_n);
+        if (pm > 0.0) t = __dmul_rn(pm, log(__dadd_rn(pm, a.epsilon)));
+      }
+      terms[threadIdx.x] = t;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        // raw -= p*log(p+eps) in bin order (entropy.hpp:154-156)
+        const int m = min(kThreads, a.k - base);
+        for (int i = 0; i < m; ++i)
+          if (a.counts[base + i] != 0ull) raw = __dsub_rn(raw, terms[i]);
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    out.raw_nats = raw;
+    out.normalized = __ddiv_rn(raw, log(static_cast<double>(a.k)));
+    out.bin_count = a.k;
+    out.sample_count = a.n_samples;
+    if (a.range_mode == CL_RANGE_FIXED) {
+      out.lo = a.fixed_lo;
+      out.hi = a.fixed_hi;
+    } else {
+      out.lo = -a.range[0];
+      out.hi = a.range[1];
+    }
+    entropy = raw;
+    if (bad) status = CL_DEV_NON_FINITE;
+    else if (a.n_samples == 0) status = CL_DEV_NO_SAMPLES;
+  } else {
+    if (threadIdx.x != 0) return;
+  }
+
+  if (status == 0) {
+    const cl_rule_spec& rule = a.rule;
+    double e_inner = entropy;
+    if (a.features_mode) {
+      const int kind = rule.kind == CL_POL_GUARDED ? rule.inner_kind : rule.kind;
+      e_inner = kind == CL_POL_SAMPLED_HIST ? a.f.sampled_entropy_nats : a.f.full_entropy_nats;
+    }
+    if (rule.kind != CL_POL_GUARDED) {
+      status = decide_simple(a, rule.kind, rule.static_chunk, e_inner, out);
+    } else {
+      // GuardedPolicy (chunk.hpp:344-358)
+      status = decide_simple(a, rule.inner_kind, rule.inner_static_chunk, e_inner, out);
+      if (!status) {
+        int delta = ilog2_pow2(out.chunk) - ilog2_pow2(rule.safe_chunk);
+        delta = delta < 0 ? -delta : delta;
+        if (delta >= rule.min_delta_buckets) {
+          out.source += CL_SRC_GUARDED;
+        } else {
+          out.chunk = rule.safe_chunk;
+          out.source = CL_SRC_GUARDED_FALLBACK;
+        }
+      }
+    }
+  }
+  out.status = status;
+  *d_out = out;
+}
+
+__global__ void entropy_masses_kernel(const double* masses, int k, double eps, double* out) {
+  __shared__ double terms[kThreads];
+  double raw = 0.0;
+  for (int base = 0; base < k; base += kThreads) {
+    const int b = base + threadIdx.x;
+    double t = 0.0;
+    if (b < k) {
+      const double pm = masses[b];
+      if (pm > 0.0) t = __dmul_rn(pm, log(__dadd_rn(pm, eps)));
+    }
+    terms[threadIdx.x] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int m = min(kThreads, k - base);
+      for (int i = 0; i < m; ++i) {
+        const double pm = masses[base + i];
+        if (pm > 0.0) raw = __dsub_rn(raw, terms[i]);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = raw;
+    out[1] = __ddiv_rn(raw, log(static_cast<double>(k)));
+  }
+}
+
+int grid_for(uint64_t work_items, int per_block, int num_sms, int blocks_per_sm) {
+  const uint64_t need = (work_items + per_block - 1) / per_block;
+  const uint64_t cap = static_cast<uint64_t>(num_sms) * blocks_per_sm;
+  return static_cast<int>(need < 1 ? 1 : (need < cap ? need : cap));
+}
+
+int stride_mode(uint64_t stride) {
+  if (stride == 1) return 0;
+  if ((stride & (stride - 1)) == 0) return 1;
+  return 2;
+}
+
+}  // namespace
+
+cudaError_t launch_range_init(double* d_range, cudaStream_t s) {
+  range_init_kernel<<<1, 1, 0, s>>>(d_range);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_minmax_f32(const float* v, uint64_t n, uint64_t g0, uint64_t stride,
+                              double* d_range, int num_sms, cudaStream_t s, int* launches) {
+  if (n == 0) return cudaSuccess;
+  const int grid = grid_for(n / 4 + 1, kThreads * 4, num_sms, 4);
+  switch (stride_mode(stride)) {
+    case 0: minmax_f32_kernel<0><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range); break;
+    case 1: minmax_f32_kernel<1><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range); break;
+    default: minmax_f32_kernel<2><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range); break;
+  }
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_minmax_f64(const double* v, uint64_t n, uint64_t g0, uint64_t stride,
+                              double* d_range, int num_sms, cudaStream_t s, int* launches) {
+  if (n == 0) return cudaSuccess;
+  const int grid = grid_for(n, kThreads * 4, num_sms, 4);
+  switch (stride_mode(stride)) {
+    case 0: minmax_f64_kernel<0><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range); break;
+    case 1: minmax_f64_kernel<1><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range); break;
+    default: minmax_f64_kernel<2><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range); break;
+  }
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_histogram_f32(const float* v, uint64_t n, uint64_t g0,
+                                 const cl_hist_spec& spec, const double* d_range,
+                                 uint64_t* d_counts, int num_sms, cudaStream_t s,
+                                 int* launches) {
+  if (n == 0) return cudaSuccess;
+  const uint64_t stride = spec.sample_stride;
+  const int k = spec.bin_count;
+  auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
+  const int mode = stride_mode(stride);
+  if (k <= 256 && n >= 4096) {
+    static bool attr_set[3] = {false, false, false};
+    const uint64_t chunks = n / kChunkFloats + 1;
+    const int grid = static_cast<int>(chunks < static_cast<uint64_t>(num_sms) ? chunks : num_sms);
+    auto launch = [&](auto kern) {
+      if (!attr_set[mode]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kHistSmem));
+        attr_set[mode] = true;
+      }
+      kern<<<grid, kHistThreads, kHistSmem, s>>>(v, n, g0, stride, spec.range_mode,
+                                                 spec.fixed_lo, spec.fixed_hi, k, d_range,
+                                                 counts);
+    };
+    if (mode == 0) launch(hist_f32_lane_kernel<0>);
+    else if (mode == 1) launch(hist_f32_lane_kernel<1>);
+    else launch(hist_f32_lane_kernel<2>);
+  } else {
+    const int use_smem = k <= 16384 ? 1 : 0;
+    const size_t smem = use_smem ? static_cast<size_t>(k) * 4 : 0;
+    const int grid = grid_for(n, kThreads * 8, num_sms, 4);
+    if (smem > 48 * 1024) {
+      cudaFuncSetAttribute(hist_atomic_kernel<float, 0>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      cudaFuncSetAttribute(hist_atomic_kernel<float, 1>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      cudaFuncSetAttribute(hist_atomic_kernel<float, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    }
+    if (mode == 0)
+      hist_atomic_kernel<float, 0><<<grid, kThreads, smem, s>>>(
+          v, n, g0, stride, spec.range_mode, spec.fixed_lo, spec.fixed_hi, k, d_range, counts,
+          use_smem);
+    else if (mode == 1)
+      hist_atomic_kernel<float, 1><<<grid, kThreads, smem, s>>>(
+          v, n, g0, stride, spec.range_mode, spec.fixed_lo, spec.fixed_hi, k, d_range, counts,
+          use_smem);
+    else
+      hist_atomic_kernel<float, 2><<<grid, kThreads, smem, s>>>(
+          v, n, g0, stride, spec.range_mode, spec.fixed_lo, spec.fixed_hi, k, d_range, counts,
+          use_smem);
+  }
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_histogram_f64(const double* v, uint64_t n, uint64_t g0,
+                                 const cl_hist_spec& spec, const double* d_range,
+                                 uint64_t* d_counts, int num_sms, cudaStream_t s,
+                                 int* launches) {
+  if (n == 0) return cudaSuccess;
+  const uint64_t stride = spec.sample_stride;
+  const int k = spec.bin_count;
+  auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
+  const int use_smem = k <= 16384 ? 1 : 0;
+  const size_t smem = use_smem ? static_cast<size_t>(k) * 4 : 0;
+  const int grid = grid_for(n, kThreads * 8, num_sms, 4);
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(hist_atomic_kernel<double, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         65536);
+    cudaFuncSetAttribute(hist_atomic_kernel<double, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         65536);
+    cudaFuncSetAttribute(hist_atomic_kernel<double, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         65536);
+  }
+  const int mode = stride_mode(stride);
+  if (mode == 0)
+    hist_atomic_kernel<double, 0><<<grid, kThreads, smem, s>>>(
+        v, n, g0, stride, spec.range_mode, spec.fixed_lo, spec.fixed_hi, k, d_range, counts,
+        use_smem);
+  else if (mode == 1)
+    hist_atomic_kernel<double, 1><<<grid, kThreads, smem, s>>>(
+        v, n, g0, stride, spec.range_mode, spec.fixed_lo, spec.fixed_hi, k, d_range, counts,
+        use_smem);
+  else
+    hist_atomic_kernel<double, 2><<<grid, kThreads, smem, s>>>(
+        v, n, g0, stride, spec.range_mode, spec.fixed_lo, spec.fixed_hi, k, d_range, counts,
+        use_smem);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decide(const uint64_t* d_counts, const double* d_range,
+                          const cl_hist_spec& spec, uint64_t n_samples, const cl_rule_spec& rule,
+                          uint64_t seq_len, const cl_features* features, cl_decision* d_out,
+                          cudaStream_t s) {
+  DecideArgs a{};
+  a.counts = reinterpret_cast<const unsigned long long*>(d_counts);
+  a.range = d_range;
+  a.k = spec.bin_count;
+  a.epsilon = spec.epsilon;
+  a.range_mode = spec.range_mode;
+  a.fixed_lo = spec.fixed_lo;
+  a.fixed_hi = spec.fixed_hi;
+  a.n_samples = n_samples;
+  a.rule = rule;
+  a.seq_len = seq_len;
+  a.features_mode = features ? 1 : 0;
+  if (features) a.f = *features;
+  decide_kernel<<<1, kThreads, 0, s>>>(a, d_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_entropy_from_masses(const double* d_masses, int k, double eps, double* d_out,
+                                       cudaStream_t s) {
+  entropy_masses_kernel<<<1, kThreads, 0, s>>>(d_masses, k, eps, d_out);
+  return cudaGetLastError();
+}
+
+}  // namespace cl

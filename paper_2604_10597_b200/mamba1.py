@@ -1,0 +1,207 @@
+"""Device path of the COREY prefill: entropy -> rule -> fused Mamba-1 scan on the B200.
+
+Tensors are torch CUDA tensors (torch is used for device memory, streams and
+torch.distributed only).  Every stage is a kernel in libchunklab_b200.so launched on
+torch's current stream; no stage synchronises with the host, so the chunk chosen by
+the device rule flows into the scan through device memory (the host sync of the
+paper's Python hook, is gone).
+
+  selective_scan_fn   mamba_ssm's public interface + chunk_size
+  Prefill             entropy (K-bin, entropy.hpp) -> policy (chunk.hpp) -> scan
+  ShardedPrefill      the same over torch.distributed ranks: rows of (batch*dim) are
+                      sharded, MAX-allreduce of the range and SUM-allreduce of the
+                      K counts are the only collectives
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _lib
+from ._lib import Context, InvalidInput
+from .chunklab import (CalibrationRef, ChunkBounds, ChunkDecision, EntropyEstimate,
+                       HistogramSpec, SchedulerPolicy, rule_spec)
+
+_VARIANTS = {"auto": _lib.CL_SCAN_AUTO, "rowseq_tma": _lib.CL_SCAN_ROWSEQ_TMA,
+             "generic": _lib.CL_SCAN_GENERIC}
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _check_f32(name, t, device):
+    if t is None:
+        return
+    if not t.is_cuda or t.device != device:
+        raise InvalidInput(f"{name} must be a CUDA tensor on {device}")
+    if t.dtype != torch.float32:
+        raise InvalidInput(f"{name} must be float32")
+    if not t.is_contiguous():
+        raise InvalidInput(f"{name} must be contiguous")
+
+
+def _mamba_args(u, delta, A, B, C_, D, z, delta_bias, h0, out, h_last, delta_softplus):
+    batch, dim, L = u.shape
+    N = A.shape[1]
+    dev = u.device
+    for name, t in (("u", u), ("delta", delta), ("A", A), ("B", B), ("C", C_), ("D", D),
+                    ("z", z), ("delta_bias", delta_bias), ("h0", h0), ("out", out),
+                    ("h_last", h_last)):
+        _check_f32(name, t, dev)
+    if tuple(delta.shape) != (batch, dim, L) or (z is not None and tuple(z.shape) != (batch, dim, L)):
+        raise InvalidInput("shape mismatch")
+    if tuple(A.shape) != (dim, N) or tuple(B.shape) != (batch, N, L) or tuple(C_.shape) != (batch, N, L):
+        raise InvalidInput("shape mismatch")
+    for t in (D, delta_bias):
+        if t is not None and t.numel() != dim:
+            raise InvalidInput("shape mismatch")
+    a = _lib.cl_mamba1_args()
+    a.u, a.delta, a.A, a.B, a.C = _ptr(u), _ptr(delta), _ptr(A), _ptr(B), _ptr(C_)
+    a.D, a.z, a.delta_bias, a.h0 = _ptr(D), _ptr(z), _ptr(delta_bias), _ptr(h0)
+    a.out, a.h_last = _ptr(out), _ptr(h_last)
+    a.batch, a.dim, a.seq_len, a.d_state = batch, dim, L, N
+    a.delta_softplus = int(bool(delta_softplus))
+    return a
+
+
+def selective_scan_fn(u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_softplus=False,
+                      return_last_state=False, chunk_size: int = 512, h0=None,
+                      variant: str = "auto", decision: Optional[torch.Tensor] = None,
+                      out: Optional[torch.Tensor] = None):
+    """mamba_ssm.selective_scan_fn semantics, fp32, on the fused sm_100a kernel.
+
+    u, delta, z: (batch, dim, L); A: (dim, N); B, C: (batch, N, L); D, delta_bias: (dim,).
+    chunk_size: L-segment length of the scan's work decomposition (the paper's runtime
+    chunk).  `decision` (a device cl_decision buffer from Prefill) makes
+    the kernel read the chunk from device memory instead.
+    """
+    ctx = Context.get(u.device.index)
+    if out is None:
+        out = torch.empty_like(u)
+    h_last = None
+    if return_last_state:
+        h_last = torch.empty(u.shape[0], u.shape[1], A.shape[1], device=u.device,
+                             dtype=torch.float32)
+    a = _mamba_args(u, delta, A, B, C, D, z, delta_bias, h0, out, h_last, delta_softplus)
+    ctx.call("cl_selective_scan_f32", C_byref(a), _ptr(decision), int(chunk_size),
+             _VARIANTS[variant], _stream_ptr(u.device))
+    return (out, h_last) if return_last_state else out
+
+
+def C_byref(x):
+    return C.byref(x)
+
+
+@dataclass
+class PrefillResult:
+    out: torch.Tensor
+    h_last: Optional[torch.Tensor]
+    decision_buf: torch.Tensor  # raw cl_decision bytes on the device
+
+    def decision(self) -> "DecisionRecord":
+        """Sync point: copy the device decision back; raise deferred device errors."""
+        return read_decision(self.decision_buf)
+
+
+@dataclass
+class DecisionRecord:
+    decision: ChunkDecision
+    entropy: EntropyEstimate
+    lo: float
+    hi: float
+
+
+def read_decision(buf: torch.Tensor) -> DecisionRecord:
+    ctx = Context.get(buf.device.index)
+    d = _lib.cl_decision()
+    ctx.call("cl_decision_check", buf.data_ptr(), C.byref(d), _stream_ptr(buf.device))
+    dec = ChunkDecision(chunk=int(d.chunk), r=float(d.r), source_policy=_lib.source_tag(d.source),
+                        signal_nats=float(d.signal_nats), margin=float(d.margin))
+    ent = EntropyEstimate(raw_nats=float(d.raw_nats), normalized=float(d.normalized),
+                          bin_count=int(d.bin_count), sample_count=int(d.sample_count))
+    return DecisionRecord(dec, ent, float(d.lo), float(d.hi))
+
+
+class Prefill:
+    """One Mamba-1 layer's COREY prefill on one GPU:
+    K-bin entropy of u -> scheduler policy -> chunked fused scan, stream-ordered.
+
+    policy=None uses the bare calibrated rule (select_chunk); otherwise any device
+    policy (Static / FullHistogram / SampledHistogram / Guarded / LearnedTable).
+    """
+
+    def __init__(self, spec: HistogramSpec = None, policy: Optional[SchedulerPolicy] = None,
+                 bounds: ChunkBounds = None, cal: CalibrationRef = None, device=None):
+        self.spec = spec or HistogramSpec()
+        self.bounds = bounds or ChunkBounds()
+        self.cal = cal or CalibrationRef.log_k(self.spec.bin_count)
+        self.policy = policy
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        self.ctx = Context.get(self.device.index)
+        self.cspec = self.spec.to_c()
+        self.rule = rule_spec(policy, self.bounds, self.cal)
+        self.ctx.call("cl_validate_hist_spec", C.byref(self.cspec))
+        self.ctx.call("cl_validate_rule", C.byref(self.rule))
+        k = self.spec.bin_count
+        self.counts = torch.zeros(k, dtype=torch.int64, device=self.device)
+        self.range = torch.zeros(4, dtype=torch.float64, device=self.device)
+        self.decision_buf = torch.zeros(C.sizeof(_lib.cl_decision), dtype=torch.uint8,
+                                        device=self.device)
+
+    # -- stages (exposed for the sharded path and for per-stage timing) --
+    def stage_minmax(self, u_flat: torch.Tensor, global_offset: int = 0, init: bool = True):
+        s = _stream_ptr(self.device)
+        if init:
+            self.ctx.call("cl_range_init", self.range.data_ptr(), s)
+        self.ctx.call("cl_minmax_f32", u_flat.data_ptr(), u_flat.numel(), int(global_offset),
+                      int(self.spec.sample_stride), self.range.data_ptr(), s)
+
+    def stage_histogram(self, u_flat: torch.Tensor, global_offset: int = 0, zero: bool = True):
+        s = _stream_ptr(self.device)
+        if zero:
+            self.ctx.call("cl_counts_zero", self.counts.data_ptr(), int(self.spec.bin_count), s)
+        self.ctx.call("cl_histogram_f32", u_flat.data_ptr(), u_flat.numel(), int(global_offset),
+                      C.byref(self.cspec), self.range.data_ptr(), self.counts.data_ptr(), s)
+
+    def stage_decide(self, n_samples_total: int, seq_len: int):
+        self.ctx.call("cl_decide", self.counts.data_ptr(), self.range.data_ptr(),
+                      C.byref(self.cspec), int(n_samples_total), C.byref(self.rule),
+                      int(seq_len), self.decision_buf.data_ptr(), _stream_ptr(self.device))
+
+    def stage_scan(self, u, delta, A, B, C, D=None, z=None, delta_bias=None,
+                   delta_softplus=True, out=None, return_last_state=False, h0=None,
+                   variant="auto"):
+        return selective_scan_fn(u, delta, A, B, C, D, z, delta_bias, delta_softplus,
+                                 return_last_state, 0, h0, variant, self.decision_buf, out)
+
+    def n_samples(self, n_values: int) -> int:
+        st = int(self.spec.sample_stride)
+        return (n_values + st - 1) // st
+
+    def __call__(self, u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_softplus=True,
+                 out=None, return_last_state=False, h0=None) -> PrefillResult:
+        if u.numel() == 0:
+            raise InvalidInput("no samples")
+        uf = u.reshape(-1)
+        self.stage_minmax(uf)
+        self.stage_histogram(uf)
+        self.stage_decide(self.n_samples(uf.numel()), u.shape[-1])
+        res = self.stage_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, out,
+                              return_last_state, h0)
+        if return_last_state:
+            o, h = res
+        else:
+            o, h = res, None
+        return PrefillResult(o, h, self.decision_buf)
+
+    def decision(self) -> DecisionRecord:
+        return read_decision(self.decision_buf)

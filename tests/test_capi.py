@@ -1,0 +1,59 @@
+"""CPU: the C-ABI library loads and exports every symbol include/*.h declares; the
+Python binding types every one of them; no compute call is made (no GPU here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2604_10597_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "chunklab_capi.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(cl_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_abi():
+    names = declared_functions()
+    assert "cl_prefill_f32" in names and "cl_scan_f64_host" in names
+    assert len(names) >= 20
+
+
+def test_library_exports_every_declared_symbol():
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2604_10597_b200 import build
+        build.build()
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    exported = set(re.findall(r" T (cl_\w+)", out))
+    assert set(declared_functions()) <= exported
+
+
+def test_binding_types_every_symbol():
+    assert set(_lib.SIGNATURES) == set(declared_functions())
+    lib = _lib.load_library()
+    assert lib.cl_abi_version() == 1
+
+
+def test_no_gpu_fails_loudly():
+    """Without a device the context refuses to start: there is no CPU fallback."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(_lib.DeviceError, match="no CPU fallback"):
+        _lib.Context(0)
+
+
+def test_kernels_are_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out

@@ -1,0 +1,142 @@
+"""GPU: the whole prefill hot path (entropy -> rule -> scan) with no host sync,
+vs the oracle; deferred device errors; guarded / learned-table policies."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_10597_b200 as cl
+from paper_2604_10597_b200.mamba1 import Prefill
+from tests._helpers import assert_close_normwise, mamba_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x, cuda):
+    return {k: torch.from_numpy(np.ascontiguousarray(v)).to(cuda) for k, v in x.items()}
+
+
+def expected_chunk(port, u32, k, stride, bounds, h_ref):
+    counts, lo, hi, n = port.histogram(u32.reshape(-1), k, 1e-8, stride)
+    raw, _ = port.entropy(counts.astype(np.float64) * (1.0 / n))
+    return port.select_chunk(raw, bounds[0], bounds[1], h_ref)[0], raw
+
+
+def test_prefill_rule_and_scan(cuda, port):
+    x = mamba_inputs(1, 2, 128, 16, 512)
+    d = dev(x, cuda)
+    pf = Prefill(cl.HistogramSpec(), device=cuda)
+    res = pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"], True,
+             return_last_state=True)
+    rec = res.decision()
+    chunk, raw = expected_chunk(port, x["u"], 256, 1, (32, 512), np.log(256))
+    assert rec.decision.chunk == chunk and rec.decision.source_policy == "rule"
+    assert rec.entropy.raw_nats == pytest.approx(raw, rel=1e-13, abs=0)
+    yr, hr = port.mamba1(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"],
+                         x["delta_bias"], True)
+    assert_close_normwise(res.out.cpu().numpy().reshape(-1, 512), yr, 1e-5)
+    assert_close_normwise(res.h_last.cpu().numpy().reshape(-1, 16), hr, 1e-5)
+
+
+@pytest.mark.parametrize("dist", ["uniform", "sparse"])
+def test_prefill_decision_follows_distribution(cuda, port, dist):
+    """Perturbation sweep (fixtures.hpp:40-47): the device rule picks the chunk the
+    reference rule picks for uniform / sparse activations."""
+    x = mamba_inputs(2, 1, 256, 16, 1024)
+    rng = np.random.default_rng(4)
+    if dist == "uniform":
+        x["u"] = rng.uniform(0, 1, x["u"].shape).astype(np.float32)
+    else:
+        x["u"] = np.where(rng.uniform(size=x["u"].shape) < 0.02, x["u"], 0).astype(np.float32)
+    d = dev(x, cuda)
+    pf = Prefill(cl.HistogramSpec(), None, cl.ChunkBounds(32, 512), cl.CalibrationRef.legacy(),
+                 device=cuda)
+    pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"], True)
+    rec = pf.decision()
+    chunk, _ = expected_chunk(port, x["u"], 256, 1, (32, 512), 8.0)
+    assert rec.decision.chunk == chunk
+
+
+def test_guarded_sampled_policy(cuda, port):
+    """C4 policy: Guarded{inner = sampled histogram stride 8, safe 512, min_delta 2}."""
+    x = mamba_inputs(3, 1, 256, 16, 1024)
+    d = dev(x, cuda)
+    inner = cl.SchedulerPolicy(cl.SampledHistogramPolicy(8), [128, 256, 512, 1024, 2048])
+    policy = cl.SchedulerPolicy(cl.GuardedPolicy(inner, 512, 2), [128, 256, 512, 1024, 2048])
+    for bounds, expect in [(cl.ChunkBounds(128, 2048), None), (cl.ChunkBounds(32, 512), 512)]:
+        pf = Prefill(cl.HistogramSpec(sample_stride=8), policy, bounds,
+                     cl.CalibrationRef.log_k(256), device=cuda)
+        res = pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"])
+        rec = res.decision()
+        counts, lo, hi, n = port.histogram(x["u"].reshape(-1), 256, 1e-8, 8)
+        raw, _ = port.entropy(counts.astype(np.float64) * (1.0 / n))
+        from oracle import oracle as O
+        p = O.Policy()
+        p.kind, p.inner_kind, p.safe_chunk, p.min_delta_buckets = 5, 3, 512, 2
+        p.n_buckets = 5
+        for i, b in enumerate([128, 256, 512, 1024, 2048]):
+            p.buckets[i] = b
+        f = O.Features(0, 0.0, 1, raw, 0, 0)
+        c, *_ = port.schedule(p, f, bounds.c_min, bounds.c_max, np.log(256))
+        assert rec.decision.chunk == c
+        if expect is not None:
+            assert c == expect
+        yr, _ = port.mamba1(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"],
+                            x["delta_bias"], True, rows=(0, 8))
+        assert_close_normwise(res.out.cpu().numpy().reshape(-1, 1024)[:8], yr, 1e-5)
+
+
+def test_learned_table_policy(cuda):
+    x = mamba_inputs(4, 1, 64, 16, 256)
+    d = dev(x, cuda)
+    pol = cl.SchedulerPolicy(cl.LearnedTablePolicy(50, 128, 512), [128, 256, 512])
+    pf = Prefill(cl.HistogramSpec(), pol, cl.ChunkBounds(128, 512), device=cuda)
+    pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"])
+    rec = pf.decision()
+    assert rec.decision.chunk == 512 and rec.decision.source_policy == "learned_table"
+
+
+def test_constant_activation_defers_signal_error(cuda):
+    """SURVEY.md finding 7: constant u -> H = -log(1+eps) < 0 -> 'signal must be >= 0',
+    raised at the decision sync point; the scan kernel writes nothing."""
+    x = mamba_inputs(5, 1, 32, 16, 64)
+    x["u"] = np.full_like(x["u"], 3.0)
+    d = dev(x, cuda)
+    out = torch.full_like(d["u"], 7.0)
+    pf = Prefill(cl.HistogramSpec(), device=cuda)
+    pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"], out=out)
+    with pytest.raises(cl.InvalidInput, match="^signal must be >= 0$"):
+        pf.decision()
+    assert (out == 7.0).all()
+
+
+def test_nonfinite_activation_defers_error(cuda):
+    x = mamba_inputs(6, 1, 32, 16, 64)
+    x["u"][0, 3, 17] = np.nan
+    d = dev(x, cuda)
+    pf = Prefill(cl.HistogramSpec(), device=cuda)
+    pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"])
+    with pytest.raises(cl.InvalidInput, match="^non-finite input$"):
+        pf.decision()
+
+
+def test_no_host_sync_in_prefill(cuda):
+    """The prefill path is capturable in a CUDA graph (proves no host sync / no
+    host-side decision between entropy and scan)."""
+    x = mamba_inputs(7, 1, 64, 16, 256)
+    d = dev(x, cuda)
+    pf = Prefill(cl.HistogramSpec(), device=cuda)
+    out = torch.empty_like(d["u"])
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"], out=out)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    ref = out.clone()
+    g = torch.cuda.CUDAGraph()
+    out.zero_()
+    with torch.cuda.graph(g):
+        pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"], out=out)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
