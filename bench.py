@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""COREY hot-path benchmark: K-bin entropy -> chunk rule -> fused Mamba-1 scan on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C3] [--scaling weak|strong] [--no-e2e] [--no-cpu]
+
+One "step" = one layer's prefill over the configured workload (BASELINE.json
+configs[2], "C3": B=8, L=8192, d_inner=4096, N=16 per rank): range_init ->
+minmax -> histogram -> [allreduce MAX range, allreduce SUM counts when N>1] ->
+device decision -> chunked fused scan, all stream-ordered with no host sync.
+Inputs are synthetic, fp32, resident in HBM, each tensor (1.07 GB) larger than
+the 126 MB L2, so no L2 flush is needed between iterations.
+
+Prints ONE JSON line on rank 0 (contract in the task statement): value = whole-job
+tokens/s (a token = one (b, l) position through all d_inner channels),
+`roofline` for the dominant kernel (the scan), `cpu_baseline`, `e2e` (the same
+metric through the public API with pinned host buffers and H2D/D2H inside the
+timed region), `clocks`, `gpu_launches`.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref: the
+reference headers compiled in place; else the oracle port) on the box's host
+cores over a bounded sample of the same workload (one batch of C3 per step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "selective-scan tokens/s & HBM GB/s (% roofline) at 1/2/4/8 B200 vs CPU ref"
+CONFIGS = {
+    # name: (batch per rank, dim, seq_len, d_state, description)
+    "C1": (1, 1536, 2048, 16, "Mamba-130M-shaped layer B=1 L=2048 d_inner=1536 N=16"),
+    "C2": (1, 2048, 4096, 16, "Mamba-370M-shaped layer B=1 L=4096 d_inner=2048 N=16"),
+    "C3": (8, 4096, 8192, 16, "Mamba-1.4B-shaped layer B=8 L=8192 d_inner=4096 N=16"),
+    "C4": (16, 5120, 16384, 16, "Mamba-2.8B-shaped layer B=16 L=16384 d_inner=5120 N=16"),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def algorithmic_bytes(batch, dim, L, N, stride=1):
+    """Per SURVEY.md 8d / DESIGN.md: per token 8*D (entropy: two reads of u) +
+    16*D (scan: read u, delta, z; write out) + 8*N (read B, C)."""
+    tokens = batch * L
+    return dict(entropy=tokens * 8 * dim, scan=tokens * (16 * dim + 8 * N),
+                total=tokens * (24 * dim + 8 * N), tokens=tokens)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.proc = None
+        self.lines = []
+        self.dev = device_index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- data
+def make_inputs(torch, device, batch, dim, L, N, seed):
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    f32 = dict(device=device, dtype=torch.float32)
+    u = torch.randn(batch, dim, L, generator=g, **f32)
+    delta = torch.randn(batch, dim, L, generator=g, **f32).mul_(0.1)
+    dt = torch.exp(torch.empty(dim, **f32).uniform_(np.log(1e-3), np.log(1e-1), generator=g))
+    delta_bias = torch.log(torch.expm1(dt))
+    A = -(torch.arange(1, N + 1, **f32)[None, :]) * (
+        1 + 0.1 * torch.empty(dim, N, **f32).uniform_(-1, 1, generator=g))
+    B = torch.randn(batch, N, L, generator=g, **f32)
+    C = torch.randn(batch, N, L, generator=g, **f32)
+    D = 1 + 0.1 * torch.randn(dim, generator=g, **f32)
+    z = torch.randn(batch, dim, L, generator=g, **f32)
+    return dict(u=u, delta=delta, A=A.contiguous(), B=B, C=C, D=D, z=z, delta_bias=delta_bias)
+
+
+# ----------------------------------------------------------------- reference arm
+def cpu_reference_step(lib_kind, x_host, dim, L, N, threads, ref, port):
+    """One bounded sample: entropy over one batch's u + rule + Mamba-1 scan of that batch,
+    through the reference's own functions (oracle/_ref) or the oracle port."""
+    u = x_host["u"]  # (1, dim, L) float32
+    t0 = time.perf_counter()
+    if lib_kind == "reference":
+        masses, lo, hi, n = ref.histogram_masses(u.reshape(-1), 256, 1e-8, 1)
+        raw, _ = ref.entropy(masses)
+        chunk, _ = ref.select_chunk(raw, 32, 512, np.log(256.0))
+        y, h = ref.mamba1_f32(u, x_host["delta"], x_host["A"], x_host["B"], x_host["C"],
+                              x_host["D"], x_host["z"], x_host["delta_bias"], True,
+                              rows=(0, dim), threads=threads)
+    else:
+        counts, lo, hi, n = port.histogram(u.reshape(-1), 256, 1e-8, 1)
+        raw, _ = port.entropy(counts.astype(np.float64) / n)
+        chunk, _ = port.select_chunk(raw, 32, 512, np.log(256.0))
+        y = _port_mamba_threaded(port, x_host, dim, L, N, threads)
+    dt = time.perf_counter() - t0
+    return dt, chunk, raw
+
+
+def _port_mamba_threaded(port, x, dim, L, N, threads):
+    from concurrent.futures import ThreadPoolExecutor
+    per = (dim + threads - 1) // threads
+    def work(i):
+        r0, r1 = i * per, min(dim, (i + 1) * per)
+        if r0 >= r1:
+            return None
+        return port.mamba1(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"],
+                           x["delta_bias"], True, rows=(r0, r1))
+    with ThreadPoolExecutor(threads) as ex:
+        return list(ex.map(work, range(threads)))
+
+
+def sample_host_inputs(cfg, seed=0):
+    import torch
+    batch, dim, L, N, _ = CONFIGS[cfg]
+    x = make_inputs(torch, "cpu", 1, dim, L, N, seed)
+    return {k: v.numpy() for k, v in x.items()}
+
+
+def reference_arm(args):
+    from oracle import oracle as O
+    batch, dim, L, N, desc = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    kind = "reference" if O.reference_available() else "port"
+    ref = O.Reference() if kind == "reference" else None
+    port = O.Port()
+    x = sample_host_inputs(args.config)
+    for _ in range(args.warmup):
+        cpu_reference_step(kind, x, dim, L, N, threads, ref, port)
+    times = []
+    chunk = raw = None
+    for _ in range(args.steps):
+        dt, chunk, raw = cpu_reference_step(kind, x, dim, L, N, threads, ref, port)
+        times.append(dt)
+    t = sum(times) / len(times)
+    tokens_per_step = L  # one batch of the workload: L positions x all d_inner channels
+    value = tokens_per_step / t
+    sample = (f"1 of {batch} batches of {args.config} per step ({dim} channels x L={L}, N={N}): "
+              f"entropy K=256 over that batch's u + calibrated rule + fp64 Mamba-1 scan "
+              f"(reference scan_sequential under the SURVEY finding-1 mapping), {threads} threads")
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (torch.randn, seed 0)",
+            "config": {"workload": f"{args.config}: {desc}", "sample": sample,
+                       "policy": "calibrated rule log K, bounds [32,512]"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "chunk": chunk, "raw_nats": raw}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--chunk-policy", default="rule", choices=["rule", "guarded", "static512"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    import paper_2604_10597_b200 as cl
+    from paper_2604_10597_b200.mamba1 import Prefill
+
+    batch, dim, L, N, desc = CONFIGS[args.config]
+    if args.scaling == "strong" and world > 1:
+        assert batch % world == 0, "strong scaling shards whole batches"
+        batch //= world
+    global_batch = batch * world
+    x = make_inputs(torch, device, batch, dim, L, N, seed=1234 + rank)
+    out = torch.empty_like(x["u"])
+    h_last = torch.empty(batch, dim, N, device=device)
+
+    spec = cl.HistogramSpec(bin_count=256, epsilon=1e-8, sample_stride=1)
+    bounds = cl.ChunkBounds(32, 512)
+    policy = None
+    if args.chunk_policy == "guarded":
+        spec.sample_stride = 8
+        inner = cl.SchedulerPolicy(cl.SampledHistogramPolicy(8), [128, 256, 512, 1024, 2048])
+        policy = cl.SchedulerPolicy(cl.GuardedPolicy(inner, 512, 2), [128, 256, 512, 1024, 2048])
+        bounds = cl.ChunkBounds(128, 2048)
+    elif args.chunk_policy == "static512":
+        policy = cl.SchedulerPolicy(cl.StaticPolicy(512), [128, 256, 512, 1024, 2048])
+    pf = Prefill(spec, policy, bounds, cl.CalibrationRef.log_k(256), device=device)
+    n_local = batch * dim * L
+    g0 = rank * n_local  # global flat offset of this rank's rows (stride sampling)
+    n_total = pf.n_samples(n_local * world)
+    uf = x["u"].reshape(-1)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record()
+        pf.stage_minmax(uf, g0)
+        if world > 1:
+            dist.all_reduce(pf.range, op=dist.ReduceOp.MAX)
+        if ev:
+            ev[1].record()
+        pf.stage_histogram(uf, g0)
+        if world > 1:
+            dist.all_reduce(pf.counts, op=dist.ReduceOp.SUM)
+        if ev:
+            ev[2].record()
+        pf.stage_decide(n_total, L)
+        if ev:
+            ev[3].record()
+        pf.stage_scan(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"],
+                      x["delta_bias"], True, out, True)
+        if ev:
+            ev[4].record()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    rec = pf.decision()  # sync point outside the timed region; raises on device errors
+
+    # per-stage CUDA events on the launching stream, read after the timed loop
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    launches0 = pf.ctx.launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        start.record()
+        for i in range(args.steps):
+            step(evs[i])
+        stop.record()
+        torch.cuda.synchronize()
+    stage_ms = {"minmax": [e[0].elapsed_time(e[1]) for e in evs],
+                "histogram": [e[1].elapsed_time(e[2]) for e in evs],
+                "decide": [e[2].elapsed_time(e[3]) for e in evs],
+                "scan": [e[3].elapsed_time(e[4]) for e in evs]}
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = start.elapsed_time(stop)
+    launches = pf.ctx.launches - launches0
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    tokens_total = global_batch * L
+    value = tokens_total / (ms_per_step / 1e3)
+
+    peak, peak_kind = peaks()
+    ab = algorithmic_bytes(batch, dim, L, N)
+    scan_ms = statistics.mean(stage_ms["scan"])
+    ent_ms = statistics.mean(stage_ms["minmax"]) + statistics.mean(stage_ms["histogram"])
+    scan_gbs = ab["scan"] / (scan_ms / 1e3) / 1e9
+    step_gbs = ab["total"] / (ms_per_step / 1e3) / 1e9  # per rank
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "scan_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            pj = json.load(f)
+        if pj.get("config") == args.config:
+            traffic = pj.get("dram_bytes_per_launch")
+
+    result = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.randn, seeded)",
+        "config": {"workload": f"{args.config}: {desc}", "batch_per_rank": batch,
+                   "global_batch": global_batch, "seq_len": L, "d_inner": dim, "d_state": N,
+                   "bins": 256, "policy": args.chunk_policy, "parallelism": f"rows x{world}",
+                   "l2": "inputs (1.07 GB per tensor) exceed the 126 MB L2; no flush needed"},
+        "hbm_gbs": step_gbs, "roofline_frac_step": step_gbs / peak,
+        "roofline": {"bound": "hbm", "achieved": scan_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": scan_gbs / peak, "traffic": traffic, "kernel": "rowseq_tma_kernel",
+                     "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": ab["scan"]},
+        "stage_ms": {k: statistics.mean(v) for k, v in stage_ms.items()},
+        "entropy_gbs": ab["entropy"] / (ent_ms / 1e3) / 1e9,
+        "chunk": rec.decision.chunk, "raw_nats": rec.entropy.raw_nats,
+        "gpu_launches": launches,
+    }
+    result["clocks"] = clocks.summary()
+
+    # ---- e2e through the public API with host buffers (pinned), H2D/D2H timed
+    if not args.no_e2e:
+        result["e2e"] = e2e_measure(torch, dist, world, device, x, pf, L, global_batch,
+                                    args.e2e_steps)
+    del x, out
+    torch.cuda.empty_cache()
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            from oracle import oracle as O
+            kind = "reference" if O.reference_available() else "port"
+            ref = O.Reference() if kind == "reference" else None
+            port = O.Port()
+            threads = os.cpu_count() or 1
+            xh = sample_host_inputs(args.config)
+            cpu_reference_step(kind, xh, dim, L, N, threads, ref, port)  # warm
+            dt, _, _ = cpu_reference_step(kind, xh, dim, L, N, threads, ref, port)
+            result["cpu_baseline"] = {
+                "value": L / dt, "unit": "tokens/s", "cores": threads, "kind": kind,
+                "sample": f"1 batch of {args.config} ({dim} x {L}): entropy + rule + fp64 "
+                          f"Mamba-1 scan, {threads} threads, {dt:.2f} s"}
+        except Exception as e:  # the baseline must never take the bench down
+            result["cpu_baseline"] = {"value": None, "error": str(e)}
+
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_measure(torch, dist, world, device, x, pf, L, global_batch, steps):
+    """Same metric through the public API (Prefill) with the step's inputs copied
+    from pinned host memory and the output read back, inside the timed region."""
+    host = {k: v.cpu().pin_memory() for k, v in x.items()}
+    h_out = torch.empty_like(host["u"]).pin_memory()
+    dev = {k: torch.empty_like(v) for k, v in x.items()}
+    out = torch.empty_like(x["u"])
+    h2d = sum(v.numel() * 4 for v in host.values())
+    d2h = h_out.numel() * 4
+
+    def one():
+        for k in dev:
+            dev[k].copy_(host[k], non_blocking=True)
+        pf(dev["u"], dev["delta"], dev["A"], dev["B"], dev["C"], dev["D"], dev["z"],
+           dev["delta_bias"], True, out=out)
+        h_out.copy_(out, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        one()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    del dev, out
+    return {"value": global_batch * L / (ms / 1e3), "unit": "tokens/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+            "steps": steps}
+
+
+if __name__ == "__main__":
+    sys.exit(main())
