@@ -198,6 +198,7 @@ int cl_ctx_destroy(cl_ctx* ctx) {
   cudaFree(ctx->d_scratch_decision);
   cudaFree(ctx->d_work);
   cudaFree(ctx->d_carry);
+  cudaFree(ctx->d_bct);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return CL_OK;

@@ -21,6 +21,8 @@ struct cl_ctx {
   size_t work_bytes = 0;
   float* d_carry = nullptr;  // scan segment carry (grown on demand)
   size_t carry_bytes = 0;
+  float* d_bct = nullptr;  // B^T / C^T (b, L, N) for the TMA scan (grown on demand)
+  size_t bct_bytes = 0;
   cudaStream_t own_stream = nullptr;
 };
 

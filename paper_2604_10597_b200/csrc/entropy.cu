@@ -17,6 +17,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "cl_internal.h"
 
@@ -63,11 +64,19 @@ __device__ __forceinline__ int bin_index_exact(double v, double lo, double width
 }
 
 // Per-launch binning parameters, derived on device from the (allreduced) range.
+//
+// Fast path: x' = fma(v, s_f, c_f) approximates X' = (v - lo)*K/width - 0.5, so
+// round-to-nearest(x') = floor(X) = the reference bin, unless x' lies within delta
+// of a half-integer (X within delta of a bin edge).  delta bounds |x' - X'| for
+// |v| <= max(|lo|,|hi|) + width:
+//   |x' - X'| <= u*(|v|*S + |c| + |x'|) + |S - s_f|*|v| + |c - c_f|  (u = 2^-24)
+// and is doubled; near-edge samples take the reference's exact fp64 path.
 struct BinParams {
   double lo, width;  // exact fp64 range
-  float lo_f, s_f;   // fast-path fp32 affine map x = (v - lo_f) * s_f
-  float delta;       // error bound on x; < 0 -> always take the exact path
+  float s_f, c_f;    // fast-path fp32 affine map x' = v*s_f + c_f
+  float thr;         // |x' - round(x')| > thr  <=>  within delta of an edge
   int k;
+  int exact_only;    // fast path unusable (pathological fixed range)
 };
 
 __device__ BinParams make_bin_params(const double* d_range, int range_mode, double fixed_lo,
@@ -84,39 +93,54 @@ __device__ BinParams make_bin_params(const double* d_range, int range_mode, doub
   p.lo = lo;
   p.width = __dsub_rn(hi, lo);
   p.k = k;
+  p.exact_only = 0;
   if (!(p.width > 0.0)) {  // degenerate range: everything in bin 0 (entropy.hpp:89)
-    p.lo_f = 0.f;
     p.s_f = 0.f;
-    p.delta = 0.f;
+    p.c_f = 0.25f;  // x' = 0.25: bin 0, never near an edge
+    p.thr = 0.5f;
     return p;
   }
   const double S = static_cast<double>(k) / p.width;
-  p.lo_f = static_cast<float>(lo);
+  const double c = -(lo * S) - 0.5;
   p.s_f = static_cast<float>(S);
+  p.c_f = static_cast<float>(c);
   const double u = 5.9604644775390625e-08;  // 2^-24
-  // |x - X| <= |X|*((1+u)^3-1) + |lo-lo_f|*S*(1+u)^3 for |X| <= k (see header);
-  // take twice that, plus room for the fp64 reference's own rounding.
-  const double err = static_cast<double>(k) * 3.0001 * u +
-                     fabs(lo - static_cast<double>(p.lo_f)) * S * 1.0001;
-  const double delta = 2.0 * err + static_cast<double>(k) * 1e-12;
-  const bool ok = isfinite(p.lo_f) && isfinite(p.s_f) && p.s_f > 0.f && delta < 0.25;
-  p.delta = ok ? static_cast<float>(delta) * 1.0001f : -1.f;
+  const double M = fmax(fabs(lo), fabs(hi)) + p.width;
+  const double err = u * (M * S + fabs(c) + k + 1.0) + fabs(S - static_cast<double>(p.s_f)) * M +
+                     fabs(c - static_cast<double>(p.c_f));
+  const double delta = 2.0 * err * 1.01 + static_cast<double>(k) * 1e-12;
+  const bool ok = isfinite(p.s_f) && isfinite(p.c_f) && p.s_f > 0.f && delta < 0.2 &&
+                  fabs(c) < 1e6 && M * S < 1e6;
+  p.thr = static_cast<float>(0.5 - delta);
+  p.exact_only = ok ? 0 : 1;
   return p;
 }
 
-// Fast fp32 bin with exact fallback.  Returns the reference bin for v.
-__device__ __forceinline__ int bin_f32(float v, const BinParams& p) {
-  const float x = (v - p.lo_f) * p.s_f;
-  const float xc = fminf(fmaxf(x, -1.0f), static_cast<float>(p.k) + 1.0f);
-  const float t = xc + 12582912.0f;  // 1.5*2^23: round-to-nearest into the mantissa
+// Fast bin: returns n = round(x') and sets *slow when the sample must take the exact
+// path.  FIXED adds clamps (fixed-range outliers) and the huge-value guard.
+template <bool FIXED>
+__device__ __forceinline__ int bin_fast(float v, const BinParams& p, bool* slow) {
+  float x = fmaf(v, p.s_f, p.c_f);
+  bool big = false;
+  if (FIXED) {
+    big = !(fabsf(x) < 2.0e9f);
+    x = fminf(fmaxf(x, -1.25f), static_cast<float>(p.k) + 0.25f);
+  }
+  const float t = x + 12582912.0f;  // 1.5*2^23: round-to-nearest into the mantissa
   const float rn = t - 12582912.0f;
-  const int n = __float_as_int(t) - 0x4B400000;
-  const int fl = n - (xc < rn ? 1 : 0);
-  const bool near = fabsf(xc - rn) <= p.delta && n >= 1 && n <= p.k - 1;
-  const bool slow = near || p.delta < 0.f || !(fabsf(x) < 1e9f);
-  if (__builtin_expect(slow, 0))
-    return bin_index_exact(static_cast<double>(v), p.lo, p.width, p.k);
-  return fl < 0 ? 0 : (fl >= p.k ? p.k - 1 : fl);
+  int n = __float_as_int(t) - 0x4B400000;
+  // written as !(d <= thr) so NaN / inf samples (flagged by minmax) take the exact path
+  *slow = !(fabsf(x - rn) <= p.thr) || big;
+  if (FIXED) n = min(max(n, 0), p.k - 1);
+  return n;
+}
+
+// Bin with exact fallback (any mode).
+__device__ __forceinline__ int bin_f32(float v, const BinParams& p, bool fixed) {
+  bool slow;
+  int n = fixed ? bin_fast<true>(v, p, &slow) : bin_fast<false>(v, p, &slow);
+  if (slow || p.exact_only) n = bin_index_exact(static_cast<double>(v), p.lo, p.width, p.k);
+  return n;
 }
 
 // ---------------------------------------------------------------------------
@@ -277,20 +301,25 @@ __global__ void range_init_kernel(double* range) {
 }
 
 // ---------------------------------------------------------------------------
-// Stage 2: histogram.  K <= 256: lane-private 16-bit counters laid out
-// [bin/2][lane] per warp, so a warp's 32 increments hit 32 distinct banks
-// whatever the bins (no atomics, no conflicts).  Input is streamed through a
-// 4-stage shared-memory ring filled by cp.async.bulk (TMA bulk copies) issued
-// by a dedicated producer warp.
+// Stage 2: histogram, K <= 256.  Each lane owns private 16-bit counters laid out
+// [bin][lane] (16 KB per warp): increments need no atomics.  The per-lane
+// read-modify-write chain is broken into groups of four samples: the four
+// counters are loaded together, and the stores (in order) carry the in-group
+// duplicate count, so the last store to a bin holds the right total.  Input is
+// streamed through a 4-stage shared-memory ring filled by cp.async.bulk (TMA bulk
+// copies) issued by a dedicated producer warp; consumers release slots through an
+// mbarrier.  Counters are flushed (per CTA, then one atomic per bin) before they
+// can overflow.
 // ---------------------------------------------------------------------------
-constexpr int kHistWarps = 8;                     // consumer warps
+constexpr int kHistWarps = 8;                        // consumer warps
 constexpr int kHistThreads = (kHistWarps + 1) * 32;  // + producer warp
 constexpr int kStages = 4;
-constexpr int kChunkFloats = 4096;                // 16 KB per stage
+constexpr int kChunkFloats = 4096;                   // 16 KB per stage
 constexpr int kChunkBytes = kChunkFloats * 4;
-constexpr int kLaneWords = 128;                   // 256 bins / 2 per word
-constexpr size_t kHistSmem =
-    size_t(kHistWarps) * kLaneWords * 32 * 4 + size_t(kStages) * kChunkBytes + 2 * kStages * 8 + 64;
+constexpr int kLaneBins = 256;
+constexpr size_t kCounterBytes = size_t(kHistWarps) * kLaneBins * 32 * 2;  // 128 KB
+constexpr size_t kHistSmem = kCounterBytes + size_t(kStages) * kChunkBytes + kLaneBins * 4 +
+                             2 * kStages * 8 + 64;
 constexpr int kFlushChunks = 4000;  // 16 samples/lane/chunk * 4000 < 65536
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -326,37 +355,40 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
-__device__ __forceinline__ void flush_lane_counters(uint32_t* cnt, int lane, int k,
-                                                    unsigned long long* d_counts) {
+// Sum this warp's lane-private counters into the CTA histogram and clear them.
+__device__ __forceinline__ void flush_warp(uint16_t* cnt, uint32_t* cta_hist, int lane, int k) {
   __syncwarp();
-  const int words = (k + 1) / 2;
-  for (int p = lane; p < words; p += 32) {
-    uint32_t lo = 0, hi = 0;
-#pragma unroll 8
-    for (int s = 0; s < 32; ++s) {
-      const int col = (lane + s) & 31;  // rotated: 32 lanes hit 32 banks
-      const uint32_t w = cnt[p * 32 + col];
-      lo += w & 0xffffu;
-      hi += w >> 16;
+  for (int b = lane; b < k; b += 32) {
+    const uint4* row = reinterpret_cast<const uint4*>(cnt + b * 32);
+    uint32_t sum = 0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const uint4 w = row[(m + (lane >> 1)) & 3];
+      sum += (w.x & 0xffffu) + (w.x >> 16) + (w.y & 0xffffu) + (w.y >> 16) + (w.z & 0xffffu) +
+             (w.z >> 16) + (w.w & 0xffffu) + (w.w >> 16);
     }
-    if (lo) atomicAdd(d_counts + 2 * p, static_cast<unsigned long long>(lo));
-    if (hi && 2 * p + 1 < k) atomicAdd(d_counts + 2 * p + 1, static_cast<unsigned long long>(hi));
+    if (sum) atomicAdd(cta_hist + b, sum);
   }
   __syncwarp();
-  for (int i = lane; i < words * 32; i += 32) cnt[i] = 0;
+  uint4* c4 = reinterpret_cast<uint4*>(cnt);
+  for (int i = lane; i < k * 32 * 2 / 16; i += 32) c4[i] = make_uint4(0, 0, 0, 0);
   __syncwarp();
 }
 
-template <int MODE>
+template <int MODE, bool FIXED>
 __global__ void __launch_bounds__(kHistThreads, 1)
     hist_f32_lane_kernel(const float* __restrict__ v, uint64_t n, uint64_t g0, uint64_t stride,
                          int range_mode, double fixed_lo, double fixed_hi, int k,
                          const double* __restrict__ d_range, unsigned long long* d_counts) {
   extern __shared__ __align__(128) unsigned char smem[];
-  uint32_t* counters = reinterpret_cast<uint32_t*>(smem);
-  unsigned char* ring = smem + size_t(kHistWarps) * kLaneWords * 32 * 4;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(kStages) * kChunkBytes);
+  uint16_t* counters = reinterpret_cast<uint16_t*>(smem);
+  unsigned char* ring = smem + kCounterBytes;
+  uint32_t* cta_hist = reinterpret_cast<uint32_t*>(ring + size_t(kStages) * kChunkBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(cta_hist + kLaneBins);
   uint64_t* empty = full + kStages;
   __shared__ BinParams sp;
 
@@ -369,13 +401,17 @@ __global__ void __launch_bounds__(kHistThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = threadIdx.x; i < kHistWarps * kLaneWords * 32; i += blockDim.x) counters[i] = 0;
+  {
+    uint4* c4 = reinterpret_cast<uint4*>(smem);
+    for (int i = threadIdx.x; i < static_cast<int>(kCounterBytes / 16); i += blockDim.x)
+      c4[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < kLaneBins; i += blockDim.x) cta_hist[i] = 0;
+  }
   __syncthreads();
   const BinParams p = sp;
 
   // Body = 16B-aligned span of v; head/tail (< 4 elements each) go to block 0.
-  const uint64_t head =
-      umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
+  const uint64_t head = umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
   const uint64_t body_n = ((n - head) / 4) * 4;
   const float* body = v + head;
   const uint64_t n_chunks = (body_n + kChunkFloats - 1) / kChunkFloats;
@@ -389,8 +425,7 @@ __global__ void __launch_bounds__(kHistThreads, 1)
         const uint32_t phase = (it / kStages) & 1;
         if (it >= kStages) mbar_wait(empty + s, phase ^ 1);
         const uint64_t off = c * kChunkFloats;
-        const uint32_t bytes =
-            static_cast<uint32_t>(umin64(kChunkFloats, body_n - off) * 4);
+        const uint32_t bytes = static_cast<uint32_t>(umin64(kChunkFloats, body_n - off) * 4);
         mbar_expect_tx(full + s, bytes);
         bulk_g2s(ring + size_t(s) * kChunkBytes, body + off, bytes, full + s);
       }
@@ -399,16 +434,17 @@ __global__ void __launch_bounds__(kHistThreads, 1)
   }
 
   // ---------------- consumer warps ----------------
-  uint32_t* cnt = counters + warp * kLaneWords * 32;
-  auto count = [&](int bin) { cnt[(bin >> 1) * 32 + lane] += 1u << ((bin & 1) << 4); };
+  uint16_t* cnt = counters + warp * kLaneBins * 32 + lane;  // cnt[bin * 32]
 
   if (blockIdx.x == 0 && warp == 0) {
     for (uint64_t i = lane; i < head; i += 32)
-      if (sampled<MODE>(g0 + i, stride)) count(bin_f32(v[i], p));
+      if (sampled<MODE>(g0 + i, stride)) cnt[bin_f32(v[i], p, FIXED) * 32] += 1;
     for (uint64_t i = head + body_n + lane; i < n; i += 32)
-      if (sampled<MODE>(g0 + i, stride)) count(bin_f32(v[i], p));
+      if (sampled<MODE>(g0 + i, stride)) cnt[bin_f32(v[i], p, FIXED) * 32] += 1;
   }
 
+  // byte address of this lane's counter for bin 0; bin b lives at + b*64
+  const uint32_t cbase = smem_u32(counters + warp * kLaneBins * 32 + lane);
   uint32_t it = 0, since_flush = 0;
   for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
     const int s = it % kStages;
@@ -417,31 +453,208 @@ __global__ void __launch_bounds__(kHistThreads, 1)
     const float4* tile = reinterpret_cast<const float4*>(ring + size_t(s) * kChunkBytes);
     const uint64_t off = c * kChunkFloats;
     const int valid4 = static_cast<int>(umin64(kChunkFloats, body_n - off) / 4);
-    float4 q[4];
+    if (MODE == 0 && !FIXED && valid4 == kChunkFloats / 4) {
+      // ---- hot path: full chunk, every element sampled ----
+      float val[16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 q = tile[j * (kHistWarps * 32) + warp * 32 + lane];
+        val[4 * j] = q.x;
+        val[4 * j + 1] = q.y;
+        val[4 * j + 2] = q.z;
+        val[4 * j + 3] = q.w;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+      int bin[16];
+      bool any_slow = p.exact_only != 0;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        bool sl;
+        bin[e] = bin_fast<false>(val[e], p, &sl);
+        any_slow |= sl;
+      }
+      if (__any_sync(0xffffffffu, any_slow)) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          bool sl;
+          bin_fast<false>(val[e], p, &sl);
+          if (sl || p.exact_only)
+            bin[e] = bin_index_exact(static_cast<double>(val[e]), p.lo, p.width, p.k);
+        }
+      }
+      // pairwise read-modify-write: both counters loaded, then stored in order with
+      // the second carrying the pair's duplicate
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const int b0 = bin[2 * g], b1 = bin[2 * g + 1];
+        const uint32_t a0 = cbase + (static_cast<uint32_t>(b0) << 6);
+        const uint32_t a1 = cbase + (static_cast<uint32_t>(b1) << 6);
+        uint32_t v0, v1;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
+        v1 += 1u + (b0 == b1 ? 1u : 0u);
+        v0 += 1u;
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(a0), "h"(static_cast<uint16_t>(v0)) : "memory");
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(a1), "h"(static_cast<uint16_t>(v1)) : "memory");
+      }
+      if (++since_flush == kFlushChunks) {
+        flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+        since_flush = 0;
+      }
+      continue;
+    }
+    float val[16];
+    uint32_t inc = 0;  // bit e: sample e is valid and sampled
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int idx = j * (kHistWarps * 32) + warp * 32 + lane;
-      q[j] = idx < valid4 ? tile[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (idx < valid4) {
+        q = tile[idx];
+        const uint64_t gi = g0 + head + off + static_cast<uint64_t>(idx) * 4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (sampled<MODE>(gi + e, stride)) inc |= 1u << (4 * j + e);
+      }
+      val[4 * j] = q.x;
+      val[4 * j + 1] = q.y;
+      val[4 * j + 2] = q.z;
+      val[4 * j + 3] = q.w;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+
+    int bin[16];
+    uint32_t slow = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      bool sl;
+      bin[e] = bin_fast<FIXED>(val[e], p, &sl);
+      slow |= (sl ? 1u : 0u) << e;
+    }
+    slow &= inc;
+    if (p.exact_only) slow = inc;
+    if (__any_sync(0xffffffffu, slow != 0)) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if (slow & (1u << e)) bin[e] = bin_index_exact(static_cast<double>(val[e]), p.lo, p.width, p.k);
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if (!(inc & (1u << e))) bin[e] = 0;  // +0 on bin 0: harmless in the grouped RMW
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const int b0 = bin[4 * g], b1 = bin[4 * g + 1], b2 = bin[4 * g + 2], b3 = bin[4 * g + 3];
+      const uint32_t i0 = (inc >> (4 * g)) & 1u, i1 = (inc >> (4 * g + 1)) & 1u;
+      const uint32_t i2 = (inc >> (4 * g + 2)) & 1u, i3 = (inc >> (4 * g + 3)) & 1u;
+      const uint32_t v0 = cnt[b0 * 32], v1 = cnt[b1 * 32], v2 = cnt[b2 * 32], v3 = cnt[b3 * 32];
+      const uint32_t n1 = v1 + i1 + (b1 == b0 ? i0 : 0u);
+      const uint32_t n2 = v2 + i2 + (b2 == b0 ? i0 : 0u) + (b2 == b1 ? i1 : 0u);
+      const uint32_t n3 = v3 + i3 + (b3 == b0 ? i0 : 0u) + (b3 == b1 ? i1 : 0u) + (b3 == b2 ? i2 : 0u);
+      cnt[b0 * 32] = static_cast<uint16_t>(v0 + i0);
+      cnt[b1 * 32] = static_cast<uint16_t>(n1);
+      cnt[b2 * 32] = static_cast<uint16_t>(n2);
+      cnt[b3 * 32] = static_cast<uint16_t>(n3);
+    }
+    if (++since_flush == kFlushChunks) {
+      flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+      since_flush = 0;
+    }
+  }
+  flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+  named_bar(1, kHistWarps * 32);
+  for (int b = threadIdx.x; b < k; b += kHistWarps * 32)
+    if (cta_hist[b]) atomicAdd(d_counts + b, static_cast<unsigned long long>(cta_hist[b]));
+}
+
+// Variant (CL_HIST_VARIANT=1): same TMA bulk ring, but per-warp u32 histograms in
+// shared memory updated with shared atomics (ATOMS); 1 KB per warp.
+template <bool FIXED>
+__global__ void __launch_bounds__(kHistThreads, 1)
+    hist_f32_atoms_kernel(const float* __restrict__ v, uint64_t n, int range_mode,
+                          double fixed_lo, double fixed_hi, int k,
+                          const double* __restrict__ d_range, unsigned long long* d_counts) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* ring = smem;
+  uint32_t* whist = reinterpret_cast<uint32_t*>(ring + size_t(kStages) * kChunkBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(whist + kHistWarps * kLaneBins);
+  uint64_t* empty = full + kStages;
+  __shared__ BinParams sp;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    sp = make_bin_params(d_range, range_mode, fixed_lo, fixed_hi, k);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kHistWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < kHistWarps * kLaneBins; i += blockDim.x) whist[i] = 0;
+  __syncthreads();
+  const BinParams p = sp;
+  const uint64_t head = umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
+  const uint64_t body_n = ((n - head) / 4) * 4;
+  const float* body = v + head;
+  const uint64_t n_chunks = (body_n + kChunkFloats - 1) / kChunkFloats;
+  if (warp == kHistWarps) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+        const int s = it % kStages;
+        const uint32_t phase = (it / kStages) & 1;
+        if (it >= kStages) mbar_wait(empty + s, phase ^ 1);
+        const uint64_t off = c * kChunkFloats;
+        const uint32_t bytes = static_cast<uint32_t>(umin64(kChunkFloats, body_n - off) * 4);
+        mbar_expect_tx(full + s, bytes);
+        bulk_g2s(ring + size_t(s) * kChunkBytes, body + off, bytes, full + s);
+      }
+    }
+    return;
+  }
+  uint32_t* h = whist + warp * kLaneBins;
+  if (blockIdx.x == 0 && warp == 0) {
+    for (uint64_t i = lane; i < head; i += 32) atomicAdd(h + bin_f32(v[i], p, FIXED), 1u);
+    for (uint64_t i = head + body_n + lane; i < n; i += 32)
+      atomicAdd(h + bin_f32(v[i], p, FIXED), 1u);
+  }
+  uint32_t it = 0;
+  for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+    const int s = it % kStages;
+    const uint32_t phase = (it / kStages) & 1;
+    mbar_wait(full + s, phase);
+    const float4* tile = reinterpret_cast<const float4*>(ring + size_t(s) * kChunkBytes);
+    const uint64_t off = c * kChunkFloats;
+    const int valid4 = static_cast<int>(umin64(kChunkFloats, body_n - off) / 4);
+    float val[16];
+    bool ok[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = j * (kHistWarps * 32) + warp * 32 + lane;
+      ok[j] = idx < valid4;
+      const float4 q = ok[j] ? tile[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+      val[4 * j] = q.x;
+      val[4 * j + 1] = q.y;
+      val[4 * j + 2] = q.z;
+      val[4 * j + 3] = q.w;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int idx = j * (kHistWarps * 32) + warp * 32 + lane;
-      if (idx < valid4) {
-        const uint64_t gi = g0 + head + off + static_cast<uint64_t>(idx) * 4;
-        if (sampled<MODE>(gi, stride)) count(bin_f32(q[j].x, p));
-        if (sampled<MODE>(gi + 1, stride)) count(bin_f32(q[j].y, p));
-        if (sampled<MODE>(gi + 2, stride)) count(bin_f32(q[j].z, p));
-        if (sampled<MODE>(gi + 3, stride)) count(bin_f32(q[j].w, p));
-      }
-    }
-    if (++since_flush == kFlushChunks) {
-      flush_lane_counters(cnt, lane, k, d_counts);
-      since_flush = 0;
+    for (int e = 0; e < 16; ++e) {
+      if (!ok[e / 4]) continue;
+      bool sl;
+      int b = bin_fast<FIXED>(val[e], p, &sl);
+      if (sl || p.exact_only) b = bin_index_exact(static_cast<double>(val[e]), p.lo, p.width, p.k);
+      atomicAdd(h + b, 1u);
     }
   }
-  flush_lane_counters(cnt, lane, k, d_counts);
+  named_bar(1, kHistWarps * 32);
+  for (int b = threadIdx.x; b < k; b += kHistWarps * 32) {
+    uint32_t sum = 0;
+    for (int w = 0; w < kHistWarps; ++w) sum += whist[w * kLaneBins + b];
+    if (sum) atomicAdd(d_counts + b, static_cast<unsigned long long>(sum));
+  }
 }
 
 // K > 256 (or f64 input): shared-memory atomics on a CTA histogram.
@@ -465,7 +678,7 @@ __global__ void __launch_bounds__(kThreads)
     if (!sampled<MODE>(g0 + i, stride)) continue;
     int b;
     if constexpr (sizeof(T) == 4)
-      b = bin_f32(v[i], p);
+      b = bin_f32(v[i], p, range_mode == CL_RANGE_FIXED);
     else
       b = bin_index_exact(v[i], p.lo, p.width, k);
     if (use_smem)
@@ -737,22 +950,35 @@ cudaError_t launch_histogram_f32(const float* v, uint64_t n, uint64_t g0,
   auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
   const int mode = stride_mode(stride);
   if (k <= 256 && n >= 4096) {
-    static bool attr_set[3] = {false, false, false};
     const uint64_t chunks = n / kChunkFloats + 1;
     const int grid = static_cast<int>(chunks < static_cast<uint64_t>(num_sms) ? chunks : num_sms);
+    const bool fixed = spec.range_mode == CL_RANGE_FIXED;
     auto launch = [&](auto kern) {
-      if (!attr_set[mode]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kHistSmem));
-        attr_set[mode] = true;
-      }
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(kHistSmem));
       kern<<<grid, kHistThreads, kHistSmem, s>>>(v, n, g0, stride, spec.range_mode,
                                                  spec.fixed_lo, spec.fixed_hi, k, d_range,
                                                  counts);
     };
-    if (mode == 0) launch(hist_f32_lane_kernel<0>);
-    else if (mode == 1) launch(hist_f32_lane_kernel<1>);
-    else launch(hist_f32_lane_kernel<2>);
+    static const int variant = [] {
+      const char* e = getenv("CL_HIST_VARIANT");
+      return e ? atoi(e) : 0;
+    }();
+    if (variant == 1 && mode == 0) {
+      const size_t smem = size_t(kStages) * kChunkBytes + kHistWarps * kLaneBins * 4 + 2 * kStages * 8 + 64;
+      auto kern = fixed ? hist_f32_atoms_kernel<true> : hist_f32_atoms_kernel<false>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      kern<<<grid, kHistThreads, smem, s>>>(v, n, spec.range_mode, spec.fixed_lo, spec.fixed_hi, k,
+                                            d_range, counts);
+    } else if (fixed) {
+      if (mode == 0) launch(hist_f32_lane_kernel<0, true>);
+      else if (mode == 1) launch(hist_f32_lane_kernel<1, true>);
+      else launch(hist_f32_lane_kernel<2, true>);
+    } else {
+      if (mode == 0) launch(hist_f32_lane_kernel<0, false>);
+      else if (mode == 1) launch(hist_f32_lane_kernel<1, false>);
+      else launch(hist_f32_lane_kernel<2, false>);
+    }
   } else {
     const int use_smem = k <= 16384 ? 1 : 0;
     const size_t smem = use_smem ? static_cast<size_t>(k) * 4 : 0;

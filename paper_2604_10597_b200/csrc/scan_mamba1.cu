@@ -25,6 +25,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 
 #include "cl_internal.h"
@@ -116,30 +117,7 @@ __global__ void __launch_bounds__(128) generic_kernel(GenericArgs a) {
 // TMA row-sequential kernel (N = 16)
 // ---------------------------------------------------------------------------
 constexpr int kN = 16;
-constexpr int kBox = 32;       // timesteps per box (128 B rows, SWIZZLE_128B)
-constexpr int kRows = 32;      // rows per tile = lanes per warp
-constexpr int kWarps = 4;      // independent warps per CTA
-constexpr int kStages = 3;
-constexpr int kTileBytes = kRows * kBox * 4;  // 4 KB (u / delta / z / y)
-constexpr int kBCBytes = kN * kBox * 4;       // 2 KB (B or C)
-constexpr int kStageBytes = 3 * kTileBytes + 2 * kBCBytes;  // 16 KB
-constexpr int kWarpBytes = kStages * kStageBytes + kTileBytes;  // 48 KB in + 4 KB y staging
-constexpr size_t kTmaSmem = size_t(kWarps) * kWarpBytes + 1024 /*align*/ + 256 /*barriers*/;
-
-struct TmaArgs {
-  const float *A, *D, *bias, *h0;
-  float* h_last;
-  float* carry;            // [n_tiles][32][16]
-  unsigned int* flags;     // [n_tiles] completed segments
-  unsigned int* ticket;    // work counter
-  uint64_t batch, dim, L;
-  int tiles_per_batch;
-  int n_tiles;
-  int softplus;
-  int has_z;
-  const cl_decision* decision;
-  int fixed_chunk;
-};
+constexpr int kRows = 32;  // rows per tile = lanes per warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -183,6 +161,9 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
 __device__ __forceinline__ void bulk_wait_read_all() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read_le1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -198,49 +179,175 @@ __device__ __forceinline__ void st_release(unsigned int* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// 128B-swizzled float4 chunk j of row r inside a [32 rows x 32 floats] box.
-__device__ __forceinline__ int swz(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
+// ---- packed fp32x2 (FFMA2) helpers: a 64-bit register pair holds two fp32 lanes ----
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t pk(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk(f2_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// 2^x on the FMA pipe for a pair (Cody-Waite split + degree-5 minimax on [-0.5, 0.5],
+// max rel err 2.4e-7 in fp32, same class as MUFU.EX2): lets the kernel move part of
+// the 16 exponentials per element off the MUFU (the scan's binding pipe).
+__device__ __forceinline__ f2_t exp2_poly2(f2_t x) {
+  float a, b;
+  upk(x, a, b);
+  a = fminf(fmaxf(a, -127.f), 127.f);
+  b = fminf(fmaxf(b, -127.f), 127.f);
+  const f2_t magic = pk(12582912.0f, 12582912.0f);
+  const f2_t t = add2(pk(a, b), magic);
+  const f2_t j = add2(t, pk(-12582912.0f, -12582912.0f));
+  const f2_t f = add2(pk(a, b), mul2(j, pk(-1.f, -1.f)));
+  f2_t p = pk(0.001327816391980198f, 0.001327816391980198f);
+  p = fma2(p, f, pk(0.00967555578392905f, 0.00967555578392905f));
+  p = fma2(p, f, pk(0.055507080479488276f, 0.055507080479488276f));
+  p = fma2(p, f, pk(0.2402211936420041f, 0.2402211936420041f));
+  p = fma2(p, f, pk(0.6931469702538122f, 0.6931469702538122f));
+  p = fma2(p, f, pk(1.0000000717654767f, 1.0000000717654767f));
+  float pl, ph, tl, th;
+  upk(p, pl, ph);
+  upk(t, tl, th);
+  pl = __int_as_float(__float_as_int(pl) + (__float_as_int(tl) << 23));
+  ph = __int_as_float(__float_as_int(ph) + (__float_as_int(th) << 23));
+  return pk(pl, ph);
+}
+
+// softplus for a pair, branch-free: max(x,0) + log1p(exp(-|x|)), log1p by a degree-9
+// minimax polynomial on [0,1] (max rel err 2e-7 in fp32).  Equals x to fp32 precision
+// above 20, matching mamba_ssm's threshold.
+__device__ __forceinline__ f2_t softplus2(f2_t x) {
+  float a, b;
+  upk(x, a, b);
+  const float ea = ex2_approx(-fabsf(a) * kLog2e);
+  const float eb = ex2_approx(-fabsf(b) * kLog2e);
+  const f2_t e = pk(ea, eb);
+  f2_t q = pk(0.005253826278033571f, 0.005253826278033571f);
+  q = fma2(q, e, pk(-0.02959069552080005f, -0.02959069552080005f));
+  q = fma2(q, e, pk(0.07836660226277938f, 0.07836660226277938f));
+  q = fma2(q, e, pk(-0.13675328086246433f, -0.13675328086246433f));
+  q = fma2(q, e, pk(0.19111774195698683f, 0.19111774195698683f));
+  q = fma2(q, e, pk(-0.24844483411506615f, -0.24844483411506615f));
+  q = fma2(q, e, pk(0.33319289806287417f, 0.33319289806287417f));
+  q = fma2(q, e, pk(-0.49999502673812024f, -0.49999502673812024f));
+  q = fma2(q, e, pk(0.9999999706625772f, 0.9999999706625772f));
+  return fma2(q, e, pk(fmaxf(a, 0.f), fmaxf(b, 0.f)));
+}
+
+// z * sigmoid(z) for a pair: one MUFU.EX2 per lane, reciprocal by Newton iterations
+// on the FMA pipe (3 steps from the bit-trick seed: rel err < 1e-7).
+__device__ __forceinline__ f2_t silu2(f2_t z) {
+  float a, b;
+  upk(z, a, b);
+  const float ea = ex2_approx(fmaxf(a, -80.f) * -kLog2e);
+  const float eb = ex2_approx(fmaxf(b, -80.f) * -kLog2e);
+  const f2_t d = add2(pk(ea, eb), pk(1.f, 1.f));
+  float dl, dh;
+  upk(d, dl, dh);
+  f2_t r = pk(__int_as_float(0x7EF311C7 - __float_as_int(dl)),
+              __int_as_float(0x7EF311C7 - __float_as_int(dh)));
+  const f2_t one = pk(1.f, 1.f);
+  const f2_t nd = mul2(d, pk(-1.f, -1.f));
+#pragma unroll
+  for (int it = 0; it < 3; ++it) {
+    const f2_t e = fma2(nd, r, one);
+    r = fma2(r, e, r);
+  }
+  return mul2(z, r);
+}
+
+struct TmaArgs {
+  const float *A, *D, *bias, *h0;
+  float* h_last;
+  float* carry;            // [n_tiles][32][16]
+  unsigned int* flags;     // [n_tiles] completed segments
+  unsigned int* ticket;    // work counter
+  uint64_t batch, dim, L;
+  int tiles_per_batch;
+  int n_tiles;
+  const cl_decision* decision;
+  int fixed_chunk;
+};
 
 struct Item {
   int tile, seg, nbox;
   int t0;
 };
 
-__global__ void __launch_bounds__(kWarps * 32, 1)
+// Geometry: BOX timesteps per TMA box (32/16/8 -> 128B/64B/32B swizzle),
+// WARPS independent warps per CTA, STAGES-deep per-warp TMA ring.
+template <int BOX>
+struct Geo {
+  static constexpr int kTileBytes = kRows * BOX * 4;            // u / delta / z / y
+  static constexpr int kBCBytes = BOX * kN * 4;                 // B^T or C^T  [BOX][16]
+  static constexpr int kStageBytes = 3 * kTileBytes + 2 * kBCBytes;
+  // 16B-chunk j (4 timesteps) of row r inside a swizzled [32 x BOX] box
+  static __device__ __forceinline__ int swz(int r, int j) {
+    if (BOX == 32) return r * 128 + ((j ^ (r & 7)) << 4);        // SWIZZLE_128B
+    if (BOX == 16) return r * 64 + ((j ^ ((r >> 1) & 3)) << 4);  // SWIZZLE_64B
+    return r * 32 + ((j ^ ((r >> 2) & 1)) << 4);                 // SWIZZLE_32B
+  }
+};
+
+template <int BOX, int STAGES>
+constexpr int warp_bytes() {
+  return STAGES * Geo<BOX>::kStageBytes + 2 * Geo<BOX>::kTileBytes;  // + 2 y staging buffers
+}
+
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int EMU>
+__global__ void __launch_bounds__(WARPS * 32, 1)
     rowseq_tma_kernel(const __grid_constant__ CUtensorMap map_u,
                       const __grid_constant__ CUtensorMap map_dt,
                       const __grid_constant__ CUtensorMap map_z,
                       const __grid_constant__ CUtensorMap map_out,
-                      const __grid_constant__ CUtensorMap map_B,
-                      const __grid_constant__ CUtensorMap map_C, TmaArgs a) {
+                      const __grid_constant__ CUtensorMap map_Bt,
+                      const __grid_constant__ CUtensorMap map_Ct, TmaArgs a) {
+  using G = Geo<BOX>;
   int status;
   const int chunk = read_chunk(a.decision, a.fixed_chunk, &status);
   if (status != 0) return;
-  int seg_len = chunk < kBox ? kBox : chunk;
-  seg_len = (seg_len + kBox - 1) / kBox * kBox;
+  int seg_len = chunk < BOX ? BOX : chunk;
+  seg_len = (seg_len + BOX - 1) / BOX * BOX;
   const int L = static_cast<int>(a.L);
   const int n_seg = (L + seg_len - 1) / seg_len;
   const int n_items = n_seg * a.n_tiles;
 
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align to 1024 B (128B swizzle atom) with pointer arithmetic on the __shared__
+  // base, so every access below stays in the shared window (LDS/STS, not generic LD)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  unsigned char* wbase = smem + size_t(warp) * kWarpBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(kWarps) * kWarpBytes) + warp * 4;
-  // per-slot metadata (item index, box) kept in registers of every lane
-  int meta_item[kStages], meta_box[kStages];
+  constexpr int kWB = warp_bytes<BOX, STAGES>();
+  unsigned char* wbase = smem + size_t(warp) * kWB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(WARPS) * kWB) + warp * 4;
+  int meta_item[STAGES], meta_box[STAGES];
 
   if (lane == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1);
+    for (int s = 0; s < STAGES; ++s) mbar_init(bars + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (warp == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_u)));
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_dt)));
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_z)));
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_B)));
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_C)));
-    }
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_u)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_dt)));
+    if (HZ) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_z)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_Bt)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_Ct)));
   }
   __syncwarp();
 
@@ -250,7 +357,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     it.tile = id % a.n_tiles;
     it.t0 = it.seg * seg_len;
     const int len = min(seg_len, L - it.t0);
-    it.nbox = (len + kBox - 1) / kBox;
+    it.nbox = (len + BOX - 1) / BOX;
     return it;
   };
   auto claim = [&]() {
@@ -259,43 +366,44 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     return __shfl_sync(0xffffffffu, id, 0);
   };
 
-  // producer cursor
   int p_item = claim();
   int p_box = 0;
+  Item p_it = decode(p_item);
   auto produce = [&](int slot) {
     meta_item[slot] = -1;
     if (p_item >= n_items) return;
-    const Item it = decode(p_item);
+    const Item it = p_it;
     meta_item[slot] = p_item;
     meta_box[slot] = p_box;
     if (lane == 0) {
-      unsigned char* st = wbase + slot * kStageBytes;
+      unsigned char* st = wbase + slot * G::kStageBytes;
       const int b = it.tile / a.tiles_per_batch;
       const int r0 = (it.tile % a.tiles_per_batch) * kRows;
-      const int t = it.t0 + p_box * kBox;
-      mbar_expect_tx(bars + slot, a.has_z ? kStageBytes : kStageBytes - kTileBytes);
+      const int t = it.t0 + p_box * BOX;
+      mbar_expect_tx(bars + slot, HZ ? G::kStageBytes : G::kStageBytes - G::kTileBytes);
       tma_load_3d(st, &map_u, t, r0, b, bars + slot);
-      tma_load_3d(st + kTileBytes, &map_dt, t, r0, b, bars + slot);
-      if (a.has_z) tma_load_3d(st + 2 * kTileBytes, &map_z, t, r0, b, bars + slot);
-      tma_load_3d(st + 3 * kTileBytes, &map_B, t, 0, b, bars + slot);
-      tma_load_3d(st + 3 * kTileBytes + kBCBytes, &map_C, t, 0, b, bars + slot);
+      tma_load_3d(st + G::kTileBytes, &map_dt, t, r0, b, bars + slot);
+      if (HZ) tma_load_3d(st + 2 * G::kTileBytes, &map_z, t, r0, b, bars + slot);
+      tma_load_3d(st + 3 * G::kTileBytes, &map_Bt, 0, t, b, bars + slot);
+      tma_load_3d(st + 3 * G::kTileBytes + G::kBCBytes, &map_Ct, 0, t, b, bars + slot);
     }
     if (++p_box == it.nbox) {
       p_box = 0;
       p_item = claim();
+      p_it = decode(p_item);
     }
   };
 
-  for (int s = 0; s < kStages; ++s) produce(s);
+  for (int s = 0; s < STAGES; ++s) produce(s);
 
-  unsigned char* ybuf = wbase + kStages * kStageBytes;
-  float h[kN], A2[kN];
+  unsigned char* ybuf0 = wbase + STAGES * G::kStageBytes;
+  f2_t h2[kN / 2], A2p[kN / 2];
   float bias = 0.f, Dc = 0.f;
   Item cur{};
   int row = 0;
   bool row_valid = false;
   for (int iter = 0;; ++iter) {
-    const int slot = iter % kStages;
+    const int slot = iter % STAGES;
     const int item = meta_item[slot];
     if (item < 0) break;
     const int box = meta_box[slot];
@@ -309,87 +417,110 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
       for (int s = 0; s < kN; s += 4) {
         const float4 q = *reinterpret_cast<const float4*>(a.A + size_t(cc) * kN + s);
-        A2[s] = q.x * kLog2e;
-        A2[s + 1] = q.y * kLog2e;
-        A2[s + 2] = q.z * kLog2e;
-        A2[s + 3] = q.w * kLog2e;
+        A2p[s / 2] = pk(q.x * kLog2e, q.y * kLog2e);
+        A2p[s / 2 + 1] = pk(q.z * kLog2e, q.w * kLog2e);
       }
       bias = a.bias ? a.bias[cc] : 0.f;
       Dc = a.D ? a.D[cc] : 0.f;
+      const float* src = nullptr;
       if (cur.seg == 0) {
-#pragma unroll
-        for (int s = 0; s < kN; ++s) h[s] = 0.f;
-        if (a.h0) {
-#pragma unroll
-          for (int s = 0; s < kN; s += 4) {
-            const float4 q = *reinterpret_cast<const float4*>(a.h0 + size_t(row) * kN + s);
-            h[s] = q.x;
-            h[s + 1] = q.y;
-            h[s + 2] = q.z;
-            h[s + 3] = q.w;
-          }
-        }
+        src = a.h0 ? a.h0 + size_t(row) * kN : nullptr;
       } else {
         // chained carry from segment seg-1 of this tile
         if (lane == 0)
           while (ld_acquire(a.flags + cur.tile) < static_cast<unsigned>(cur.seg)) __nanosleep(64);
         __syncwarp();
-        const float* cr = a.carry + (size_t(cur.tile) * kRows + lane) * kN;
+        src = a.carry + (size_t(cur.tile) * kRows + lane) * kN;
+      }
 #pragma unroll
-        for (int s = 0; s < kN; s += 4) {
-          const float4 q = __ldcg(reinterpret_cast<const float4*>(cr + s));
-          h[s] = q.x;
-          h[s + 1] = q.y;
-          h[s + 2] = q.z;
-          h[s + 3] = q.w;
-        }
+      for (int s = 0; s < kN; s += 4) {
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (src) q = __ldcg(reinterpret_cast<const float4*>(src + s));
+        h2[s / 2] = pk(q.x, q.y);
+        h2[s / 2 + 1] = pk(q.z, q.w);
       }
     }
 
-    mbar_wait(bars + slot, (iter / kStages) & 1);
-    // the y staging buffer is free once the previous box's store has read it
-    if (lane == 0) bulk_wait_read_all();
+    mbar_wait(bars + slot, (iter / STAGES) & 1);
+    // y staging is double-buffered: this buffer is free once the store issued two
+    // boxes ago has read it (at most the newest store may still be in flight)
+    unsigned char* ybuf = ybuf0 + (iter & 1) * G::kTileBytes;
+    if (lane == 0) bulk_wait_read_le1();
     __syncwarp();
-    unsigned char* st = wbase + slot * kStageBytes;
-    const float* sB = reinterpret_cast<const float*>(st + 3 * kTileBytes);
-    const float* sC = reinterpret_cast<const float*>(st + 3 * kTileBytes + kBCBytes);
-    const int tbox = cur.t0 + box * kBox;
-    const int valid = min(kBox, L - tbox);  // multiple of 4 (L % 4 == 0)
+    unsigned char* st = wbase + slot * G::kStageBytes;
+    const unsigned char* sB = st + 3 * G::kTileBytes;
+    const unsigned char* sC = sB + G::kBCBytes;
+    const int tbox = cur.t0 + box * BOX;
+    const int valid = min(BOX, L - tbox);  // multiple of 4 (L % 4 == 0)
+    const f2_t bias2 = pk(bias, bias);
     for (int j = 0; j < valid / 4; ++j) {
-      const int off = swz(lane, j);
+      const int off = G::swz(lane, j);
       const float4 u4 = *reinterpret_cast<const float4*>(st + off);
-      const float4 d4 = *reinterpret_cast<const float4*>(st + kTileBytes + off);
-      float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (a.has_z) z4 = *reinterpret_cast<const float4*>(st + 2 * kTileBytes + off);
-      const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
-      const float dd[4] = {d4.x, d4.y, d4.z, d4.w};
-      const float zz[4] = {z4.x, z4.y, z4.z, z4.w};
-      float yy[4];
-      float4 Bq[kN], Cq[kN];
-#pragma unroll
-      for (int s = 0; s < kN; ++s) {
-        Bq[s] = *reinterpret_cast<const float4*>(sB + s * kBox + 4 * j);
-        Cq[s] = *reinterpret_cast<const float4*>(sC + s * kBox + 4 * j);
+      const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
+      // elementwise prologue for the 4 timesteps, packed in pairs
+      f2_t dt01 = add2(pk(d4.x, d4.y), bias2), dt23 = add2(pk(d4.z, d4.w), bias2);
+      if (SP) {
+        dt01 = softplus2(dt01);
+        dt23 = softplus2(dt23);
       }
+      const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
+      float dt[4], xs[4];
+      upk(dt01, dt[0], dt[1]);
+      upk(dt23, dt[2], dt[3]);
+      upk(x01, xs[0], xs[1]);
+      upk(x23, xs[2], xs[3]);
+      float yy[4];
+      // phase A: the 4x16 transition factors exp(dt*A) do not depend on the state,
+      // so they are all issued up front (MUFU-paced, independent)
+      f2_t dA[4][kN / 2];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        float dt = dd[k] + bias;
-        if (a.softplus) dt = softplus_f32(dt);
-        const float x = dt * uu[k];
-        float y = 0.f;
+        const f2_t dd = pk(dt[k], dt[k]);
 #pragma unroll
-        for (int s = 0; s < kN; ++s) {
-          const float bs = k == 0 ? Bq[s].x : (k == 1 ? Bq[s].y : (k == 2 ? Bq[s].z : Bq[s].w));
-          const float cs = k == 0 ? Cq[s].x : (k == 1 ? Cq[s].y : (k == 2 ? Cq[s].z : Cq[s].w));
-          const float dA = ex2_approx(dt * A2[s]);
-          h[s] = fmaf(dA, h[s], bs * x);
-          y = fmaf(cs, h[s], y);
+        for (int i = 0; i < kN / 2; ++i) {
+          const f2_t arg = mul2(A2p[i], dd);
+          if (i < EMU) {
+            dA[k][i] = exp2_poly2(arg);
+          } else {
+            float al, ah;
+            upk(arg, al, ah);
+            dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+          }
         }
-        y = fmaf(Dc, uu[k], y);
-        if (a.has_z) y *= silu_f32(zz[k]);
-        yy[k] = y;
       }
-      *reinterpret_cast<float4*>(ybuf + off) = make_float4(yy[0], yy[1], yy[2], yy[3]);
+      // phase B: recurrence h = dA*h + B*x and y = C.h, FFMA2 on state pairs
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int t = 4 * j + k;
+        const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + t * kN * 4);
+        const ulonglong2* Ct = reinterpret_cast<const ulonglong2*>(sC + t * kN * 4);
+        const f2_t xx = pk(xs[k], xs[k]);
+        f2_t ya = 0ull, yb = 0ull;
+#pragma unroll
+        for (int q = 0; q < kN / 4; ++q) {
+          const ulonglong2 bq = Bt[q];
+          const ulonglong2 cq = Ct[q];
+          h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
+          h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
+          ya = fma2(cq.x, h2[2 * q], ya);
+          yb = fma2(cq.y, h2[2 * q + 1], yb);
+        }
+        float a0, a1;
+        upk(add2(ya, yb), a0, a1);
+        yy[k] = a0 + a1;
+      }
+      const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+      f2_t y01 = fma2(pk(Dc, Dc), pk(uu[0], uu[1]), pk(yy[0], yy[1]));
+      f2_t y23 = fma2(pk(Dc, Dc), pk(uu[2], uu[3]), pk(yy[2], yy[3]));
+      if (HZ) {
+        const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
+        y01 = mul2(y01, silu2(pk(z4.x, z4.y)));
+        y23 = mul2(y23, silu2(pk(z4.z, z4.w)));
+      }
+      float o0, o1, o2, o3;
+      upk(y01, o0, o1);
+      upk(y23, o2, o3);
+      *reinterpret_cast<float4*>(ybuf + off) = make_float4(o0, o1, o2, o3);
     }
     fence_proxy_async();
     __syncwarp();
@@ -400,28 +531,319 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     }
 
     if (box == cur.nbox - 1) {
+      float hs[kN];
+#pragma unroll
+      for (int i = 0; i < kN / 2; ++i) upk(h2[i], hs[2 * i], hs[2 * i + 1]);
       if (cur.seg == n_seg - 1) {
         if (a.h_last && row_valid) {
 #pragma unroll
           for (int s = 0; s < kN; s += 4)
             *reinterpret_cast<float4*>(a.h_last + size_t(row) * kN + s) =
-                make_float4(h[s], h[s + 1], h[s + 2], h[s + 3]);
+                make_float4(hs[s], hs[s + 1], hs[s + 2], hs[s + 3]);
         }
       } else {
         float* cw = a.carry + (size_t(cur.tile) * kRows + lane) * kN;
 #pragma unroll
         for (int s = 0; s < kN; s += 4)
-          __stcg(reinterpret_cast<float4*>(cw + s), make_float4(h[s], h[s + 1], h[s + 2], h[s + 3]));
+          __stcg(reinterpret_cast<float4*>(cw + s),
+                 make_float4(hs[s], hs[s + 1], hs[s + 2], hs[s + 3]));
         __threadfence();
         __syncwarp();
         if (lane == 0) st_release(a.flags + cur.tile, static_cast<unsigned>(cur.seg + 1));
       }
     }
-    // every lane has consumed this slot: refill it for iteration iter + kStages
+    // every lane has consumed this slot: refill it for iteration iter + STAGES
+    __syncwarp();
     produce(slot);
   }
   if (lane == 0) bulk_wait_all();
   __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// Lane-pair variant: a warp owns a 16-row tile; lanes (2r, 2r+1) share row r and
+// hold states 0-7 / 8-15.  Twice the independent row chains of the 32-row kernel
+// for the same shape (the chained-segment schedule caps busy warps at the tile
+// count), at the cost of one 64-bit shuffle pair per 4 timesteps.
+// ---------------------------------------------------------------------------
+constexpr int kRowsP = 16;
+
+template <int BOX>
+struct GeoP {
+  static constexpr int kTileBytes = kRowsP * BOX * 4;
+  static constexpr int kBCBytes = BOX * kN * 4;
+  static constexpr int kStageBytes = 3 * kTileBytes + 2 * kBCBytes;
+};
+
+template <int BOX, int STAGES>
+constexpr int warp_bytes_p() {
+  return STAGES * GeoP<BOX>::kStageBytes + 2 * GeoP<BOX>::kTileBytes;
+}
+
+__device__ __forceinline__ f2_t shfl_xor2(f2_t v, int m) {
+  float lo, hi;
+  upk(v, lo, hi);
+  return pk(__shfl_xor_sync(0xffffffffu, lo, m), __shfl_xor_sync(0xffffffffu, hi, m));
+}
+
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int EMU>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    rowpair_tma_kernel(const __grid_constant__ CUtensorMap map_u,
+                       const __grid_constant__ CUtensorMap map_dt,
+                       const __grid_constant__ CUtensorMap map_z,
+                       const __grid_constant__ CUtensorMap map_out,
+                       const __grid_constant__ CUtensorMap map_Bt,
+                       const __grid_constant__ CUtensorMap map_Ct, TmaArgs a) {
+  using G = GeoP<BOX>;
+  int status;
+  const int chunk = read_chunk(a.decision, a.fixed_chunk, &status);
+  if (status != 0) return;
+  int seg_len = chunk < BOX ? BOX : chunk;
+  seg_len = (seg_len + BOX - 1) / BOX * BOX;
+  const int L = static_cast<int>(a.L);
+  const int n_seg = (L + seg_len - 1) / seg_len;
+  const int n_items = n_seg * a.n_tiles;
+
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int r = lane >> 1, hf = lane & 1;
+  constexpr int kWB = warp_bytes_p<BOX, STAGES>();
+  unsigned char* wbase = smem + size_t(warp) * kWB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(WARPS) * kWB) + warp * 4;
+  int meta_item[STAGES], meta_box[STAGES];
+
+  if (lane == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_u)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_dt)));
+    if (HZ) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_z)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_Bt)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_Ct)));
+  }
+  __syncwarp();
+
+  auto decode = [&](int id) {
+    Item it;
+    it.seg = id / a.n_tiles;
+    it.tile = id % a.n_tiles;
+    it.t0 = it.seg * seg_len;
+    const int len = min(seg_len, L - it.t0);
+    it.nbox = (len + BOX - 1) / BOX;
+    return it;
+  };
+  auto claim = [&]() {
+    int id = 0;
+    if (lane == 0) id = static_cast<int>(atomicAdd(a.ticket, 1u));
+    return __shfl_sync(0xffffffffu, id, 0);
+  };
+
+  int p_item = claim();
+  int p_box = 0;
+  Item p_it = decode(p_item);
+  auto produce = [&](int slot) {
+    meta_item[slot] = -1;
+    if (p_item >= n_items) return;
+    const Item it = p_it;
+    meta_item[slot] = p_item;
+    meta_box[slot] = p_box;
+    if (lane == 0) {
+      unsigned char* st = wbase + slot * G::kStageBytes;
+      const int b = it.tile / a.tiles_per_batch;
+      const int r0 = (it.tile % a.tiles_per_batch) * kRowsP;
+      const int t = it.t0 + p_box * BOX;
+      mbar_expect_tx(bars + slot, HZ ? G::kStageBytes : G::kStageBytes - G::kTileBytes);
+      tma_load_3d(st, &map_u, t, r0, b, bars + slot);
+      tma_load_3d(st + G::kTileBytes, &map_dt, t, r0, b, bars + slot);
+      if (HZ) tma_load_3d(st + 2 * G::kTileBytes, &map_z, t, r0, b, bars + slot);
+      tma_load_3d(st + 3 * G::kTileBytes, &map_Bt, 0, t, b, bars + slot);
+      tma_load_3d(st + 3 * G::kTileBytes + G::kBCBytes, &map_Ct, 0, t, b, bars + slot);
+    }
+    if (++p_box == it.nbox) {
+      p_box = 0;
+      p_item = claim();
+      p_it = decode(p_item);
+    }
+  };
+
+  for (int s = 0; s < STAGES; ++s) produce(s);
+
+  unsigned char* ybuf0 = wbase + STAGES * G::kStageBytes;
+  constexpr int kP = kN / 4;  // state pairs per lane
+  f2_t h2[kP], A2p[kP];
+  float bias = 0.f, Dc = 0.f;
+  Item cur{};
+  int row = 0;
+  bool row_valid = false;
+  for (int iter = 0;; ++iter) {
+    const int slot = iter % STAGES;
+    const int item = meta_item[slot];
+    if (item < 0) break;
+    const int box = meta_box[slot];
+    if (box == 0) {
+      cur = decode(item);
+      const int b = cur.tile / a.tiles_per_batch;
+      const int c = (cur.tile % a.tiles_per_batch) * kRowsP + r;
+      row_valid = c < static_cast<int>(a.dim);
+      const int cc = row_valid ? c : 0;
+      row = b * static_cast<int>(a.dim) + cc;
+#pragma unroll
+      for (int s = 0; s < kN / 2; s += 4) {
+        const float4 q = *reinterpret_cast<const float4*>(a.A + size_t(cc) * kN + 8 * hf + s);
+        A2p[s / 2] = pk(q.x * kLog2e, q.y * kLog2e);
+        A2p[s / 2 + 1] = pk(q.z * kLog2e, q.w * kLog2e);
+      }
+      bias = a.bias ? a.bias[cc] : 0.f;
+      Dc = a.D ? a.D[cc] : 0.f;
+      const float* src = nullptr;
+      if (cur.seg == 0) {
+        src = a.h0 ? a.h0 + size_t(row) * kN + 8 * hf : nullptr;
+      } else {
+        if (lane == 0)
+          while (ld_acquire(a.flags + cur.tile) < static_cast<unsigned>(cur.seg)) __nanosleep(64);
+        __syncwarp();
+        src = a.carry + (size_t(cur.tile) * kRowsP + r) * kN + 8 * hf;
+      }
+#pragma unroll
+      for (int s = 0; s < kN / 2; s += 4) {
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (src) q = __ldcg(reinterpret_cast<const float4*>(src + s));
+        h2[s / 2] = pk(q.x, q.y);
+        h2[s / 2 + 1] = pk(q.z, q.w);
+      }
+    }
+
+    mbar_wait(bars + slot, (iter / STAGES) & 1);
+    unsigned char* ybuf = ybuf0 + (iter & 1) * G::kTileBytes;
+    if (lane == 0) bulk_wait_read_le1();
+    __syncwarp();
+    unsigned char* st = wbase + slot * G::kStageBytes;
+    const unsigned char* sB = st + 3 * G::kTileBytes + 32 * hf;  // this lane's 8 states
+    const unsigned char* sC = sB + G::kBCBytes;
+    const int tbox = cur.t0 + box * BOX;
+    const int valid = min(BOX, L - tbox);
+    const f2_t bias2 = pk(bias, bias);
+    for (int j = 0; j < valid / 4; ++j) {
+      const int off = Geo<BOX>::swz(r, j);
+      const float4 u4 = *reinterpret_cast<const float4*>(st + off);
+      const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
+      // softplus of timesteps (2hf, 2hf+1) here, the other pair from the partner lane
+      f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
+      if (SP) mine = softplus2(mine);
+      const f2_t other = shfl_xor2(mine, 1);
+      const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
+      const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
+      float dt[4], xs[4];
+      upk(dt01, dt[0], dt[1]);
+      upk(dt23, dt[2], dt[3]);
+      upk(x01, xs[0], xs[1]);
+      upk(x23, xs[2], xs[3]);
+      f2_t dA[4][kP];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const f2_t dd = pk(dt[k], dt[k]);
+#pragma unroll
+        for (int i = 0; i < kP; ++i) {
+          const f2_t arg = mul2(A2p[i], dd);
+          if (i < EMU) {
+            dA[k][i] = exp2_poly2(arg);
+          } else {
+            float al, ah;
+            upk(arg, al, ah);
+            dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+          }
+        }
+      }
+      float yp[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int t = 4 * j + k;
+        const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + t * kN * 4);
+        const ulonglong2* Ct = reinterpret_cast<const ulonglong2*>(sC + t * kN * 4);
+        const f2_t xx = pk(xs[k], xs[k]);
+        f2_t ya = 0ull, yb = 0ull;
+#pragma unroll
+        for (int q = 0; q < kP / 2; ++q) {
+          const ulonglong2 bq = Bt[q];
+          const ulonglong2 cq = Ct[q];
+          h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
+          h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
+          ya = fma2(cq.x, h2[2 * q], ya);
+          yb = fma2(cq.y, h2[2 * q + 1], yb);
+        }
+        float a0, a1;
+        upk(add2(ya, yb), a0, a1);
+        yp[k] = a0 + a1;
+      }
+      // lane hf finalises timesteps (2hf, 2hf+1): swap the partial sums it does not own
+      const f2_t keep = hf ? pk(yp[2], yp[3]) : pk(yp[0], yp[1]);
+      const f2_t give = hf ? pk(yp[0], yp[1]) : pk(yp[2], yp[3]);
+      const f2_t ysum = add2(keep, shfl_xor2(give, 1));
+      const f2_t u2 = hf ? pk(u4.z, u4.w) : pk(u4.x, u4.y);
+      f2_t yo = fma2(pk(Dc, Dc), u2, ysum);
+      if (HZ) {
+        const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
+        yo = mul2(yo, silu2(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y)));
+      }
+      *reinterpret_cast<f2_t*>(ybuf + off + 8 * hf) = yo;
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      const int b = cur.tile / a.tiles_per_batch;
+      const int r0 = (cur.tile % a.tiles_per_batch) * kRowsP;
+      tma_store_3d(&map_out, ybuf, tbox, r0, b);
+    }
+
+    if (box == cur.nbox - 1) {
+      float hs[kN / 2];
+#pragma unroll
+      for (int i = 0; i < kP; ++i) upk(h2[i], hs[2 * i], hs[2 * i + 1]);
+      float* dst = nullptr;
+      if (cur.seg == n_seg - 1) {
+        if (a.h_last && row_valid) dst = a.h_last + size_t(row) * kN + 8 * hf;
+      } else {
+        dst = a.carry + (size_t(cur.tile) * kRowsP + r) * kN + 8 * hf;
+      }
+      if (dst) {
+        __stcg(reinterpret_cast<float4*>(dst), make_float4(hs[0], hs[1], hs[2], hs[3]));
+        __stcg(reinterpret_cast<float4*>(dst + 4), make_float4(hs[4], hs[5], hs[6], hs[7]));
+      }
+      if (cur.seg != n_seg - 1) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release(a.flags + cur.tile, static_cast<unsigned>(cur.seg + 1));
+      }
+    }
+    __syncwarp();
+    produce(slot);
+  }
+  if (lane == 0) bulk_wait_all();
+  __syncwarp();
+}
+
+// (b, N, L) -> (b, L, N) for B and C, so a timestep's 16 state coefficients are one
+// contiguous 64-byte row: the scan then reads them as FFMA2 register pairs.
+__global__ void __launch_bounds__(256) transpose_bc_kernel(const float* __restrict__ B,
+                                                           const float* __restrict__ C,
+                                                           float* __restrict__ Bt,
+                                                           float* __restrict__ Ct, int L) {
+  __shared__ float tile[kN][33];
+  const float* src = blockIdx.z ? C : B;
+  float* dst = blockIdx.z ? Ct : Bt;
+  const int b = blockIdx.y, t0 = blockIdx.x * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // ty 0..7
+  for (int s = ty; s < kN; s += 8) {
+    const int t = t0 + tx;
+    tile[s][tx] = t < L ? src[(size_t(b) * kN + s) * L + t] : 0.f;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * kN; e += 256) {
+    const int tt = e / kN, s = e % kN;
+    const int t = t0 + tt;
+    if (t < L) dst[(size_t(b) * L + t) * kN + s] = tile[s][tt];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -447,17 +869,19 @@ EncodeFn get_encode() {
 }
 
 bool make_map(CUtensorMap* m, const float* base, uint64_t d0, uint64_t d1, uint64_t d2,
-              uint32_t box0, uint32_t box1, bool swizzle) {
+              uint32_t box0, uint32_t box1, int swizzle_bytes) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
   const cuuint64_t dims[3] = {d0, d1, d2};
   const cuuint64_t strides[2] = {d0 * 4, d0 * d1 * 4};
   const cuuint32_t box[3] = {box0, box1, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                      : CU_TENSOR_MAP_SWIZZLE_NONE;
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
-             estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -475,24 +899,92 @@ bool tma_eligible(const cl_mamba1_args& a) {
   return get_encode() != nullptr;
 }
 
-int ensure_scratch(cl_ctx* ctx, size_t work_bytes, size_t carry_bytes) {
-  if (ctx->work_bytes < work_bytes) {
-    if (ctx->d_work) cudaFree(ctx->d_work);
-    ctx->d_work = nullptr;
-    ctx->work_bytes = 0;
-    cudaError_t e = cudaMalloc(&ctx->d_work, work_bytes);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(scan work)");
-    ctx->work_bytes = work_bytes;
-  }
-  if (ctx->carry_bytes < carry_bytes) {
-    if (ctx->d_carry) cudaFree(ctx->d_carry);
-    ctx->d_carry = nullptr;
-    ctx->carry_bytes = 0;
-    cudaError_t e = cudaMalloc(&ctx->d_carry, carry_bytes);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(scan carry)");
-    ctx->carry_bytes = carry_bytes;
-  }
+template <typename T>
+int grow(cl_ctx* ctx, T** ptr, size_t* have, size_t need, const char* what) {
+  if (*have >= need) return CL_OK;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *have = 0;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), need);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, what);
+  *have = need;
   return CL_OK;
+}
+
+// ---- kernel geometry table (tuning knob: CL_SCAN_CFG=<index>) ----
+struct ScanCfg {
+  int box, warps, stages, emu, pair;
+};
+constexpr ScanCfg kCfgs[] = {
+    {32, 4, 3, 0, 0},  {32, 4, 3, 1, 0},  {32, 4, 3, 2, 0},  {16, 8, 3, 0, 0},  {16, 8, 3, 1, 0},
+    {16, 8, 3, 2, 0},  {16, 6, 4, 0, 0},  {16, 6, 4, 1, 0},  {16, 8, 3, 3, 0},  {16, 12, 2, 1, 0},
+    {8, 16, 3, 1, 0},  {16, 12, 2, 0, 0}, {8, 16, 3, 0, 0},  {8, 16, 3, 2, 0},  {8, 12, 4, 1, 0},
+    // lane-pair kernels (16-row tiles)
+    {32, 6, 3, 0, 1},  {32, 6, 3, 1, 1},  {16, 12, 3, 0, 1}, {16, 12, 3, 1, 1}, {16, 8, 4, 0, 1},
+    {16, 14, 2, 0, 1}, {32, 8, 2, 0, 1},
+};
+constexpr int kDefaultCfg = 20;
+
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int EMU>
+cudaError_t launch_rowseq(const CUtensorMap& mu, const CUtensorMap& mdt, const CUtensorMap& mz,
+                          const CUtensorMap& mout, const CUtensorMap& mB, const CUtensorMap& mC,
+                          const TmaArgs& t, int num_sms, cudaStream_t s) {
+  auto kern = rowseq_tma_kernel<BOX, WARPS, STAGES, SP, HZ, EMU>;
+  const size_t smem = size_t(WARPS) * warp_bytes<BOX, STAGES>() + 1024 + 256;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int grid = num_sms;
+  const int max_useful = (t.n_tiles + WARPS - 1) / WARPS;
+  if (max_useful < grid) grid = max_useful < 1 ? 1 : max_useful;
+  kern<<<grid, WARPS * 32, smem, s>>>(mu, mdt, mz, mout, mB, mC, t);
+  return cudaGetLastError();
+}
+
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int EMU>
+cudaError_t launch_rowpair(const CUtensorMap& mu, const CUtensorMap& mdt, const CUtensorMap& mz,
+                           const CUtensorMap& mout, const CUtensorMap& mB, const CUtensorMap& mC,
+                           const TmaArgs& t, int num_sms, cudaStream_t s) {
+  auto kern = rowpair_tma_kernel<BOX, WARPS, STAGES, SP, HZ, EMU>;
+  const size_t smem = size_t(WARPS) * warp_bytes_p<BOX, STAGES>() + 1024 + 256;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int grid = num_sms;
+  const int max_useful = (t.n_tiles + WARPS - 1) / WARPS;
+  if (max_useful < grid) grid = max_useful < 1 ? 1 : max_useful;
+  kern<<<grid, WARPS * 32, smem, s>>>(mu, mdt, mz, mout, mB, mC, t);
+  return cudaGetLastError();
+}
+
+template <int BOX, int WARPS, int STAGES, int EMU>
+cudaError_t dispatch_pair(bool sp, bool hz, const CUtensorMap& mu, const CUtensorMap& mdt,
+                          const CUtensorMap& mz, const CUtensorMap& mout, const CUtensorMap& mB,
+                          const CUtensorMap& mC, const TmaArgs& t, int num_sms, cudaStream_t s) {
+  if (sp && hz) return launch_rowpair<BOX, WARPS, STAGES, true, true, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
+  if (sp) return launch_rowpair<BOX, WARPS, STAGES, true, false, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
+  if (hz) return launch_rowpair<BOX, WARPS, STAGES, false, true, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
+  return launch_rowpair<BOX, WARPS, STAGES, false, false, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
+}
+
+template <int BOX, int WARPS, int STAGES, int EMU>
+cudaError_t dispatch_flags(bool sp, bool hz, const CUtensorMap& mu, const CUtensorMap& mdt,
+                           const CUtensorMap& mz, const CUtensorMap& mout, const CUtensorMap& mB,
+                           const CUtensorMap& mC, const TmaArgs& t, int num_sms, cudaStream_t s) {
+  if (sp && hz) return launch_rowseq<BOX, WARPS, STAGES, true, true, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
+  if (sp) return launch_rowseq<BOX, WARPS, STAGES, true, false, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
+  if (hz) return launch_rowseq<BOX, WARPS, STAGES, false, true, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
+  return launch_rowseq<BOX, WARPS, STAGES, false, false, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
+}
+
+int scan_cfg_index() {
+  static int idx = [] {
+    const char* e = getenv("CL_SCAN_CFG");
+    int v = e ? atoi(e) : kDefaultCfg;
+    if (v < 0 || v >= static_cast<int>(sizeof(kCfgs) / sizeof(kCfgs[0]))) v = kDefaultCfg;
+    return v;
+  }();
+  return idx;
 }
 
 }  // namespace
@@ -504,23 +996,37 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     return fail(ctx, CL_E_INVALID, "scan variant rowseq_tma needs d_state 16, L % 4 == 0 and 16-byte aligned buffers");
   const bool use_tma = variant == CL_SCAN_ROWSEQ_TMA || (variant == CL_SCAN_AUTO && tma_ok);
   if (use_tma) {
-    CUtensorMap mu, mdt, mz, mout, mB, mC;
+    const ScanCfg cfg = kCfgs[scan_cfg_index()];
     const uint64_t L = a.seq_len, D = a.dim, Bt = a.batch;
-    bool ok = make_map(&mu, a.u, L, D, Bt, kBox, kRows, true) &&
-              make_map(&mdt, a.delta, L, D, Bt, kBox, kRows, true) &&
-              make_map(&mout, a.out, L, D, Bt, kBox, kRows, true) &&
-              make_map(&mB, a.B, L, kN, Bt, kBox, kN, false) &&
-              make_map(&mC, a.C, L, kN, Bt, kBox, kN, false);
-    if (ok) ok = make_map(&mz, a.z ? a.z : a.u, L, D, Bt, kBox, kRows, true);
-    if (!ok) return fail(ctx, CL_E_CUDA, "cuTensorMapEncodeTiled failed");
-    const int tiles_per_batch = static_cast<int>((D + kRows - 1) / kRows);
+    const int rows_per_tile = cfg.pair ? kRowsP : kRows;
+    const int tiles_per_batch = static_cast<int>((D + rows_per_tile - 1) / rows_per_tile);
     const int n_tiles = tiles_per_batch * static_cast<int>(Bt);
     const size_t work_bytes = (size_t(n_tiles) + 32) * sizeof(unsigned int);
-    const size_t carry_bytes = size_t(n_tiles) * kRows * kN * sizeof(float);
-    int rc = ensure_scratch(ctx, work_bytes, carry_bytes);
+    const size_t carry_bytes = size_t(n_tiles) * rows_per_tile * kN * sizeof(float);
+    const size_t bc_bytes = 2 * size_t(Bt) * L * kN * sizeof(float);
+    int rc = grow(ctx, &ctx->d_work, &ctx->work_bytes, work_bytes, "cudaMalloc(scan work)");
+    if (!rc) rc = grow(ctx, &ctx->d_carry, &ctx->carry_bytes, carry_bytes, "cudaMalloc(carry)");
+    if (!rc) rc = grow(ctx, &ctx->d_bct, &ctx->bct_bytes, bc_bytes, "cudaMalloc(B/C transpose)");
     if (rc) return rc;
+    float* d_Bt = ctx->d_bct;
+    float* d_Ct = ctx->d_bct + size_t(Bt) * L * kN;
+    const int box = cfg.box;
+    const int sw = box == 32 ? 128 : (box == 16 ? 64 : 32);
+    CUtensorMap mu, mdt, mz, mout, mB, mC;
+    bool ok = make_map(&mu, a.u, L, D, Bt, box, rows_per_tile, sw) &&
+              make_map(&mdt, a.delta, L, D, Bt, box, rows_per_tile, sw) &&
+              make_map(&mout, a.out, L, D, Bt, box, rows_per_tile, sw) &&
+              make_map(&mB, d_Bt, kN, L, Bt, kN, box, 0) &&
+              make_map(&mC, d_Ct, kN, L, Bt, kN, box, 0);
+    if (ok) ok = make_map(&mz, a.z ? a.z : a.u, L, D, Bt, box, rows_per_tile, sw);
+    if (!ok) return fail(ctx, CL_E_CUDA, "cuTensorMapEncodeTiled failed");
     cudaError_t e = cudaMemsetAsync(ctx->d_work, 0, work_bytes, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(scan work)");
+    const dim3 tgrid(static_cast<unsigned>((L + 31) / 32), static_cast<unsigned>(Bt), 2);
+    transpose_bc_kernel<<<tgrid, 256, 0, s>>>(a.B, a.C, d_Bt, d_Ct, static_cast<int>(L));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "transpose_bc_kernel launch");
+    ++ctx->launches;
     TmaArgs t{};
     t.A = a.A;
     t.D = a.D;
@@ -535,23 +1041,34 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     t.L = L;
     t.tiles_per_batch = tiles_per_batch;
     t.n_tiles = n_tiles;
-    t.softplus = a.delta_softplus;
-    t.has_z = a.z != nullptr;
     t.decision = d_decision;
     t.fixed_chunk = fixed_chunk;
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(rowseq_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(kTmaSmem));
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaFuncSetAttribute(rowseq_tma)");
-      attr = true;
+    const bool sp = a.delta_softplus != 0, hz = a.z != nullptr;
+    const int n = ctx->num_sms;
+    switch (scan_cfg_index()) {
+      case 0: e = dispatch_flags<32, 4, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 1: e = dispatch_flags<32, 4, 3, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 2: e = dispatch_flags<32, 4, 3, 2>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 3: e = dispatch_flags<16, 8, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 4: e = dispatch_flags<16, 8, 3, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 5: e = dispatch_flags<16, 8, 3, 2>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 6: e = dispatch_flags<16, 6, 4, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 7: e = dispatch_flags<16, 6, 4, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 8: e = dispatch_flags<16, 8, 3, 3>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 9: e = dispatch_flags<16, 12, 2, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 10: e = dispatch_flags<8, 16, 3, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 11: e = dispatch_flags<16, 12, 2, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 12: e = dispatch_flags<8, 16, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 13: e = dispatch_flags<8, 16, 3, 2>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 14: e = dispatch_flags<8, 12, 4, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 15: e = dispatch_pair<32, 6, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 16: e = dispatch_pair<32, 6, 3, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 17: e = dispatch_pair<16, 12, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 18: e = dispatch_pair<16, 12, 3, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 19: e = dispatch_pair<16, 8, 4, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 20: e = dispatch_pair<16, 14, 2, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      default: e = dispatch_pair<32, 8, 2, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
     }
-    // persistent: one CTA (4 independent warps) per SM, capped by the tile count
-    int grid = ctx->num_sms;
-    const int max_useful = (n_tiles + kWarps - 1) / kWarps;
-    if (max_useful < grid) grid = max_useful < 1 ? 1 : max_useful;
-    rowseq_tma_kernel<<<grid, kWarps * 32, kTmaSmem, s>>>(mu, mdt, mz, mout, mB, mC, t);
-    e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rowseq_tma_kernel launch");
     ++ctx->launches;
     return CL_OK;
