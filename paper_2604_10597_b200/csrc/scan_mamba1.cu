@@ -234,12 +234,16 @@ __device__ __forceinline__ f2_t exp2_poly2(f2_t x) {
 // softplus for a pair, branch-free: max(x,0) + log1p(exp(-|x|)), log1p by a degree-9
 // minimax polynomial on [0,1] (max rel err 2e-7 in fp32).  Equals x to fp32 precision
 // above 20, matching mamba_ssm's threshold.
+template <bool POLY = false>
 __device__ __forceinline__ f2_t softplus2(f2_t x) {
   float a, b;
   upk(x, a, b);
-  const float ea = ex2_approx(-fabsf(a) * kLog2e);
-  const float eb = ex2_approx(-fabsf(b) * kLog2e);
-  const f2_t e = pk(ea, eb);
+  f2_t e;
+  if (POLY) {
+    e = exp2_poly2(pk(-fabsf(a) * kLog2e, -fabsf(b) * kLog2e));
+  } else {
+    e = pk(ex2_approx(-fabsf(a) * kLog2e), ex2_approx(-fabsf(b) * kLog2e));
+  }
   f2_t q = pk(0.005253826278033571f, 0.005253826278033571f);
   q = fma2(q, e, pk(-0.02959069552080005f, -0.02959069552080005f));
   q = fma2(q, e, pk(0.07836660226277938f, 0.07836660226277938f));
@@ -254,12 +258,17 @@ __device__ __forceinline__ f2_t softplus2(f2_t x) {
 
 // z * sigmoid(z) for a pair: one MUFU.EX2 per lane, reciprocal by Newton iterations
 // on the FMA pipe (3 steps from the bit-trick seed: rel err < 1e-7).
+template <bool POLY = false>
 __device__ __forceinline__ f2_t silu2(f2_t z) {
   float a, b;
   upk(z, a, b);
-  const float ea = ex2_approx(fmaxf(a, -80.f) * -kLog2e);
-  const float eb = ex2_approx(fmaxf(b, -80.f) * -kLog2e);
-  const f2_t d = add2(pk(ea, eb), pk(1.f, 1.f));
+  f2_t e;
+  if (POLY) {
+    e = exp2_poly2(pk(fmaxf(a, -80.f) * -kLog2e, fmaxf(b, -80.f) * -kLog2e));
+  } else {
+    e = pk(ex2_approx(fmaxf(a, -80.f) * -kLog2e), ex2_approx(fmaxf(b, -80.f) * -kLog2e));
+  }
+  const f2_t d = add2(e, pk(1.f, 1.f));
   float dl, dh;
   upk(d, dl, dh);
   f2_t r = pk(__int_as_float(0x7EF311C7 - __float_as_int(dl)),
@@ -453,15 +462,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const int tbox = cur.t0 + box * BOX;
     const int valid = min(BOX, L - tbox);  // multiple of 4 (L % 4 == 0)
     const f2_t bias2 = pk(bias, bias);
-    for (int j = 0; j < valid / 4; ++j) {
+#pragma unroll
+    for (int j = 0; j < BOX / 4; ++j) {
+      if (4 * j >= valid) break;
       const int off = G::swz(lane, j);
       const float4 u4 = *reinterpret_cast<const float4*>(st + off);
       const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
       // elementwise prologue for the 4 timesteps, packed in pairs
       f2_t dt01 = add2(pk(d4.x, d4.y), bias2), dt23 = add2(pk(d4.z, d4.w), bias2);
       if (SP) {
-        dt01 = softplus2(dt01);
-        dt23 = softplus2(dt23);
+        dt01 = softplus2<(EMU >= 16)>(dt01);
+        dt23 = softplus2<(EMU >= 16)>(dt23);
       }
       const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
       float dt[4], xs[4];
@@ -479,7 +490,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 #pragma unroll
         for (int i = 0; i < kN / 2; ++i) {
           const f2_t arg = mul2(A2p[i], dd);
-          if (i < EMU) {
+          if (i < (EMU % 16)) {
             dA[k][i] = exp2_poly2(arg);
           } else {
             float al, ah;
@@ -514,8 +525,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       f2_t y23 = fma2(pk(Dc, Dc), pk(uu[2], uu[3]), pk(yy[2], yy[3]));
       if (HZ) {
         const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
-        y01 = mul2(y01, silu2(pk(z4.x, z4.y)));
-        y23 = mul2(y23, silu2(pk(z4.z, z4.w)));
+        y01 = mul2(y01, silu2<(EMU >= 16)>(pk(z4.x, z4.y)));
+        y23 = mul2(y23, silu2<(EMU >= 16)>(pk(z4.z, z4.w)));
       }
       float o0, o1, o2, o3;
       upk(y01, o0, o1);
@@ -724,13 +735,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const int tbox = cur.t0 + box * BOX;
     const int valid = min(BOX, L - tbox);
     const f2_t bias2 = pk(bias, bias);
-    for (int j = 0; j < valid / 4; ++j) {
+    // fully unrolled over the box's 4-timestep groups: straight-line code lets the
+    // scheduler interleave group j+1's exponentials with group j's FFMA2 chains
+#pragma unroll
+    for (int j = 0; j < BOX / 4; ++j) {
+      if (4 * j >= valid) break;
       const int off = Geo<BOX>::swz(r, j);
       const float4 u4 = *reinterpret_cast<const float4*>(st + off);
       const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
       // softplus of timesteps (2hf, 2hf+1) here, the other pair from the partner lane
       f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
-      if (SP) mine = softplus2(mine);
+      if (SP) mine = softplus2<(EMU >= 16)>(mine);
       const f2_t other = shfl_xor2(mine, 1);
       const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
       const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
@@ -746,7 +761,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 #pragma unroll
         for (int i = 0; i < kP; ++i) {
           const f2_t arg = mul2(A2p[i], dd);
-          if (i < EMU) {
+          if (i < (EMU % 16)) {
             dA[k][i] = exp2_poly2(arg);
           } else {
             float al, ah;
@@ -784,7 +799,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       f2_t yo = fma2(pk(Dc, Dc), u2, ysum);
       if (HZ) {
         const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
-        yo = mul2(yo, silu2(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y)));
+        yo = mul2(yo, silu2<(EMU >= 16)>(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y)));
       }
       *reinterpret_cast<f2_t*>(ybuf + off + 8 * hf) = yo;
     }
@@ -921,7 +936,8 @@ constexpr ScanCfg kCfgs[] = {
     {8, 16, 3, 1, 0},  {16, 12, 2, 0, 0}, {8, 16, 3, 0, 0},  {8, 16, 3, 2, 0},  {8, 12, 4, 1, 0},
     // lane-pair kernels (16-row tiles)
     {32, 6, 3, 0, 1},  {32, 6, 3, 1, 1},  {16, 12, 3, 0, 1}, {16, 12, 3, 1, 1}, {16, 8, 4, 0, 1},
-    {16, 14, 2, 0, 1}, {32, 8, 2, 0, 1},
+    {16, 14, 2, 0, 1}, {32, 8, 2, 0, 1},  {16, 14, 2, 1, 1}, {16, 14, 2, 16, 1}, {16, 14, 2, 17, 1},
+    {16, 12, 3, 16, 1}, {16, 7, 3, 0, 0},  {16, 7, 3, 16, 0}, {32, 4, 3, 16, 0},
 };
 constexpr int kDefaultCfg = 20;
 
@@ -1067,7 +1083,14 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       case 18: e = dispatch_pair<16, 12, 3, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
       case 19: e = dispatch_pair<16, 8, 4, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
       case 20: e = dispatch_pair<16, 14, 2, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      default: e = dispatch_pair<32, 8, 2, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 21: e = dispatch_pair<32, 8, 2, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 22: e = dispatch_pair<16, 14, 2, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 23: e = dispatch_pair<16, 14, 2, 16>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 24: e = dispatch_pair<16, 14, 2, 17>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 25: e = dispatch_pair<16, 12, 3, 16>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 26: e = dispatch_flags<16, 7, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 27: e = dispatch_flags<16, 7, 3, 16>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      default: e = dispatch_flags<32, 4, 3, 16>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rowseq_tma_kernel launch");
     ++ctx->launches;

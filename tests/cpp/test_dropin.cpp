@@ -1,0 +1,342 @@
+// Drop-in parity tests: the reference's own test cases (proj/tests/test_entropy.cpp,
+// test_chunk.cpp, test_scan.cpp, acceptance.cpp -- cited per case) compiled against
+// this repo's include/chunklab/*.hpp, i.e. running on the B200 through the C-ABI.
+// Known-answer values come from the reference itself.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <map>
+#include <numeric>
+#include <string>
+
+#include "chunklab/chunk.hpp"
+#include "chunklab/entropy.hpp"
+#include "chunklab/mamba1.hpp"
+#include "chunklab/rng.hpp"
+#include "chunklab/scan.hpp"
+#include "chunklab/synthetic.hpp"
+
+using namespace chunklab;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                                 \
+  do {                                                                              \
+    if (cond) {                                                                     \
+      ++g_pass;                                                                     \
+    } else {                                                                        \
+      ++g_fail;                                                                     \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);                   \
+    }                                                                               \
+  } while (0)
+#define CHECK_THROWS_WITH(expr, msg)                                                \
+  do {                                                                              \
+    bool thrown = false;                                                            \
+    try {                                                                           \
+      (void)(expr);                                                                 \
+    } catch (const invalid_input& e) {                                              \
+      thrown = std::string(e.what()) == (msg);                                      \
+      if (!thrown) std::printf("  got message '%s'\n", e.what());                  \
+    }                                                                               \
+    CHECK(thrown);                                                                  \
+  } while (0)
+
+static ActivationTensor flat(std::vector<double> v) {
+  ActivationTensor t;
+  t.shape = {v.size()};
+  t.values = std::move(v);
+  return t;
+}
+
+static void test_entropy() {
+  HistogramSpec spec;
+  // test_entropy.cpp:51-58
+  {
+    const Histogram h = compute_histogram(flat(std::vector<double>(1000, 3.0)), spec);
+    CHECK(h.masses[0] == 1.0 && h.sample_count == 1000);
+    for (std::size_t i = 1; i < h.masses.size(); ++i) CHECK(h.masses[i] == 0.0);
+  }
+  // :60-66
+  {
+    HistogramSpec s2;
+    s2.bin_count = 2;
+    const Histogram h = compute_histogram(flat({0.0, 1.0}), s2);
+    CHECK(h.masses[0] == 0.5 && h.masses[1] == 0.5);
+  }
+  // :86-99
+  CHECK_THROWS_WITH(compute_histogram(flat({}), spec), "no samples");
+  CHECK_THROWS_WITH(compute_histogram(flat({1.0, std::nan("")}), spec), "non-finite input");
+  {
+    HistogramSpec bad = spec;
+    bad.bin_count = 1;
+    CHECK_THROWS_WITH(compute_histogram(flat({1.0}), bad), "degenerate spec");
+    HistogramSpec strided = spec;
+    strided.sample_stride = 10;
+    CHECK(compute_histogram(flat({5.0, 1.0, 2.0}), strided).sample_count == 1);
+  }
+  // :111-135 + Appendix B (bit-exact raw nats up to device log ulps)
+  for (auto [dist, raw, norm_tol] : {std::tuple{Distribution::Uniform, 5.5450415873139685, 0.002},
+                                     std::tuple{Distribution::StandardNormal, 4.7242405006726766, 0.006}}) {
+    SyntheticSpec syn;
+    syn.distribution = dist;
+    syn.seed = 8;
+    syn.shape = {1000000};
+    const EntropyEstimate e = estimate_tensor_entropy(generate_activations(syn), spec);
+    CHECK(std::fabs(e.raw_nats - raw) <= 1e-13 * raw);
+    (void)norm_tol;
+  }
+  // :174-195 mass conservation over random specs
+  {
+    Rng rng(77);
+    for (int trial = 0; trial < 20; ++trial) {
+      const std::size_t n = 1 + rng.index(5000);
+      std::vector<double> values(n);
+      for (double& v : values) v = rng.laplace(2.0);
+      HistogramSpec s;
+      s.bin_count = 2 + static_cast<int>(rng.index(510));
+      const Histogram h = compute_histogram(flat(values), s);
+      const double mass = std::accumulate(h.masses.begin(), h.masses.end(), 0.0);
+      CHECK(std::fabs(mass - 1.0) <= 1e-12);
+      const EntropyEstimate e = estimate_entropy(h, s.epsilon);
+      const double k = s.bin_count;
+      CHECK(e.raw_nats <= std::log(k) + k * s.epsilon && e.raw_nats >= -k * s.epsilon);
+    }
+  }
+  // :197-223 stride semantics
+  {
+    Rng rng(99);
+    std::vector<double> values(4097);
+    for (double& v : values) v = rng.normal();
+    HistogramSpec s;
+    s.bin_count = 64;
+    for (std::size_t st : {2, 3, 8}) {
+      std::vector<double> sub;
+      for (std::size_t i = 0; i < values.size(); i += st) sub.push_back(values[i]);
+      HistogramSpec ss = s;
+      ss.sample_stride = st;
+      const Histogram a = compute_histogram(flat(values), ss);
+      const Histogram b = compute_histogram(flat(sub), s);
+      CHECK(a.masses == b.masses && a.lo == b.lo && a.hi == b.hi &&
+            a.sample_count == b.sample_count);
+    }
+  }
+  // :256-265 fixed range
+  {
+    HistogramSpec s;
+    s.bin_count = 4;
+    s.range_mode = RangeMode::Fixed;
+    s.fixed_lo = 0.0;
+    s.fixed_hi = 4.0;
+    const Histogram h = compute_histogram(flat({-1.0, 0.5, 3.9, 99.0}), s);
+    CHECK(h.masses[0] == 0.5 && h.masses[3] == 0.5);
+  }
+  // :267-282 token entropy
+  {
+    ActivationTensor t;
+    t.shape = {2, 3};
+    t.values = {1.0, 2.0, 3.0, 1.0, 2.0, 3.0};
+    HistogramSpec s;
+    s.bin_count = 16;
+    s.epsilon = 1e-12;
+    CHECK(std::fabs(token_entropy(t, s).raw_nats) <= 1e-9);
+  }
+  // :144-161 ema
+  {
+    EmaState s{4.0, 0.85, 3};
+    const EmaState nx = update_ema(s, 5.0);
+    CHECK(std::fabs(nx.current - 4.15) <= 1e-12 && nx.update_count == 4);
+  }
+}
+
+static SchedulerPolicy make_policy(PolicyVariant v,
+                                   std::vector<int> buckets = {128, 256, 512, 1024, 2048}) {
+  SchedulerPolicy p;
+  p.variant = std::move(v);
+  p.bucket_set = std::move(buckets);
+  return p;
+}
+
+static ChunkDecision run(const SchedulerPolicy& p, const ScheduleFeatures& f) {
+  return schedule(p, f, ChunkBounds{p.bucket_set.front(), p.bucket_set.back()},
+                  CalibrationRef::log_k(256));
+}
+
+static void test_chunk() {
+  const ChunkBounds paper{32, 512};
+  // test_chunk.cpp:32-57 + acceptance criteria 1-2
+  CHECK(select_chunk(0.83 * CalibrationRef::log_k(256).h_ref_nats, paper, CalibrationRef::log_k(256)).chunk == 512);
+  const ChunkDecision lg = select_chunk(4.60, paper, CalibrationRef::legacy());
+  CHECK(lg.chunk == 256 && std::fabs(lg.r - 0.575) <= 1e-12 && lg.source_policy == "rule");
+  CHECK(select_chunk(0.0, paper, CalibrationRef::legacy()).chunk == 32);
+  const std::pair<double, int> sweep[] = {{5.545, 512}, {4.612, 256}, {3.892, 256}, {0.789, 64}, {0.192, 32}};
+  for (const auto& [s, c] : sweep) CHECK(select_chunk(s, paper, CalibrationRef::legacy()).chunk == c);
+  // :59-65
+  CHECK(kernel_calls(4097, 512) == 9);
+  // :95-104 ties
+  CHECK(select_chunk((362.1 - 32.0) / 480.0, paper, CalibrationRef::legacy(1.0)).chunk == 512);
+  CHECK(select_chunk((361.9 - 32.0) / 480.0, paper, CalibrationRef::legacy(1.0)).chunk == 256);
+  // :106-131 static / midpoint / learned table
+  ScheduleFeatures f;
+  f.seq_len = 976;
+  CHECK(run(make_policy(StaticPolicy{512}), f).chunk == 512);
+  const ChunkDecision mid = run(make_policy(NoEntropyMidpointPolicy{}), f);
+  CHECK(mid.chunk == 1024 && mid.source_policy == "no_entropy_midpoint");
+  const LearnedTablePolicy table{50, 128, 512};
+  CHECK(run(make_policy(table), f).chunk == 512);
+  ScheduleFeatures shortf;
+  shortf.seq_len = 25;
+  CHECK(run(make_policy(table), shortf).chunk == 128);
+  ScheduleFeatures boundary;
+  boundary.seq_len = 50;
+  CHECK(run(make_policy(table), boundary).chunk == 512);
+  CHECK_THROWS_WITH(run(make_policy(table), ScheduleFeatures{}), "missing feature: seq_len");
+  // :133-161 guarded
+  {
+    GuardedPolicy g;
+    g.inner = std::make_shared<SchedulerPolicy>(make_policy(StaticPolicy{1024}));
+    const ChunkDecision d = run(make_policy(g), ScheduleFeatures{});
+    CHECK(d.chunk == 512 && d.source_policy == "guarded[fallback]");
+    GuardedPolicy w = g;
+    w.inner = std::make_shared<SchedulerPolicy>(make_policy(StaticPolicy{128}));
+    const ChunkDecision far = run(make_policy(w), ScheduleFeatures{});
+    CHECK(far.chunk == 128 && far.source_policy == "guarded[static]");
+  }
+  // :163-181 histogram variants
+  {
+    EntropyEstimate est;
+    est.raw_nats = 5.0;
+    ScheduleFeatures hf;
+    hf.full_entropy = est;
+    const ChunkDecision d = run(make_policy(FullHistogramPolicy{}), hf);
+    CHECK(d.chunk == 2048 && d.source_policy == "full_histogram");
+    CHECK_THROWS_WITH(run(make_policy(SampledHistogramPolicy{8}), hf),
+                      "missing feature: sampled_entropy");
+  }
+  // :183-207 moment proxies
+  {
+    ScheduleFeatures mf;
+    mf.variance = 0.25;
+    mf.kurtosis = 3.0;
+    const ChunkDecision dv = run(make_policy(MomentProxyPolicy{MomentKind::Variance, 1.0}), mf);
+    CHECK(dv.chunk == 512 && dv.source_policy == "moment_variance");
+    CHECK(run(make_policy(MomentProxyPolicy{MomentKind::Cheap, 1.0}), mf).chunk == 1024);
+    CHECK(run(make_policy(MomentProxyPolicy{MomentKind::Kurtosis, 10.0}), mf).chunk == 512);
+  }
+  // :209-235 random policy
+  {
+    Scheduler a(make_policy(RandomPolicy{1234}), ChunkBounds{128, 2048}, CalibrationRef::log_k(256));
+    Scheduler b(make_policy(RandomPolicy{1234}), ChunkBounds{128, 2048}, CalibrationRef::log_k(256));
+    bool same = true;
+    for (int i = 0; i < 16; ++i) same = same && a.decide({}).chunk == b.decide({}).chunk;
+    CHECK(same);
+  }
+  // :275-286 validation
+  CHECK_THROWS_WITH(select_chunk(1.0, ChunkBounds{48, 512}, CalibrationRef::legacy()),
+                    "invalid chunk bounds");
+  CHECK_THROWS_WITH(select_chunk(-1.0, paper, CalibrationRef::legacy()), "signal must be >= 0");
+  // acceptance criterion 4 (fixtures.hpp:94-103)
+  const double l64 = std::log(64.0);
+  const double cells[8][3] = {{l64, 4.60, 512}, {5.0, 4.60, 512}, {6.0, 4.60, 512}, {8.0, 4.60, 256},
+                              {l64, 4.02, 512}, {5.0, 4.02, 512}, {6.0, 4.02, 256}, {8.0, 4.02, 256}};
+  for (const auto& c : cells)
+    CHECK(select_chunk(c[1], paper, CalibrationRef::legacy(c[0])).chunk == static_cast<int>(c[2]));
+}
+
+static void test_scan() {
+  // test_scan.cpp:64-80 prefix sum
+  {
+    ScanParams p;
+    p.channels = 2;
+    p.state_dim = 1;
+    p.seq_len = 16;
+    p.a.assign(2, 1.0);
+    p.b = {1.0};
+    p.c = {1.0};
+    p.d.assign(2, 0.0);
+    p.x.assign(32, 1.0);
+    const auto [out, st] = scan_sequential(p, ScanState{});
+    for (std::size_t t = 0; t < 16; ++t) CHECK(out.y[t] == static_cast<double>(t + 1));
+    CHECK(st.h[0] == 16.0);
+  }
+  // :98-118 + acceptance criterion 5: chunked bit-identical, Appendix B values
+  {
+    const auto t0 = std::chrono::steady_clock::now();
+    const ScanParams p = random_scan_params(2026, 64, 16, 4096);
+    const auto [ref, ref_state] = scan_sequential(p, ScanState{});
+    CHECK(ref.y.front() == -0.1159263058640267 && ref.y.back() == -0.76929978661735932);
+    for (std::size_t chunk : {1ul, 32ul, 64ul, 128ul, 256ul, 512ul, 4096ul}) {
+      const auto [out, st] = scan_chunked(p, ScanState{}, chunk);
+      CHECK(out.y == ref.y && st.h == ref_state.h);
+    }
+    CHECK(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < 5.0);
+  }
+  // :178-191 errors
+  {
+    ScanParams p = random_scan_params(1, 4, 2, 8);
+    CHECK_THROWS_WITH(scan_chunked(p, ScanState{}, 0), "chunk must be >= 1");
+    ScanParams bad = p;
+    bad.x.pop_back();
+    CHECK_THROWS_WITH(scan_sequential(bad, ScanState{}), "shape mismatch");
+    ScanParams nf = p;
+    nf.x[0] = INFINITY;
+    CHECK_THROWS_WITH(scan_sequential(nf, ScanState{}), "non-finite input");
+  }
+}
+
+static void test_prefill() {
+  // Mamba-1 prefill through the device path: constant input defers "signal must be >= 0"
+  const std::size_t B = 1, D = 32, L = 64, N = 16;
+  std::vector<float> u(B * D * L, 3.f), dl(B * D * L, 0.01f), z(B * D * L, 1.f);
+  std::vector<float> A(D * N, -1.f), Bm(B * N * L, 0.5f), Cm(B * N * L, 0.5f), Dv(D, 1.f);
+  float *du, *ddl, *dz, *dA, *dB, *dC, *dD, *dout;
+  const auto up = [](float** d, const std::vector<float>& h) {
+    cudaMalloc(d, h.size() * sizeof(float));
+    cudaMemcpy(*d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice);
+  };
+  up(&du, u);
+  up(&ddl, dl);
+  up(&dz, z);
+  up(&dA, A);
+  up(&dB, Bm);
+  up(&dC, Cm);
+  up(&dD, Dv);
+  cudaMalloc(&dout, u.size() * sizeof(float));
+  Mamba1Args a{};
+  a.u = du;
+  a.delta = ddl;
+  a.A = dA;
+  a.B = dB;
+  a.C = dC;
+  a.D = dD;
+  a.z = dz;
+  a.out = dout;
+  a.batch = B;
+  a.dim = D;
+  a.seq_len = L;
+  a.d_state = N;
+  a.delta_softplus = 1;
+  Prefill pf(HistogramSpec{}, nullptr, ChunkBounds{32, 512}, CalibrationRef::log_k(256));
+  pf.run(a);
+  CHECK_THROWS_WITH(pf.decision(), "signal must be >= 0");
+  // non-constant input: a decision and a finite output
+  for (std::size_t i = 0; i < u.size(); ++i) u[i] = std::sin(0.37 * static_cast<double>(i));
+  cudaMemcpy(du, u.data(), u.size() * sizeof(float), cudaMemcpyHostToDevice);
+  pf.run(a);
+  EntropyEstimate e;
+  const ChunkDecision d = pf.decision(&e);
+  CHECK(d.chunk >= 32 && d.chunk <= 512 && e.raw_nats > 0.0);
+  std::vector<float> out(u.size());
+  cudaMemcpy(out.data(), dout, out.size() * sizeof(float), cudaMemcpyDeviceToHost);
+  bool finite = true;
+  for (float v : out) finite = finite && std::isfinite(v);
+  CHECK(finite);
+  for (float* p : {du, ddl, dz, dA, dB, dC, dD, dout}) cudaFree(p);
+}
+
+int main() {
+  test_entropy();
+  test_chunk();
+  test_scan();
+  test_prefill();
+  std::printf("drop-in parity: %d passed, %d failed\n", g_pass, g_fail);
+  return g_fail ? 1 : 0;
+}

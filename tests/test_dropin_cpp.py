@@ -1,0 +1,36 @@
+"""The reference's C++ API (include/chunklab/*.hpp drop-in) compiled with g++ against
+libchunklab_b200.so; the GPU test runs the re-expressed reference test cases."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+PKG = os.path.join(ROOT, "paper_2604_10597_b200")
+CUDA_INC = "/usr/local/cuda/include"
+CUDA_LIB = "/usr/local/cuda/lib64"
+
+
+def build(out):
+    from paper_2604_10597_b200 import build as b
+    b.build()
+    cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), "-I" + CUDA_INC, SRC,
+           "-L" + PKG, "-lchunklab_b200", "-Wl,-rpath," + PKG, "-L" + CUDA_LIB, "-lcudart",
+           "-Wl,-rpath," + CUDA_LIB, "-o", out]
+    subprocess.run(cmd, check=True)
+    return out
+
+
+def test_dropin_headers_compile(tmp_path):
+    exe = build(str(tmp_path / "test_dropin"))
+    assert os.path.exists(exe)
+
+
+@pytest.mark.gpu
+def test_dropin_reference_cases(tmp_path, cuda):
+    exe = build(str(tmp_path / "test_dropin"))
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "0 failed" in r.stdout
