@@ -281,22 +281,32 @@ def main():
     n_total = pf.n_samples(n_local * world)
     uf = x["u"].reshape(-1)
 
+    from paper_2604_10597_b200.sharded import DeviceStages, plan_rows, sharded_entropy_decision
+    plan = plan_rows(global_batch, dim, L, rank, world)
+    assert plan.b0 * dim * L == g0 and plan.local_batch == batch
+    stages = DeviceStages(pf)
+
     def step(ev=None):
         if ev:
             ev[0].record()
-        pf.stage_minmax(uf, g0)
         if world > 1:
-            dist.all_reduce(pf.range, op=dist.ReduceOp.MAX)
-        if ev:
-            ev[1].record()
-        pf.stage_histogram(uf, g0)
-        if world > 1:
-            dist.all_reduce(pf.counts, op=dist.ReduceOp.SUM)
-        if ev:
-            ev[2].record()
-        pf.stage_decide(n_total, L)
-        if ev:
-            ev[3].record()
+            # the product multi-GPU protocol: MAX-allreduce of the range, SUM-allreduce
+            # of the counts, identical device decision on every rank
+            sharded_entropy_decision(stages, uf, plan, int(spec.sample_stride))
+            if ev:
+                ev[1].record()
+                ev[2].record()
+                ev[3].record()
+        else:
+            pf.stage_minmax(uf, g0)
+            if ev:
+                ev[1].record()
+            pf.stage_histogram(uf, g0)
+            if ev:
+                ev[2].record()
+            pf.stage_decide(n_total, L)
+            if ev:
+                ev[3].record()
         pf.stage_scan(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"],
                       x["delta_bias"], True, out, True)
         if ev:
