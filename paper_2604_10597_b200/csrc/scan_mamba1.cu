@@ -1090,6 +1090,7 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       case 25: e = dispatch_pair<16, 12, 3, 16>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
       case 26: e = dispatch_flags<16, 7, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
       case 27: e = dispatch_flags<16, 7, 3, 16>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+      case 28:
       default: e = dispatch_flags<32, 4, 3, 16>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rowseq_tma_kernel launch");

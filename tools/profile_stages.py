@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--variant", default="auto")
     ap.add_argument("--chunk", type=int, default=0, help="fixed chunk (0 = device rule)")
+    ap.add_argument("--no-softplus", action="store_true")
+    ap.add_argument("--no-z", action="store_true")
     args = ap.parse_args()
     batch, dim, L, N, _ = bench.CONFIGS[args.config]
     dev = torch.device("cuda", 0)
@@ -39,11 +41,13 @@ def main():
         ev[2].record()
         pf.stage_decide(pf.n_samples(uf.numel()), L)
         ev[3].record()
-        if args.chunk:
+        sp = not args.no_softplus
+        zz = None if args.no_z else x["z"]
+        if args.chunk or args.no_softplus or args.no_z:
             from paper_2604_10597_b200.mamba1 import selective_scan_fn
-            selective_scan_fn(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"],
-                              x["delta_bias"], True, False, args.chunk, variant=args.variant,
-                              out=out)
+            selective_scan_fn(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], zz,
+                              x["delta_bias"], sp, False, args.chunk or 512,
+                              variant=args.variant, out=out)
         else:
             pf.stage_scan(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"],
                           x["delta_bias"], True, out, False, variant=args.variant)
