@@ -11,7 +11,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libchunklab_b200.so")
+LIB_PATH = os.environ.get("CHUNKLAB_LIB", os.path.join(PKG, "libchunklab_b200.so"))
 
 CL_OK, CL_E_INVALID, CL_E_CUDA, CL_E_DEVICE, CL_E_NOMEM = range(5)
 CL_RANGE_DYNAMIC, CL_RANGE_FIXED = 0, 1

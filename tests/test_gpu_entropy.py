@@ -246,3 +246,29 @@ def test_unaligned_and_tiny_inputs(cuda, port):
             assert (pf.counts.cpu().numpy().astype(np.uint64) == oc).all(), (off, n)
             r = pf.range.cpu().numpy()
             assert -r[0] == olo and r[1] == ohi
+
+
+def test_repeated_runs_deterministic(cuda, port, golden):
+    """Counts must be identical over repeated launches (catches cross-warp counter races,
+    e.g. padding samples of a partial chunk addressing another warp's rows)."""
+    meta, arrays = golden
+    m = meta["hist"]["uniform"]
+    v32 = _gen(port, m).astype(np.float32)
+    ref = arrays["uniform_counts_f32"]
+    for _ in range(20):
+        counts, *_ = _device_counts(cuda, v32, 256, 1)
+        assert (counts == ref).all()
+
+
+def test_strided_unsampled_outliers(cuda, port):
+    """Unsampled elements far outside the sampled range must not touch any counter."""
+    rng = np.random.default_rng(9)
+    v = rng.standard_normal(1 << 18).astype(np.float32)
+    for s in (2, 3, 8):
+        w = v.copy()
+        idx = np.arange(w.size)
+        w[idx % s != 0] *= 1e6  # only unsampled positions get huge magnitudes
+        for _ in range(3):
+            counts, lo, hi, _ = _device_counts(cuda, w, 256, s)
+            oc, olo, ohi, _ = port.histogram(w, 256, 1e-8, s)
+            assert (counts == oc).all() and lo == olo and hi == ohi
