@@ -374,7 +374,7 @@ def main():
                    "l2": "inputs (1.07 GB per tensor) exceed the 126 MB L2; no flush needed"},
         "hbm_gbs": step_gbs, "roofline_frac_step": step_gbs / peak,
         "roofline": {"bound": "hbm", "achieved": scan_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": scan_gbs / peak, "traffic": traffic, "kernel": "rowseq_tma_kernel",
+                     "frac": scan_gbs / peak, "traffic": traffic, "kernel": "rowpair_ws_kernel",
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": ab["scan"]},
         "stage_ms": {k: statistics.mean(v) for k, v in stage_ms.items()},

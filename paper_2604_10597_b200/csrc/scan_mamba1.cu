@@ -7,18 +7,19 @@
 //   h_s    = exp(delta'*A[c,s]) * h_s + B[b,s,t] * (delta'*u)     s = 0..N-1
 //   y      = (sum_s C[b,s,t]*h_s + D[c]*u) * z*sigmoid(z)
 //
-// Two kernels:
-//   * rowseq_tma_kernel (the hot path, N = 16): one thread owns one (b, c) row
-//     and keeps its 16 states in registers.  A warp owns a 32-row tile; each
-//     warp runs its own 3-stage TMA pipeline (cp.async.bulk.tensor, 128B
-//     swizzle) over 32-timestep boxes of u / delta / z and the tile's B / C
-//     boxes, writes y in place of u and TMA-stores it.  Work items are
-//     (row tile, L-segment) pairs with segment length = the chunk chosen by the
-//     device rule (read from device memory, rounded up to whole boxes),
-//     dispatched in segment-major order through an atomic ticket; the state
-//     carry between consecutive segments of a tile is a chained scan (flag +
-//     release/acquire), so chunking never changes a single floating-point
-//     operation: outputs are bit-identical for every chunk size.
+// Kernels:
+//   * rowpair_ws_kernel (the hot path, N = 16): warp-specialised.  Consumer warps own
+//     16-row tiles (two lanes per (b, c) row, 8 states each in FFMA2 register pairs);
+//     producer warps feed each consumer a 2-stage TMA ring of 16-timestep boxes
+//     (u / delta / z with 64B swizzle, one interleaved [B^T | C^T] box).  y is stored
+//     from registers.  Work items are (row tile, L-segment) pairs with segment length
+//     = the chunk chosen by the device rule (read from device memory, rounded up to
+//     whole boxes), dispatched segment-major through an atomic ticket; the state carry
+//     between consecutive segments of a tile is a chained scan (flag + release /
+//     acquire), so chunking never changes a single floating-point operation: outputs
+//     are bit-identical for every chunk size.
+//   * rowseq_tma_kernel: one lane per row (32-row tiles), each warp feeding its own
+//     TMA ring and TMA-storing y; kept as a selectable variant (CL_SCAN_CFG=1..3).
 //   * generic_kernel: any N <= 64, any alignment; one thread per row, direct loads.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(128) generic_kernel(GenericArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// TMA row-sequential kernel (N = 16)
+// TMA kernels (N = 16): shared helpers, then the 32-row row-sequential kernel
 // ---------------------------------------------------------------------------
 constexpr int kN = 16;
 constexpr int kRows = 32;  // rows per tile = lanes per warp
@@ -141,6 +142,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             int c2, uint64_t* bar) {
   asm volatile(
@@ -157,9 +174,6 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
       "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
       : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read_all() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_read_le1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -205,45 +219,13 @@ __device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
   return r;
 }
 
-// 2^x on the FMA pipe for a pair (Cody-Waite split + degree-5 minimax on [-0.5, 0.5],
-// max rel err 2.4e-7 in fp32, same class as MUFU.EX2): lets the kernel move part of
-// the 16 exponentials per element off the MUFU (the scan's binding pipe).
-__device__ __forceinline__ f2_t exp2_poly2(f2_t x) {
-  float a, b;
-  upk(x, a, b);
-  a = fminf(fmaxf(a, -127.f), 127.f);
-  b = fminf(fmaxf(b, -127.f), 127.f);
-  const f2_t magic = pk(12582912.0f, 12582912.0f);
-  const f2_t t = add2(pk(a, b), magic);
-  const f2_t j = add2(t, pk(-12582912.0f, -12582912.0f));
-  const f2_t f = add2(pk(a, b), mul2(j, pk(-1.f, -1.f)));
-  f2_t p = pk(0.001327816391980198f, 0.001327816391980198f);
-  p = fma2(p, f, pk(0.00967555578392905f, 0.00967555578392905f));
-  p = fma2(p, f, pk(0.055507080479488276f, 0.055507080479488276f));
-  p = fma2(p, f, pk(0.2402211936420041f, 0.2402211936420041f));
-  p = fma2(p, f, pk(0.6931469702538122f, 0.6931469702538122f));
-  p = fma2(p, f, pk(1.0000000717654767f, 1.0000000717654767f));
-  float pl, ph, tl, th;
-  upk(p, pl, ph);
-  upk(t, tl, th);
-  pl = __int_as_float(__float_as_int(pl) + (__float_as_int(tl) << 23));
-  ph = __int_as_float(__float_as_int(ph) + (__float_as_int(th) << 23));
-  return pk(pl, ph);
-}
-
 // softplus for a pair, branch-free: max(x,0) + log1p(exp(-|x|)), log1p by a degree-9
 // minimax polynomial on [0,1] (max rel err 2e-7 in fp32).  Equals x to fp32 precision
 // above 20, matching mamba_ssm's threshold.
-template <bool POLY = false>
 __device__ __forceinline__ f2_t softplus2(f2_t x) {
   float a, b;
   upk(x, a, b);
-  f2_t e;
-  if (POLY) {
-    e = exp2_poly2(pk(-fabsf(a) * kLog2e, -fabsf(b) * kLog2e));
-  } else {
-    e = pk(ex2_approx(-fabsf(a) * kLog2e), ex2_approx(-fabsf(b) * kLog2e));
-  }
+  const f2_t e = pk(ex2_approx(-fabsf(a) * kLog2e), ex2_approx(-fabsf(b) * kLog2e));
   f2_t q = pk(0.005253826278033571f, 0.005253826278033571f);
   q = fma2(q, e, pk(-0.02959069552080005f, -0.02959069552080005f));
   q = fma2(q, e, pk(0.07836660226277938f, 0.07836660226277938f));
@@ -258,16 +240,11 @@ __device__ __forceinline__ f2_t softplus2(f2_t x) {
 
 // z * sigmoid(z) for a pair: one MUFU.EX2 per lane, reciprocal by Newton iterations
 // on the FMA pipe (3 steps from the bit-trick seed: rel err < 1e-7).
-template <bool POLY = false>
 __device__ __forceinline__ f2_t silu2(f2_t z) {
   float a, b;
   upk(z, a, b);
-  f2_t e;
-  if (POLY) {
-    e = exp2_poly2(pk(fmaxf(a, -80.f) * -kLog2e, fmaxf(b, -80.f) * -kLog2e));
-  } else {
-    e = pk(ex2_approx(fmaxf(a, -80.f) * -kLog2e), ex2_approx(fmaxf(b, -80.f) * -kLog2e));
-  }
+  const f2_t e =
+      pk(ex2_approx(fmaxf(a, -80.f) * -kLog2e), ex2_approx(fmaxf(b, -80.f) * -kLog2e));
   const f2_t d = add2(e, pk(1.f, 1.f));
   float dl, dh;
   upk(d, dl, dh);
@@ -285,6 +262,7 @@ __device__ __forceinline__ f2_t silu2(f2_t z) {
 
 struct TmaArgs {
   const float *A, *D, *bias, *h0;
+  float* out;              // y, for the direct-store (warp-specialised) kernel
   float* h_last;
   float* carry;            // [n_tiles][32][16]
   unsigned int* flags;     // [n_tiles] completed segments
@@ -321,7 +299,7 @@ constexpr int warp_bytes() {
   return STAGES * Geo<BOX>::kStageBytes + 2 * Geo<BOX>::kTileBytes;  // + 2 y staging buffers
 }
 
-template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int EMU>
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     rowseq_tma_kernel(const __grid_constant__ CUtensorMap map_u,
                       const __grid_constant__ CUtensorMap map_dt,
@@ -471,8 +449,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       // elementwise prologue for the 4 timesteps, packed in pairs
       f2_t dt01 = add2(pk(d4.x, d4.y), bias2), dt23 = add2(pk(d4.z, d4.w), bias2);
       if (SP) {
-        dt01 = softplus2<(EMU >= 16)>(dt01);
-        dt23 = softplus2<(EMU >= 16)>(dt23);
+        dt01 = softplus2(dt01);
+        dt23 = softplus2(dt23);
       }
       const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
       float dt[4], xs[4];
@@ -489,14 +467,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         const f2_t dd = pk(dt[k], dt[k]);
 #pragma unroll
         for (int i = 0; i < kN / 2; ++i) {
-          const f2_t arg = mul2(A2p[i], dd);
-          if (i < (EMU % 16)) {
-            dA[k][i] = exp2_poly2(arg);
-          } else {
-            float al, ah;
-            upk(arg, al, ah);
-            dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
-          }
+          float al, ah;
+          upk(mul2(A2p[i], dd), al, ah);
+          dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
         }
       }
       // phase B: recurrence h = dA*h + B*x and y = C.h, FFMA2 on state pairs
@@ -525,8 +498,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       f2_t y23 = fma2(pk(Dc, Dc), pk(uu[2], uu[3]), pk(yy[2], yy[3]));
       if (HZ) {
         const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
-        y01 = mul2(y01, silu2<(EMU >= 16)>(pk(z4.x, z4.y)));
-        y23 = mul2(y23, silu2<(EMU >= 16)>(pk(z4.z, z4.w)));
+        y01 = mul2(y01, silu2(pk(z4.x, z4.y)));
+        y23 = mul2(y23, silu2(pk(z4.z, z4.w)));
       }
       float o0, o1, o2, o3;
       upk(y01, o0, o1);
@@ -572,24 +545,32 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Lane-pair variant: a warp owns a 16-row tile; lanes (2r, 2r+1) share row r and
-// hold states 0-7 / 8-15.  Twice the independent row chains of the 32-row kernel
-// for the same shape (the chained-segment schedule caps busy warps at the tile
-// count), at the cost of one 64-bit shuffle pair per 4 timesteps.
+// Warp-specialised lane-pair kernel (the hot path).
+//
+// Layout: a consumer warp owns a 16-row tile; lanes (2r, 2r+1) share row r and hold
+// states 0-7 / 8-15 as FFMA2 register pairs.  That doubles the independent row
+// chains of the 32-row kernel for the same shape (the chained-segment schedule caps
+// busy warps at the tile count: 2048 tiles at C3 = 13.8 warps per SM), at the cost
+// of one 64-bit shuffle pair per 4 timesteps.
+//
+// Roles: WARPS consumer warps only compute; NPROD producer warps run the consumers'
+// TMA rings (lane l of producer p owns consumer p*ceil(WARPS/NPROD) + l): ticket
+// claims, expect_tx and the four tile loads per box (u, delta, z and one interleaved
+// [B | C] box).  Measured on C3: issuing TMA from the compute warps cost ~10% of
+// the scan, one producer warp could not keep up with 14 consumers (its per-lane
+// TMA issue serialises through uniform registers), two can.  y is stored straight
+// from registers (8 B per lane per 4 timesteps, st.global.cs): the four stores of a
+// box complete each 64-byte row segment in L2 within microseconds, and dropping the
+// y staging buffer, proxy fence and TMA store saved another ~3%.
 // ---------------------------------------------------------------------------
 constexpr int kRowsP = 16;
 
 template <int BOX>
 struct GeoP {
-  static constexpr int kTileBytes = kRowsP * BOX * 4;
-  static constexpr int kBCBytes = BOX * kN * 4;
-  static constexpr int kStageBytes = 3 * kTileBytes + 2 * kBCBytes;
+  static constexpr int kTileBytes = kRowsP * BOX * 4;  // u / delta / z: [16 rows][BOX]
+  static constexpr int kBCBytes = BOX * 2 * kN * 4;    // [BOX][B 0..15 | C 0..15]
+  static constexpr int kStageBytes = 3 * kTileBytes + kBCBytes;
 };
-
-template <int BOX, int STAGES>
-constexpr int warp_bytes_p() {
-  return STAGES * GeoP<BOX>::kStageBytes + 2 * GeoP<BOX>::kTileBytes;
-}
 
 __device__ __forceinline__ f2_t shfl_xor2(f2_t v, int m) {
   float lo, hi;
@@ -597,14 +578,98 @@ __device__ __forceinline__ f2_t shfl_xor2(f2_t v, int m) {
   return pk(__shfl_xor_sync(0xffffffffu, lo, m), __shfl_xor_sync(0xffffffffu, hi, m));
 }
 
-template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int EMU>
-__global__ void __launch_bounds__(WARPS * 32, 1)
-    rowpair_tma_kernel(const __grid_constant__ CUtensorMap map_u,
-                       const __grid_constant__ CUtensorMap map_dt,
-                       const __grid_constant__ CUtensorMap map_z,
-                       const __grid_constant__ CUtensorMap map_out,
-                       const __grid_constant__ CUtensorMap map_Bt,
-                       const __grid_constant__ CUtensorMap map_Ct, TmaArgs a) {
+// One 16-row x BOX-timestep box: lane (r, hf) owns row r's states 8hf..8hf+7.  Reads
+// u / delta / z / [B | C] from the TMA stage `st`, advances the carried state h2 and
+// stores y for timesteps (4j + 2hf, 4j + 2hf + 1) of row r to ydst (nullptr: pad row).
+template <int BOX, bool SP, bool HZ>
+__device__ __forceinline__ void pair_box(const unsigned char* st, float* ydst, int r, int hf,
+                                         int valid, float bias, float Dc,
+                                         const f2_t (&A2p)[kN / 4], f2_t (&h2)[kN / 4]) {
+  using G = GeoP<BOX>;
+  constexpr int kP = kN / 4;
+  constexpr int kBCRow = 2 * kN * 4;
+  const unsigned char* sB = st + 3 * G::kTileBytes + 32 * hf;  // this lane's 8 states
+  const unsigned char* sC = sB + kN * 4;
+  const f2_t bias2 = pk(bias, bias);
+  // fully unrolled over the box's 4-timestep groups: straight-line code lets the
+  // scheduler interleave group j+1's exponentials with group j's FFMA2 chains
+#pragma unroll
+  for (int j = 0; j < BOX / 4; ++j) {
+    if (4 * j >= valid) break;
+    const int off = Geo<BOX>::swz(r, j);
+    const float4 u4 = *reinterpret_cast<const float4*>(st + off);
+    const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
+    // softplus of timesteps (2hf, 2hf+1) here, the other pair from the partner lane
+    f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
+    if (SP) mine = softplus2(mine);
+    const f2_t other = shfl_xor2(mine, 1);
+    const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
+    const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
+    float dt[4], xs[4];
+    upk(dt01, dt[0], dt[1]);
+    upk(dt23, dt[2], dt[3]);
+    upk(x01, xs[0], xs[1]);
+    upk(x23, xs[2], xs[3]);
+    // the 4x8 transition factors exp(dt*A) do not depend on the state: issue them all
+    f2_t dA[4][kP];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const f2_t dd = pk(dt[k], dt[k]);
+#pragma unroll
+      for (int i = 0; i < kP; ++i) {
+        float al, ah;
+        upk(mul2(A2p[i], dd), al, ah);
+        dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+      }
+    }
+    float yp[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = 4 * j + k;
+      const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + t * kBCRow);
+      const ulonglong2* Ct = reinterpret_cast<const ulonglong2*>(sC + t * kBCRow);
+      const f2_t xx = pk(xs[k], xs[k]);
+      f2_t ya = 0ull, yb = 0ull;
+#pragma unroll
+      for (int q = 0; q < kP / 2; ++q) {
+        const ulonglong2 bq = Bt[q];
+        const ulonglong2 cq = Ct[q];
+        h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
+        h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
+        ya = fma2(cq.x, h2[2 * q], ya);
+        yb = fma2(cq.y, h2[2 * q + 1], yb);
+      }
+      float a0, a1;
+      upk(add2(ya, yb), a0, a1);
+      yp[k] = a0 + a1;
+    }
+    // lane hf finalises timesteps (2hf, 2hf+1): swap the partial sums it does not own
+    const f2_t keep = hf ? pk(yp[2], yp[3]) : pk(yp[0], yp[1]);
+    const f2_t give = hf ? pk(yp[0], yp[1]) : pk(yp[2], yp[3]);
+    const f2_t ysum = add2(keep, shfl_xor2(give, 1));
+    const f2_t u2 = hf ? pk(u4.z, u4.w) : pk(u4.x, u4.y);
+    f2_t yo = fma2(pk(Dc, Dc), u2, ysum);
+    if (HZ) {
+      const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
+      yo = mul2(yo, silu2(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y)));
+    }
+    if (ydst) {
+      float y0, y1;
+      upk(yo, y0, y1);
+      __stcs(reinterpret_cast<float2*>(ydst + 4 * j + 2 * hf), make_float2(y0, y1));
+    }
+  }
+}
+
+// Per consumer warp and stage: full[s] (producer arrive.expect_tx + TMA bytes) and
+// empty[s] (consumer lane 0 arrive after its last shared-memory read of the stage).
+// The meta words (item, box) travel through shared memory under full[s]'s release.
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int NPROD>
+__global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
+    rowpair_ws_kernel(const __grid_constant__ CUtensorMap map_u,
+                      const __grid_constant__ CUtensorMap map_dt,
+                      const __grid_constant__ CUtensorMap map_z,
+                      const __grid_constant__ CUtensorMap map_bc, TmaArgs a) {
   using G = GeoP<BOX>;
   int status;
   const int chunk = read_chunk(a.decision, a.fixed_chunk, &status);
@@ -618,22 +683,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int r = lane >> 1, hf = lane & 1;
-  constexpr int kWB = warp_bytes_p<BOX, STAGES>();
-  unsigned char* wbase = smem + size_t(warp) * kWB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(WARPS) * kWB) + warp * 4;
-  int meta_item[STAGES], meta_box[STAGES];
+  constexpr int kWB = STAGES * G::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(WARPS) * kWB);  // [WARPS][STAGES]
+  uint64_t* empty = full + WARPS * STAGES;                                  // [WARPS][STAGES]
+  int2* meta = reinterpret_cast<int2*>(empty + WARPS * STAGES);              // [WARPS][STAGES]
 
-  if (lane == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(bars + s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_u)));
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_dt)));
-    if (HZ) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_z)));
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_Bt)));
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_Ct)));
+  if (threadIdx.x < WARPS * STAGES) {
+    mbar_init(full + threadIdx.x, 1);
+    mbar_init(empty + threadIdx.x, 1);
   }
-  __syncwarp();
+  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
 
   auto decode = [&](int id) {
     Item it;
@@ -644,44 +704,69 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     it.nbox = (len + BOX - 1) / BOX;
     return it;
   };
-  auto claim = [&]() {
-    int id = 0;
-    if (lane == 0) id = static_cast<int>(atomicAdd(a.ticket, 1u));
-    return __shfl_sync(0xffffffffu, id, 0);
-  };
 
-  int p_item = claim();
-  int p_box = 0;
-  Item p_it = decode(p_item);
-  auto produce = [&](int slot) {
-    meta_item[slot] = -1;
-    if (p_item >= n_items) return;
-    const Item it = p_it;
-    meta_item[slot] = p_item;
-    meta_box[slot] = p_box;
-    if (lane == 0) {
-      unsigned char* st = wbase + slot * G::kStageBytes;
-      const int b = it.tile / a.tiles_per_batch;
-      const int r0 = (it.tile % a.tiles_per_batch) * kRowsP;
-      const int t = it.t0 + p_box * BOX;
-      mbar_expect_tx(bars + slot, HZ ? G::kStageBytes : G::kStageBytes - G::kTileBytes);
-      tma_load_3d(st, &map_u, t, r0, b, bars + slot);
-      tma_load_3d(st + G::kTileBytes, &map_dt, t, r0, b, bars + slot);
-      if (HZ) tma_load_3d(st + 2 * G::kTileBytes, &map_z, t, r0, b, bars + slot);
-      tma_load_3d(st + 3 * G::kTileBytes, &map_Bt, 0, t, b, bars + slot);
-      tma_load_3d(st + 3 * G::kTileBytes + G::kBCBytes, &map_Ct, 0, t, b, bars + slot);
+  if (warp >= WARPS) {
+    // ---------------- producers ----------------
+    constexpr int kPer = (WARPS + NPROD - 1) / NPROD;
+    const int w = (warp - WARPS) * kPer + lane;
+    bool live = lane < kPer && w < WARPS;
+    if (lane == 0 && warp == WARPS) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_u)));
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_dt)));
+      if (HZ) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_z)));
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bc)));
     }
-    if (++p_box == it.nbox) {
-      p_box = 0;
-      p_item = claim();
-      p_it = decode(p_item);
+    // boxes go through each consumer's ring in ticket order
+    int p_item = live ? static_cast<int>(atomicAdd(a.ticket, 1u)) : 0;
+    Item p_it = decode(p_item);
+    int p_b = p_it.tile / a.tiles_per_batch, p_r0 = (p_it.tile % a.tiles_per_batch) * kRowsP;
+    int p_box = 0, n_issued = 0;
+    unsigned char* wbase = smem + size_t(w < WARPS ? w : 0) * kWB;
+    while (__any_sync(0xffffffffu, live)) {
+      bool issued = false;
+      if (live) {
+        const int slot = n_issued % STAGES;
+        const bool free = n_issued < STAGES ||
+                          mbar_test(empty + w * STAGES + slot, ((n_issued / STAGES) - 1) & 1);
+        if (free) {
+          uint64_t* bar = full + w * STAGES + slot;
+          if (p_item >= n_items) {
+            meta[w * STAGES + slot] = make_int2(-1, 0);
+            mbar_arrive(bar);
+            live = false;
+          } else {
+            meta[w * STAGES + slot] = make_int2(p_item, p_box);
+            unsigned char* st = wbase + slot * G::kStageBytes;
+            const int t = p_it.t0 + p_box * BOX;
+            mbar_expect_tx(bar, HZ ? G::kStageBytes : G::kStageBytes - G::kTileBytes);
+            tma_load_3d(st, &map_u, t, p_r0, p_b, bar);
+            tma_load_3d(st + G::kTileBytes, &map_dt, t, p_r0, p_b, bar);
+            if (HZ) tma_load_3d(st + 2 * G::kTileBytes, &map_z, t, p_r0, p_b, bar);
+            tma_load_3d(st + 3 * G::kTileBytes, &map_bc, 0, t, p_b, bar);
+            if (++p_box == p_it.nbox) {
+              p_box = 0;
+              p_item = static_cast<int>(atomicAdd(a.ticket, 1u));
+              p_it = decode(p_item);
+              p_b = p_it.tile / a.tiles_per_batch;
+              p_r0 = (p_it.tile % a.tiles_per_batch) * kRowsP;
+            }
+          }
+          ++n_issued;
+          issued = true;
+        }
+      }
+      if (!__any_sync(0xffffffffu, issued)) __nanosleep(32);
     }
-  };
+    return;
+  }
 
-  for (int s = 0; s < STAGES; ++s) produce(s);
-
-  unsigned char* ybuf0 = wbase + STAGES * G::kStageBytes;
-  constexpr int kP = kN / 4;  // state pairs per lane
+  // ---------------- consumers ----------------
+  const int r = lane >> 1, hf = lane & 1;
+  const unsigned char* wbase = smem + size_t(warp) * kWB;
+  uint64_t* wfull = full + warp * STAGES;
+  uint64_t* wempty = empty + warp * STAGES;
+  const int2* wmeta = meta + warp * STAGES;
+  constexpr int kP = kN / 4;
   f2_t h2[kP], A2p[kP];
   float bias = 0.f, Dc = 0.f;
   Item cur{};
@@ -689,11 +774,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   bool row_valid = false;
   for (int iter = 0;; ++iter) {
     const int slot = iter % STAGES;
-    const int item = meta_item[slot];
-    if (item < 0) break;
-    const int box = meta_box[slot];
+    mbar_wait(wfull + slot, (iter / STAGES) & 1);
+    const int2 m = wmeta[slot];
+    if (m.x < 0) break;
+    const int box = m.y;
     if (box == 0) {
-      cur = decode(item);
+      cur = decode(m.x);
       const int b = cur.tile / a.tiles_per_batch;
       const int c = (cur.tile % a.tiles_per_batch) * kRowsP + r;
       row_valid = c < static_cast<int>(a.dim);
@@ -711,6 +797,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       if (cur.seg == 0) {
         src = a.h0 ? a.h0 + size_t(row) * kN + 8 * hf : nullptr;
       } else {
+        // chained carry from segment seg-1 of this tile
         if (lane == 0)
           while (ld_acquire(a.flags + cur.tile) < static_cast<unsigned>(cur.seg)) __nanosleep(64);
         __syncwarp();
@@ -725,91 +812,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
       }
     }
 
-    mbar_wait(bars + slot, (iter / STAGES) & 1);
-    unsigned char* ybuf = ybuf0 + (iter & 1) * G::kTileBytes;
-    if (lane == 0) bulk_wait_read_le1();
-    __syncwarp();
-    unsigned char* st = wbase + slot * G::kStageBytes;
-    const unsigned char* sB = st + 3 * G::kTileBytes + 32 * hf;  // this lane's 8 states
-    const unsigned char* sC = sB + G::kBCBytes;
     const int tbox = cur.t0 + box * BOX;
-    const int valid = min(BOX, L - tbox);
-    const f2_t bias2 = pk(bias, bias);
-    // fully unrolled over the box's 4-timestep groups: straight-line code lets the
-    // scheduler interleave group j+1's exponentials with group j's FFMA2 chains
-#pragma unroll
-    for (int j = 0; j < BOX / 4; ++j) {
-      if (4 * j >= valid) break;
-      const int off = Geo<BOX>::swz(r, j);
-      const float4 u4 = *reinterpret_cast<const float4*>(st + off);
-      const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
-      // softplus of timesteps (2hf, 2hf+1) here, the other pair from the partner lane
-      f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
-      if (SP) mine = softplus2<(EMU >= 16)>(mine);
-      const f2_t other = shfl_xor2(mine, 1);
-      const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
-      const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
-      float dt[4], xs[4];
-      upk(dt01, dt[0], dt[1]);
-      upk(dt23, dt[2], dt[3]);
-      upk(x01, xs[0], xs[1]);
-      upk(x23, xs[2], xs[3]);
-      f2_t dA[4][kP];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const f2_t dd = pk(dt[k], dt[k]);
-#pragma unroll
-        for (int i = 0; i < kP; ++i) {
-          const f2_t arg = mul2(A2p[i], dd);
-          if (i < (EMU % 16)) {
-            dA[k][i] = exp2_poly2(arg);
-          } else {
-            float al, ah;
-            upk(arg, al, ah);
-            dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
-          }
-        }
-      }
-      float yp[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int t = 4 * j + k;
-        const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + t * kN * 4);
-        const ulonglong2* Ct = reinterpret_cast<const ulonglong2*>(sC + t * kN * 4);
-        const f2_t xx = pk(xs[k], xs[k]);
-        f2_t ya = 0ull, yb = 0ull;
-#pragma unroll
-        for (int q = 0; q < kP / 2; ++q) {
-          const ulonglong2 bq = Bt[q];
-          const ulonglong2 cq = Ct[q];
-          h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
-          h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
-          ya = fma2(cq.x, h2[2 * q], ya);
-          yb = fma2(cq.y, h2[2 * q + 1], yb);
-        }
-        float a0, a1;
-        upk(add2(ya, yb), a0, a1);
-        yp[k] = a0 + a1;
-      }
-      // lane hf finalises timesteps (2hf, 2hf+1): swap the partial sums it does not own
-      const f2_t keep = hf ? pk(yp[2], yp[3]) : pk(yp[0], yp[1]);
-      const f2_t give = hf ? pk(yp[0], yp[1]) : pk(yp[2], yp[3]);
-      const f2_t ysum = add2(keep, shfl_xor2(give, 1));
-      const f2_t u2 = hf ? pk(u4.z, u4.w) : pk(u4.x, u4.y);
-      f2_t yo = fma2(pk(Dc, Dc), u2, ysum);
-      if (HZ) {
-        const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
-        yo = mul2(yo, silu2<(EMU >= 16)>(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y)));
-      }
-      *reinterpret_cast<f2_t*>(ybuf + off + 8 * hf) = yo;
-    }
-    fence_proxy_async();
+    pair_box<BOX, SP, HZ>(wbase + slot * G::kStageBytes,
+                          row_valid ? a.out + size_t(row) * a.L + tbox : nullptr, r, hf,
+                          min(BOX, L - tbox), bias, Dc, A2p, h2);
     __syncwarp();
-    if (lane == 0) {
-      const int b = cur.tile / a.tiles_per_batch;
-      const int r0 = (cur.tile % a.tiles_per_batch) * kRowsP;
-      tma_store_3d(&map_out, ybuf, tbox, r0, b);
-    }
+    if (lane == 0) mbar_arrive(wempty + slot);  // stage consumed: producer may refill
 
     if (box == cur.nbox - 1) {
       float hs[kN / 2];
@@ -826,16 +834,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         __stcg(reinterpret_cast<float4*>(dst + 4), make_float4(hs[4], hs[5], hs[6], hs[7]));
       }
       if (cur.seg != n_seg - 1) {
-        __threadfence();
+        // bar.warp.sync orders every lane's carry store before lane 0's gpu-scope
+        // release (cumulative); the reader pairs it with ld.acquire + bar.warp.sync
         __syncwarp();
         if (lane == 0) st_release(a.flags + cur.tile, static_cast<unsigned>(cur.seg + 1));
       }
     }
-    __syncwarp();
-    produce(slot);
   }
-  if (lane == 0) bulk_wait_all();
-  __syncwarp();
 }
 
 // (b, N, L) -> (b, L, N) for B and C, so a timestep's 16 state coefficients are one
@@ -843,7 +848,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 __global__ void __launch_bounds__(256) transpose_bc_kernel(const float* __restrict__ B,
                                                            const float* __restrict__ C,
                                                            float* __restrict__ Bt,
-                                                           float* __restrict__ Ct, int L) {
+                                                           float* __restrict__ Ct, int L,
+                                                           int row_stride) {
   __shared__ float tile[kN][33];
   const float* src = blockIdx.z ? C : B;
   float* dst = blockIdx.z ? Ct : Bt;
@@ -857,7 +863,7 @@ __global__ void __launch_bounds__(256) transpose_bc_kernel(const float* __restri
   for (int e = threadIdx.x; e < 32 * kN; e += 256) {
     const int tt = e / kN, s = e % kN;
     const int t = t0 + tt;
-    if (t < L) dst[(size_t(b) * L + t) * kN + s] = tile[s][tt];
+    if (t < L) dst[(size_t(b) * L + t) * row_stride + s] = tile[s][tt];
   }
 }
 
@@ -926,71 +932,69 @@ int grow(cl_ctx* ctx, T** ptr, size_t* have, size_t need, const char* what) {
   return CL_OK;
 }
 
-// ---- kernel geometry table (tuning knob: CL_SCAN_CFG=<index>) ----
+// ---- kernel table (CL_SCAN_CFG=<index> selects a row, for experiments) ----
+enum ScanKind { kWarpSpecPair = 0, kRowSeq = 1 };
 struct ScanCfg {
-  int box, warps, stages, emu, pair;
+  int kind, box, warps, stages;
 };
 constexpr ScanCfg kCfgs[] = {
-    {32, 4, 3, 0, 0},  {32, 4, 3, 1, 0},  {32, 4, 3, 2, 0},  {16, 8, 3, 0, 0},  {16, 8, 3, 1, 0},
-    {16, 8, 3, 2, 0},  {16, 6, 4, 0, 0},  {16, 6, 4, 1, 0},  {16, 8, 3, 3, 0},  {16, 12, 2, 1, 0},
-    {8, 16, 3, 1, 0},  {16, 12, 2, 0, 0}, {8, 16, 3, 0, 0},  {8, 16, 3, 2, 0},  {8, 12, 4, 1, 0},
-    // lane-pair kernels (16-row tiles)
-    {32, 6, 3, 0, 1},  {32, 6, 3, 1, 1},  {16, 12, 3, 0, 1}, {16, 12, 3, 1, 1}, {16, 8, 4, 0, 1},
-    {16, 14, 2, 0, 1}, {32, 8, 2, 0, 1},  {16, 14, 2, 1, 1}, {16, 14, 2, 16, 1}, {16, 14, 2, 17, 1},
-    {16, 12, 3, 16, 1}, {16, 7, 3, 0, 0},  {16, 7, 3, 16, 0}, {32, 4, 3, 16, 0},
+    {kWarpSpecPair, 16, 14, 2},  // default: 14 consumer + 2 producer warps per SM
+    {kRowSeq, 32, 4, 3},         // 32-row tiles, self-fed TMA rings
+    {kRowSeq, 16, 8, 3},
+    {kRowSeq, 16, 7, 3},
 };
-constexpr int kDefaultCfg = 20;
+constexpr int kDefaultCfg = 0;
+constexpr int kProducers = 2;
 
-template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int EMU>
-cudaError_t launch_rowseq(const CUtensorMap& mu, const CUtensorMap& mdt, const CUtensorMap& mz,
-                          const CUtensorMap& mout, const CUtensorMap& mB, const CUtensorMap& mC,
-                          const TmaArgs& t, int num_sms, cudaStream_t s) {
-  auto kern = rowseq_tma_kernel<BOX, WARPS, STAGES, SP, HZ, EMU>;
+template <typename K>
+cudaError_t set_smem(K kern, size_t smem) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(smem));
+}
+
+int grid_for(int n_tiles, int warps, int num_sms) {
+  const int max_useful = (n_tiles + warps - 1) / warps;
+  return max_useful < num_sms ? (max_useful < 1 ? 1 : max_useful) : num_sms;
+}
+
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ>
+cudaError_t launch_ws(const CUtensorMap (&m)[6], const TmaArgs& t, int num_sms, cudaStream_t s) {
+  auto kern = rowpair_ws_kernel<BOX, WARPS, STAGES, SP, HZ, kProducers>;
+  const size_t smem = size_t(WARPS) * STAGES * GeoP<BOX>::kStageBytes + 1024 +
+                      size_t(WARPS) * STAGES * (16 + 8);
+  cudaError_t e = set_smem(kern, smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid_for(t.n_tiles, WARPS, num_sms), (WARPS + kProducers) * 32, smem, s>>>(
+      m[0], m[1], m[2], m[4], t);
+  return cudaGetLastError();
+}
+
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ>
+cudaError_t launch_rowseq(const CUtensorMap (&m)[6], const TmaArgs& t, int num_sms,
+                          cudaStream_t s) {
+  auto kern = rowseq_tma_kernel<BOX, WARPS, STAGES, SP, HZ>;
   const size_t smem = size_t(WARPS) * warp_bytes<BOX, STAGES>() + 1024 + 256;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = set_smem(kern, smem);
   if (e != cudaSuccess) return e;
-  int grid = num_sms;
-  const int max_useful = (t.n_tiles + WARPS - 1) / WARPS;
-  if (max_useful < grid) grid = max_useful < 1 ? 1 : max_useful;
-  kern<<<grid, WARPS * 32, smem, s>>>(mu, mdt, mz, mout, mB, mC, t);
+  kern<<<grid_for(t.n_tiles, WARPS, num_sms), WARPS * 32, smem, s>>>(m[0], m[1], m[2], m[3],
+                                                                      m[4], m[5], t);
   return cudaGetLastError();
 }
 
-template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int EMU>
-cudaError_t launch_rowpair(const CUtensorMap& mu, const CUtensorMap& mdt, const CUtensorMap& mz,
-                           const CUtensorMap& mout, const CUtensorMap& mB, const CUtensorMap& mC,
-                           const TmaArgs& t, int num_sms, cudaStream_t s) {
-  auto kern = rowpair_tma_kernel<BOX, WARPS, STAGES, SP, HZ, EMU>;
-  const size_t smem = size_t(WARPS) * warp_bytes_p<BOX, STAGES>() + 1024 + 256;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  int grid = num_sms;
-  const int max_useful = (t.n_tiles + WARPS - 1) / WARPS;
-  if (max_useful < grid) grid = max_useful < 1 ? 1 : max_useful;
-  kern<<<grid, WARPS * 32, smem, s>>>(mu, mdt, mz, mout, mB, mC, t);
-  return cudaGetLastError();
-}
-
-template <int BOX, int WARPS, int STAGES, int EMU>
-cudaError_t dispatch_pair(bool sp, bool hz, const CUtensorMap& mu, const CUtensorMap& mdt,
-                          const CUtensorMap& mz, const CUtensorMap& mout, const CUtensorMap& mB,
-                          const CUtensorMap& mC, const TmaArgs& t, int num_sms, cudaStream_t s) {
-  if (sp && hz) return launch_rowpair<BOX, WARPS, STAGES, true, true, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
-  if (sp) return launch_rowpair<BOX, WARPS, STAGES, true, false, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
-  if (hz) return launch_rowpair<BOX, WARPS, STAGES, false, true, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
-  return launch_rowpair<BOX, WARPS, STAGES, false, false, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
-}
-
-template <int BOX, int WARPS, int STAGES, int EMU>
-cudaError_t dispatch_flags(bool sp, bool hz, const CUtensorMap& mu, const CUtensorMap& mdt,
-                           const CUtensorMap& mz, const CUtensorMap& mout, const CUtensorMap& mB,
-                           const CUtensorMap& mC, const TmaArgs& t, int num_sms, cudaStream_t s) {
-  if (sp && hz) return launch_rowseq<BOX, WARPS, STAGES, true, true, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
-  if (sp) return launch_rowseq<BOX, WARPS, STAGES, true, false, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
-  if (hz) return launch_rowseq<BOX, WARPS, STAGES, false, true, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
-  return launch_rowseq<BOX, WARPS, STAGES, false, false, EMU>(mu, mdt, mz, mout, mB, mC, t, num_sms, s);
+// softplus / z-gate are compile-time switches: four instantiations per geometry
+template <bool WS, int BOX, int WARPS, int STAGES>
+cudaError_t dispatch(bool sp, bool hz, const CUtensorMap (&m)[6], const TmaArgs& t, int n,
+                     cudaStream_t s) {
+  if (WS) {
+    if (sp && hz) return launch_ws<BOX, WARPS, STAGES, true, true>(m, t, n, s);
+    if (sp) return launch_ws<BOX, WARPS, STAGES, true, false>(m, t, n, s);
+    if (hz) return launch_ws<BOX, WARPS, STAGES, false, true>(m, t, n, s);
+    return launch_ws<BOX, WARPS, STAGES, false, false>(m, t, n, s);
+  }
+  if (sp && hz) return launch_rowseq<BOX, WARPS, STAGES, true, true>(m, t, n, s);
+  if (sp) return launch_rowseq<BOX, WARPS, STAGES, true, false>(m, t, n, s);
+  if (hz) return launch_rowseq<BOX, WARPS, STAGES, false, true>(m, t, n, s);
+  return launch_rowseq<BOX, WARPS, STAGES, false, false>(m, t, n, s);
 }
 
 int scan_cfg_index() {
@@ -1012,9 +1016,11 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     return fail(ctx, CL_E_INVALID, "scan variant rowseq_tma needs d_state 16, L % 4 == 0 and 16-byte aligned buffers");
   const bool use_tma = variant == CL_SCAN_ROWSEQ_TMA || (variant == CL_SCAN_AUTO && tma_ok);
   if (use_tma) {
-    const ScanCfg cfg = kCfgs[scan_cfg_index()];
+    const int cfg_idx = scan_cfg_index();
+    const ScanCfg cfg = kCfgs[cfg_idx];
+    const bool ws = cfg.kind == kWarpSpecPair;
     const uint64_t L = a.seq_len, D = a.dim, Bt = a.batch;
-    const int rows_per_tile = cfg.pair ? kRowsP : kRows;
+    const int rows_per_tile = ws ? kRowsP : kRows;
     const int tiles_per_batch = static_cast<int>((D + rows_per_tile - 1) / rows_per_tile);
     const int n_tiles = tiles_per_batch * static_cast<int>(Bt);
     const size_t work_bytes = (size_t(n_tiles) + 32) * sizeof(unsigned int);
@@ -1024,26 +1030,33 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     if (!rc) rc = grow(ctx, &ctx->d_carry, &ctx->carry_bytes, carry_bytes, "cudaMalloc(carry)");
     if (!rc) rc = grow(ctx, &ctx->d_bct, &ctx->bct_bytes, bc_bytes, "cudaMalloc(B/C transpose)");
     if (rc) return rc;
+    // B^T / C^T: interleaved per timestep ([B | C], 128 B rows, one TMA box) for the
+    // warp-specialised kernel, two separate (b, L, 16) arrays for the row kernel
     float* d_Bt = ctx->d_bct;
-    float* d_Ct = ctx->d_bct + size_t(Bt) * L * kN;
+    float* d_Ct = ws ? ctx->d_bct + kN : ctx->d_bct + size_t(Bt) * L * kN;
     const int box = cfg.box;
     const int sw = box == 32 ? 128 : (box == 16 ? 64 : 32);
-    CUtensorMap mu, mdt, mz, mout, mB, mC;
-    bool ok = make_map(&mu, a.u, L, D, Bt, box, rows_per_tile, sw) &&
-              make_map(&mdt, a.delta, L, D, Bt, box, rows_per_tile, sw) &&
-              make_map(&mout, a.out, L, D, Bt, box, rows_per_tile, sw) &&
-              make_map(&mB, d_Bt, kN, L, Bt, kN, box, 0) &&
-              make_map(&mC, d_Ct, kN, L, Bt, kN, box, 0);
-    if (ok) ok = make_map(&mz, a.z ? a.z : a.u, L, D, Bt, box, rows_per_tile, sw);
+    CUtensorMap m[6];  // u, delta, z, out, B^T (or [B|C]), C^T
+    std::memset(m, 0, sizeof(m));
+    bool ok = make_map(&m[0], a.u, L, D, Bt, box, rows_per_tile, sw) &&
+              make_map(&m[1], a.delta, L, D, Bt, box, rows_per_tile, sw) &&
+              make_map(&m[2], a.z ? a.z : a.u, L, D, Bt, box, rows_per_tile, sw) &&
+              make_map(&m[3], a.out, L, D, Bt, box, rows_per_tile, sw);
+    if (ok && ws) ok = make_map(&m[4], d_Bt, 2 * kN, L, Bt, 2 * kN, box, 0);
+    if (ok && !ws)
+      ok = make_map(&m[4], d_Bt, kN, L, Bt, kN, box, 0) &&
+           make_map(&m[5], d_Ct, kN, L, Bt, kN, box, 0);
     if (!ok) return fail(ctx, CL_E_CUDA, "cuTensorMapEncodeTiled failed");
     cudaError_t e = cudaMemsetAsync(ctx->d_work, 0, work_bytes, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(scan work)");
     const dim3 tgrid(static_cast<unsigned>((L + 31) / 32), static_cast<unsigned>(Bt), 2);
-    transpose_bc_kernel<<<tgrid, 256, 0, s>>>(a.B, a.C, d_Bt, d_Ct, static_cast<int>(L));
+    transpose_bc_kernel<<<tgrid, 256, 0, s>>>(a.B, a.C, d_Bt, d_Ct, static_cast<int>(L),
+                                              ws ? 2 * kN : kN);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "transpose_bc_kernel launch");
     ++ctx->launches;
     TmaArgs t{};
+    t.out = a.out;
     t.A = a.A;
     t.D = a.D;
     t.bias = a.delta_bias;
@@ -1061,39 +1074,13 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     t.fixed_chunk = fixed_chunk;
     const bool sp = a.delta_softplus != 0, hz = a.z != nullptr;
     const int n = ctx->num_sms;
-    switch (scan_cfg_index()) {
-      case 0: e = dispatch_flags<32, 4, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 1: e = dispatch_flags<32, 4, 3, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 2: e = dispatch_flags<32, 4, 3, 2>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 3: e = dispatch_flags<16, 8, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 4: e = dispatch_flags<16, 8, 3, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 5: e = dispatch_flags<16, 8, 3, 2>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 6: e = dispatch_flags<16, 6, 4, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 7: e = dispatch_flags<16, 6, 4, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 8: e = dispatch_flags<16, 8, 3, 3>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 9: e = dispatch_flags<16, 12, 2, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 10: e = dispatch_flags<8, 16, 3, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 11: e = dispatch_flags<16, 12, 2, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 12: e = dispatch_flags<8, 16, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 13: e = dispatch_flags<8, 16, 3, 2>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 14: e = dispatch_flags<8, 12, 4, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 15: e = dispatch_pair<32, 6, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 16: e = dispatch_pair<32, 6, 3, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 17: e = dispatch_pair<16, 12, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 18: e = dispatch_pair<16, 12, 3, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 19: e = dispatch_pair<16, 8, 4, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 20: e = dispatch_pair<16, 14, 2, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 21: e = dispatch_pair<32, 8, 2, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 22: e = dispatch_pair<16, 14, 2, 1>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 23: e = dispatch_pair<16, 14, 2, 16>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 24: e = dispatch_pair<16, 14, 2, 17>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 25: e = dispatch_pair<16, 12, 3, 16>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 26: e = dispatch_flags<16, 7, 3, 0>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 27: e = dispatch_flags<16, 7, 3, 16>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
-      case 28:
-      default: e = dispatch_flags<32, 4, 3, 16>(sp, hz, mu, mdt, mz, mout, mB, mC, t, n, s); break;
+    switch (cfg_idx) {
+      case 1: e = dispatch<false, 32, 4, 3>(sp, hz, m, t, n, s); break;
+      case 2: e = dispatch<false, 16, 8, 3>(sp, hz, m, t, n, s); break;
+      case 3: e = dispatch<false, 16, 7, 3>(sp, hz, m, t, n, s); break;
+      default: e = dispatch<true, 16, 14, 2>(sp, hz, m, t, n, s); break;
     }
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "rowseq_tma_kernel launch");
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     ++ctx->launches;
     return CL_OK;
   }

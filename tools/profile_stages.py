@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--variant", default="auto")
+    ap.add_argument("--median", action="store_true")
     ap.add_argument("--chunk", type=int, default=0, help="fixed chunk (0 = device rule)")
     ap.add_argument("--no-softplus", action="store_true")
     ap.add_argument("--no-z", action="store_true")
@@ -55,7 +56,12 @@ def main():
         torch.cuda.synchronize()
         for i, k in enumerate(times):
             times[k].append(ev[i].elapsed_time(ev[i + 1]))
-    print({k: [round(t, 4) for t in v] for k, v in times.items()})
+    if args.median:
+        import statistics
+        print(f"cfg={os.environ.get('CL_SCAN_CFG', 'default')} chunk={args.chunk} "
+              + " ".join(f"{k}={statistics.median(v[1:]):.4f}" for k, v in times.items()))
+    else:
+        print({k: [round(t, 4) for t in v] for k, v in times.items()})
     print("decision", pf.decision().decision)
 
 
