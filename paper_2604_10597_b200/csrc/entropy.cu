@@ -303,21 +303,23 @@ __global__ void range_init_kernel(double* range) {
 // ---------------------------------------------------------------------------
 // Stage 2: histogram, K <= 256.  Each lane owns private 16-bit counters laid out
 // [bin][lane] (16 KB per warp): increments need no atomics.  The per-lane
-// read-modify-write chain is broken into groups of four samples: the four
-// counters are loaded together, and the stores (in order) carry the in-group
-// duplicate count, so the last store to a bin holds the right total.  Input is
-// streamed through a 4-stage shared-memory ring filled by cp.async.bulk (TMA bulk
+// read-modify-write chain is broken into pairs (full chunks) or groups of four
+// samples: the counters are loaded together, and the stores (in order) carry the
+// in-group duplicate count, so the last store to a bin holds the right total.  Input
+// is streamed through a 3-stage shared-memory ring filled by cp.async.bulk (TMA bulk
 // copies) issued by a dedicated producer warp; consumers release slots through an
-// mbarrier.  Counters are flushed (per CTA, then one atomic per bin) before they
-// can overflow.
+// mbarrier.  10 consumer warps (160 KB of counters) is what fits beside the ring;
+// the kernel is latency-bound, 8 -> 10 warps measured -4%.  Fire-and-forget shared
+// atomics on a conflict-free packed layout measured +39% (ATOMS throughput).
+// Counters are flushed (per CTA, then one atomic per bin) before they can overflow.
 // ---------------------------------------------------------------------------
-constexpr int kHistWarps = 8;                        // consumer warps
+constexpr int kHistWarps = 10;                       // consumer warps (10 x 16 KB counters)
 constexpr int kHistThreads = (kHistWarps + 1) * 32;  // + producer warp
-constexpr int kStages = 4;
-constexpr int kChunkFloats = 4096;                   // 16 KB per stage
+constexpr int kStages = 3;
+constexpr int kChunkFloats = kHistWarps * 512;        // 16 samples per lane per stage
 constexpr int kChunkBytes = kChunkFloats * 4;
 constexpr int kLaneBins = 256;
-constexpr size_t kCounterBytes = size_t(kHistWarps) * kLaneBins * 32 * 2;  // 128 KB
+constexpr size_t kCounterBytes = size_t(kHistWarps) * kLaneBins * 32 * 2;  // 160 KB
 constexpr size_t kHistSmem = kCounterBytes + size_t(kStages) * kChunkBytes + kLaneBins * 4 +
                              2 * kStages * 8 + 64;
 constexpr int kFlushChunks = 4000;  // 16 samples/lane/chunk * 4000 < 65536
