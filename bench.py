@@ -3,6 +3,7 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config C3] [--scaling weak|strong] [--no-e2e] [--no-cpu]
+                    [--no-producer]
 
 One "step" = one layer's prefill over the configured workload (BASELINE.json
 configs[2], "C3": B=8, L=8192, d_inner=4096, N=16 per rank): range_init ->
@@ -15,7 +16,8 @@ Prints ONE JSON line on rank 0 (contract in the task statement): value = whole-j
 tokens/s (a token = one (b, l) position through all d_inner channels),
 `roofline` for the dominant kernel (the scan), `cpu_baseline`, `e2e` (the same
 metric through the public API with pinned host buffers and H2D/D2H inside the
-timed region), `clocks`, `gpu_launches`.
+timed region), `clocks`, `gpu_launches`, and (N=1) `producer_fusion`: the conv1d+SiLU
+producer of u with the min/max pass fused into its epilogue vs run separately.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref: the
 reference headers compiled in place; else the oracle port) on the box's host
@@ -232,6 +234,8 @@ def main():
     ap.add_argument("--chunk-policy", default="rule", choices=["rule", "guarded", "static512"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-producer", action="store_true",
+                    help="skip the conv1d producer-fusion side measurement")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -383,6 +387,22 @@ def main():
         "gpu_launches": launches,
     }
     result["clocks"] = clocks.summary()
+    # SFU roofline of the scan: 18 MUFU per (b, d, l) -- 16 state
+    # exponentials, one ex2 in softplus, one in SiLU -- at 16 MUFU/clk/SM x SMs x the
+    # SM clock sampled during the timed region (the scan's binding pipe; HBM is not)
+    sm_mhz = result["clocks"].get("sm_mhz") or 1965.0
+    n_sms = torch.cuda.get_device_properties(device).multi_processor_count
+    mufu_per_launch = batch * dim * L * (N + 2)
+    sfu_peak = 16 * n_sms * sm_mhz * 1e6 / 1e12
+    sfu_ach = mufu_per_launch / (scan_ms / 1e3) / 1e12
+    result["roofline"]["sfu"] = {"achieved": sfu_ach, "peak": sfu_peak, "unit": "TMUFU/s",
+                                 "frac": sfu_ach / sfu_peak,
+                                 "mufu_per_launch": mufu_per_launch,
+                                 "peak_basis": f"16/clk/SM x {n_sms} SMs x {sm_mhz:.0f} MHz"}
+
+    # ---- producer fusion (conv1d + SiLU with the min/max epilogue), side measurement
+    if not args.no_producer and world == 1:
+        result["producer_fusion"] = producer_fusion_measure(torch, device, x, pf)
 
     # ---- e2e through the public API with host buffers (pinned), H2D/D2H timed
     if not args.no_e2e:
@@ -414,6 +434,49 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def producer_fusion_measure(torch, device, x, pf, reps=20):
+    """the conv1d(+SiLU) producer of u with the stage-1 min/max in its
+    epilogue, vs the same conv followed by the separate min/max pass (device time)."""
+    from paper_2604_10597_b200.mamba1 import causal_conv1d_fn
+    batch, dim, L = x["u"].shape
+    g = torch.Generator(device=device)
+    g.manual_seed(7)
+    xin = torch.randn(batch, dim, L, generator=g, device=device, dtype=torch.float32)
+    w = torch.randn(dim, 4, generator=g, device=device, dtype=torch.float32).mul_(0.5)
+    b = torch.randn(dim, generator=g, device=device, dtype=torch.float32).mul_(0.1)
+    u = torch.empty_like(xin)
+    uf = u.reshape(-1)
+
+    def fused():
+        pf.stage_conv(xin, w, b, "silu", out=u)
+
+    def unfused():
+        causal_conv1d_fn(xin, w, b, "silu", out=u)
+        pf.stage_minmax(uf)
+
+    def conv_only():
+        causal_conv1d_fn(xin, w, b, "silu", out=u)
+
+    res = {}
+    for name, fn in (("fused_ms", fused), ("unfused_ms", unfused), ("conv_only_ms", conv_only)):
+        fn()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(reps)]
+        for a, e in evs:
+            a.record()
+            fn()
+            e.record()
+        torch.cuda.synchronize()
+        res[name] = statistics.median(a.elapsed_time(e) for a, e in evs)
+    fused_bytes = 2 * xin.numel() * 4  # read x, write u
+    res["saved_ms"] = res["unfused_ms"] - res["fused_ms"]
+    res["fused_gbs"] = fused_bytes / (res["fused_ms"] / 1e3) / 1e9
+    res["workload"] = f"conv width 4 + SiLU over ({batch}, {dim}, {L}) fp32, stride 1"
+    del xin, u
+    return res
 
 
 def e2e_measure(torch, dist, world, device, x, pf, L, global_batch, steps):

@@ -140,6 +140,19 @@ int cl_minmax_f32(cl_ctx* ctx, const float* d_values, uint64_t n, uint64_t globa
 int cl_minmax_f64(cl_ctx* ctx, const double* d_values, uint64_t n, uint64_t global_offset,
                   uint64_t stride, double* d_range, void* stream);
 
+/* Producer fusion (no reference counterpart -- the paper's u comes
+ * out of mamba_ssm's causal_conv1d_fn):
+ *   u[b,d,t] = act(bias[d] + sum_{k<width} weight[d,k] * x[b,d,t-width+1+k])
+ * with x zero before t = 0, act = SiLU (silu != 0) or identity; x, u (batch, dim,
+ * seq_len) fp32, weight (dim, width), bias (dim) or NULL, width in [1, 4].  When
+ * d_range is not NULL the kernel also performs cl_minmax_f32 over the u it writes
+ * (same global_offset / stride semantics, same d_range protocol), so the separate
+ * min/max pass -- one full read of u -- disappears from the prefill. */
+int cl_conv1d_f32(cl_ctx* ctx, const float* d_x, const float* d_weight, const float* d_bias,
+                  float* d_u, uint64_t batch, uint64_t dim, uint64_t seq_len, int width,
+                  int silu, uint64_t global_offset, uint64_t stride, double* d_range,
+                  void* stream);
+
 /* Stage 2 (entropy.hpp:116-126): accumulate K uint64 counts of the strided
  * samples, binned exactly as detail::bin_index (entropy.hpp:87-94) over the
  * (global) range in d_range, or the spec's fixed range.  d_counts must be

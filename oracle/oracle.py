@@ -299,5 +299,24 @@ class Reference(_Lib):
         return y.reshape(r1 - r0, L), h.reshape(r1 - r0, N)
 
 
+def causal_conv1d_f64(x, weight, bias=None, silu=True):
+    """fp64 restatement of causal_conv1d_fn(x, weight, bias, activation) -- the producer
+    of u in the paper's MambaMixer.  PARITY UNPINNED: the reference has
+    no convolution; this restates the package's published formula
+        u[b,d,t] = act(bias[d] + sum_k weight[d,k] * x[b,d,t-W+1+k]),  x[<0] = 0.
+    x (batch, dim, L), weight (dim, W), bias (dim,)."""
+    x = np.asarray(x, dtype=np.float64)
+    w = np.asarray(weight, dtype=np.float64)
+    W = w.shape[1]
+    L = x.shape[-1]
+    xp = np.concatenate([np.zeros(x.shape[:-1] + (W - 1,)), x], axis=-1)
+    out = np.zeros_like(x) + (0.0 if bias is None else np.asarray(bias, np.float64)[:, None])
+    for k in range(W):
+        out = out + w[None, :, k:k + 1] * xp[..., k:k + L]
+    if silu:
+        out = out / (1.0 + np.exp(-out))
+    return out
+
+
 def reference_available():
     return os.path.exists(REF_SO)

@@ -246,6 +246,22 @@ int cl_minmax_f64(cl_ctx* ctx, const double* d_values, uint64_t n, uint64_t glob
   return check_launch(ctx, e, "minmax_f64");
 }
 
+int cl_conv1d_f32(cl_ctx* ctx, const float* d_x, const float* d_weight, const float* d_bias,
+                  float* d_u, uint64_t batch, uint64_t dim, uint64_t seq_len, int width,
+                  int silu, uint64_t global_offset, uint64_t stride, double* d_range,
+                  void* stream) {
+  const uint64_t n = batch * dim * seq_len;
+  if (!ctx || (n && (!d_x || !d_weight || !d_u))) return fail(ctx, CL_E_INVALID, "null argument");
+  if (width < 1 || width > 4) return fail(ctx, CL_E_INVALID, "conv width must lie in [1, 4]");
+  if (stride < 1) return fail(ctx, CL_E_INVALID, "stride must be >= 1");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_conv1d_f32(d_x, d_weight, d_bias, d_u, batch, dim, seq_len, width,
+                                    silu, global_offset, stride, d_range, ctx->num_sms,
+                                    static_cast<cudaStream_t>(stream));
+  if (n) ++ctx->launches;
+  return check_launch(ctx, e, "conv1d_f32");
+}
+
 int cl_counts_zero(cl_ctx* ctx, uint64_t* d_counts, int bin_count, void* stream) {
   if (!ctx || !d_counts || bin_count < 1) return fail(ctx, CL_E_INVALID, "null argument");
   DeviceGuard g(ctx->device);

@@ -55,6 +55,11 @@ cudaError_t launch_decide(const uint64_t* d_counts, const double* d_range,
                           cl_decision* d_out, cudaStream_t s);
 cudaError_t launch_entropy_from_masses(const double* d_masses, int k, double eps, double* d_out,
                                        cudaStream_t s);
+// conv1d.cu
+cudaError_t launch_conv1d_f32(const float* x, const float* w, const float* bias, float* u,
+                              uint64_t batch, uint64_t dim, uint64_t L, int width, int silu,
+                              uint64_t g0, uint64_t stride, double* d_range, int num_sms,
+                              cudaStream_t s);
 // scan_f64.cu
 cudaError_t launch_scan_f64(const cl_scan_params_f64& p, const double* d_h0, uint64_t chunk,
                             double* d_y, double* d_h, cudaStream_t s);

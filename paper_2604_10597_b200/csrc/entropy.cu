@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "cl_internal.h"
+#include "range.cuh"
 
 namespace cl {
 namespace {
@@ -28,22 +29,9 @@ constexpr int kThreads = 256;
 
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
-__device__ __forceinline__ bool finite_f32(float x) {
-  return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u;
-}
-__device__ __forceinline__ bool finite_f64(double x) {
-  return (__double_as_longlong(x) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;
-}
-
-__device__ __forceinline__ void atomic_max_f64(double* addr, double v) {
-  unsigned long long* a = reinterpret_cast<unsigned long long*>(addr);
-  unsigned long long old = *a;
-  while (__longlong_as_double(static_cast<long long>(old)) < v) {
-    const unsigned long long assumed = old;
-    old = atomicCAS(a, assumed, static_cast<unsigned long long>(__double_as_longlong(v)));
-    if (old == assumed) break;
-  }
-}
+using range::atomic_max_f64;
+using range::finite_f32;
+using range::finite_f64;
 
 // detail::bin_index (entropy.hpp:87-94), operation-for-operation in fp64.  The
 // int conversion reproduces x86-64 cvttsd2si (out-of-range -> INT_MIN), which is
@@ -168,20 +156,11 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads) minmax_f32_kernel(const float* __restrict__ v,
                                                               uint64_t n, uint64_t g0,
                                                               uint64_t stride, double* range) {
-  float lo = FLT_MAX, hi = -FLT_MAX;
-  bool any = false;
-  bool bad = false;
+  range::Acc acc;
   const uint64_t head = umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
   const uint64_t n4 = (n - head) / 4;
   const uint64_t tail0 = head + n4 * 4;
-  auto visit = [&](float x, uint64_t i) {
-    bad |= !finite_f32(x);
-    if (sampled<MODE>(g0 + i, stride)) {
-      lo = fminf(lo, x);
-      hi = fmaxf(hi, x);
-      any = true;
-    }
-  };
+  auto visit = [&](float x, uint64_t i) { acc.visit(x, sampled<MODE>(g0 + i, stride)); };
   if (blockIdx.x == 0) {
     for (uint64_t i = threadIdx.x; i < head; i += blockDim.x) visit(v[i], i);
     for (uint64_t i = tail0 + threadIdx.x; i < n; i += blockDim.x) visit(v[i], i);
@@ -210,36 +189,7 @@ __global__ void __launch_bounds__(kThreads) minmax_f32_kernel(const float* __res
     visit(q.z, i + 2);
     visit(q.w, i + 3);
   }
-  // block reduce
-  for (int o = 16; o; o >>= 1) {
-    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  any = __any_sync(0xffffffffu, any);
-  bad = __any_sync(0xffffffffu, bad);
-  __shared__ float s_lo[kThreads / 32], s_hi[kThreads / 32];
-  __shared__ int s_any[kThreads / 32], s_bad[kThreads / 32];
-  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
-  if (l == 0) {
-    s_lo[w] = lo;
-    s_hi[w] = hi;
-    s_any[w] = any;
-    s_bad[w] = bad;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 1; k < kThreads / 32; ++k) {
-      lo = fminf(lo, s_lo[k]);
-      hi = fmaxf(hi, s_hi[k]);
-      any |= s_any[k] != 0;
-      bad |= s_bad[k] != 0;
-    }
-    if (any) {
-      atomic_max_f64(range + 0, -static_cast<double>(lo));
-      atomic_max_f64(range + 1, static_cast<double>(hi));
-    }
-    if (bad) atomic_max_f64(range + 2, 1.0);
-  }
+  range::commit<kThreads>(acc, range);
 }
 
 template <int MODE>

@@ -96,6 +96,32 @@ def selective_scan_fn(u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_
     return (out, h_last) if return_last_state else out
 
 
+def causal_conv1d_fn(x, weight, bias=None, activation: Optional[str] = "silu",
+                     out: Optional[torch.Tensor] = None, range_buf: Optional[torch.Tensor] = None,
+                     global_offset: int = 0, stride: int = 1):
+    """causal_conv1d_fn(x, weight, bias, activation) semantics (fp32) on the sm_100a kernel.
+
+    x (batch, dim, L), weight (dim, width <= 4), bias (dim,).  With range_buf (4 fp64,
+    initialised by cl_range_init) the kernel also runs the entropy stage-1 min/max over
+    the u it produces (producer fusion, SURVEY.md 8(f) #1)."""
+    dev = x.device
+    _check_f32("x", x, dev)
+    _check_f32("weight", weight, dev)
+    _check_f32("bias", bias, dev)
+    if activation not in (None, "silu", "swish"):
+        raise InvalidInput("activation must be None, 'silu' or 'swish'")
+    batch, dim, L = x.shape
+    if weight.dim() != 2 or weight.shape[0] != dim or (bias is not None and bias.numel() != dim):
+        raise InvalidInput("shape mismatch")
+    out = torch.empty_like(x) if out is None else out
+    _check_f32("out", out, dev)
+    ctx = Context.get(dev.index)
+    ctx.call("cl_conv1d_f32", x.data_ptr(), weight.data_ptr(), _ptr(bias), out.data_ptr(),
+             batch, dim, L, int(weight.shape[1]), int(activation is not None), int(global_offset),
+             int(stride), _ptr(range_buf), _stream_ptr(dev))
+    return out
+
+
 def C_byref(x):
     return C.byref(x)
 
@@ -165,6 +191,14 @@ class Prefill:
         self.ctx.call("cl_minmax_f32", u_flat.data_ptr(), u_flat.numel(), int(global_offset),
                       int(self.spec.sample_stride), self.range.data_ptr(), s)
 
+    def stage_conv(self, x, weight, bias=None, activation="silu", out=None,
+                   global_offset: int = 0, init: bool = True):
+        """Producer fusion: u = causal_conv1d(x) (+ SiLU) with stage 1 in its epilogue."""
+        if init:
+            self.ctx.call("cl_range_init", self.range.data_ptr(), _stream_ptr(self.device))
+        return causal_conv1d_fn(x, weight, bias, activation, out, self.range, global_offset,
+                                int(self.spec.sample_stride))
+
     def stage_histogram(self, u_flat: torch.Tensor, global_offset: int = 0, zero: bool = True):
         s = _stream_ptr(self.device)
         if zero:
@@ -202,6 +236,22 @@ class Prefill:
         else:
             o, h = res, None
         return PrefillResult(o, h, self.decision_buf)
+
+    def from_conv(self, x, conv_weight, conv_bias, delta, A, B, C, D=None, z=None,
+                  delta_bias=None, delta_softplus=True, out=None, return_last_state=False,
+                  h0=None, activation="silu"):
+        """The prefill with its producer fused: conv1d(+SiLU) -> u with the min/max
+        epilogue, then histogram -> decide -> scan.  Returns (PrefillResult, u)."""
+        if x.numel() == 0:
+            raise InvalidInput("no samples")
+        u = self.stage_conv(x, conv_weight, conv_bias, activation)
+        uf = u.reshape(-1)
+        self.stage_histogram(uf)
+        self.stage_decide(self.n_samples(uf.numel()), u.shape[-1])
+        res = self.stage_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, out,
+                              return_last_state, h0)
+        o, h = res if return_last_state else (res, None)
+        return PrefillResult(o, h, self.decision_buf), u
 
     def decision(self) -> DecisionRecord:
         return read_decision(self.decision_buf)
