@@ -235,7 +235,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-producer", action="store_true",
-                    help="skip the conv1d producer-fusion side measurement")
+                    help="skip the side measurements (conv1d producer fusion, token entropy)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -403,6 +403,7 @@ def main():
     # ---- producer fusion (conv1d + SiLU with the min/max epilogue), side measurement
     if not args.no_producer and world == 1:
         result["producer_fusion"] = producer_fusion_measure(torch, device, x, pf)
+        result["token_entropy"] = token_entropy_measure(torch, device, x)
 
     # ---- e2e through the public API with host buffers (pinned), H2D/D2H timed
     if not args.no_e2e:
@@ -477,6 +478,32 @@ def producer_fusion_measure(torch, device, x, pf, reps=20):
     res["workload"] = f"conv width 4 + SiLU over ({batch}, {dim}, {L}) fp32, stride 1"
     del xin, u
     return res
+
+
+def token_entropy_measure(torch, device, x, reps=10):
+    """token_entropy (per-position histograms over channels) of u on the
+    device, as the TokenHistogram policy's prefill stage (both passes + per-position
+    entropies + the ordered mean)."""
+    from paper_2604_10597_b200.mamba1 import Prefill
+    import paper_2604_10597_b200 as cl
+    pf = Prefill(cl.HistogramSpec(), cl.SchedulerPolicy(cl.TokenHistogramPolicy(),
+                                                        [128, 256, 512, 1024, 2048]),
+                 cl.ChunkBounds(128, 2048), device=device)
+    u = x["u"]
+    pf.stage_token(u)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(reps)]
+    for a, e in evs:
+        a.record()
+        pf.stage_token(u)
+        e.record()
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(e) for a, e in evs)
+    raw = float(pf.token_buf[0].item())
+    return {"ms": ms, "gbs": 2 * u.numel() * 4 / (ms / 1e3) / 1e9, "raw_nats": raw,
+            "workload": f"u {tuple(u.shape)} as (channels={u.numel() // u.shape[-1]}, "
+                        f"length={u.shape[-1]}), K=256, two passes over u"}
 
 
 def e2e_measure(torch, dist, world, device, x, pf, L, global_batch, steps):

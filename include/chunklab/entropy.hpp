@@ -93,9 +93,20 @@ inline Histogram compute_histogram(std::span<const double> values, const Histogr
   return h;
 }
 
+namespace detail {
+// validate_tensor's value check (entropy.hpp:42) over every value, on the device
+inline void require_all_finite(const ActivationTensor& t) {
+  int ok = 1;
+  b200::check(cl_all_finite_host(b200::Runtime::get().ctx(), t.values.data(), t.values.size(),
+                                 &ok));
+  if (!ok) throw invalid_input("non-finite input");
+}
+}  // namespace detail
+
 inline Histogram compute_histogram(const ActivationTensor& tensor, const HistogramSpec& spec) {
   if (tensor.values.empty()) throw invalid_input("no samples");
   validate_tensor_shape(tensor);
+  detail::require_all_finite(tensor);
   return compute_histogram(std::span<const double>(tensor.values), spec);
 }
 
@@ -116,26 +127,21 @@ inline EntropyEstimate estimate_tensor_entropy(const ActivationTensor& tensor,
   return e;
 }
 
-// entropy.hpp:180-210: mean over positions of the per-position histogram entropy.
+// entropy.hpp:180-210: mean over positions of the per-position histogram entropy, one
+// device call (cl_token_entropy_host: a block per 8 positions, both passes on the GPU).
 inline EntropyEstimate token_entropy(const ActivationTensor& tensor, const HistogramSpec& spec) {
   validate_tensor_shape(tensor);
+  detail::require_all_finite(tensor);
   validate_spec(spec);
   if (tensor.shape.size() < 2)
     throw invalid_input("token entropy needs a (channels, length) tensor");
   const std::size_t length = tensor.shape.back();
   const std::size_t channels = tensor.values.size() / length;
-  std::vector<double> slice(channels);
-  double raw_sum = 0.0;
-  std::size_t samples = 0;
-  for (std::size_t t = 0; t < length; ++t) {
-    for (std::size_t c = 0; c < channels; ++c) slice[c] = tensor.values[c * length + t];
-    const Histogram h = compute_histogram(std::span<const double>(slice), spec);
-    raw_sum += estimate_entropy(h, spec.epsilon).raw_nats;
-    samples += h.sample_count;
-  }
+  const cl_hist_spec cs = detail::to_c(spec);
   EntropyEstimate e;
-  e.raw_nats = raw_sum / static_cast<double>(length);
-  e.normalized = e.raw_nats / std::log(static_cast<double>(spec.bin_count));
+  std::uint64_t samples = 0;
+  b200::check(cl_token_entropy_host(b200::Runtime::get().ctx(), tensor.values.data(), channels,
+                                    length, &cs, &e.raw_nats, &e.normalized, &samples));
   e.bin_count = spec.bin_count;
   e.epsilon = spec.epsilon;
   e.sample_stride = spec.sample_stride;

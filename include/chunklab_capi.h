@@ -88,7 +88,8 @@ enum {
   CL_POL_SAMPLED_HIST = 3,
   CL_POL_LEARNED_TABLE = 4,
   CL_POL_GUARDED = 5,
-  CL_POL_RULE = 6 /* bare select_chunk (chunk.hpp:68-89), no bucket snap */
+  CL_POL_RULE = 6, /* bare select_chunk (chunk.hpp:68-89), no bucket snap */
+  CL_POL_TOKEN_HIST = 7 /* TokenHistogramPolicy (chunk.hpp:311-315): rule on token_entropy */
 };
 
 /* Source tags (ChunkDecision::source_policy, chunk.hpp:265-368):
@@ -224,6 +225,38 @@ typedef struct {
 int cl_scan_f64(cl_ctx* ctx, const cl_scan_params_f64* d_params, const double* d_h0,
                 uint64_t chunk, double* d_y, double* d_h, void* stream);
 
+/* token_entropy (entropy.hpp:180-210) of a (channels, length) tensor, length contiguous
+ * (Mamba u (B, D, L) is channels = B*D): one histogram per position t over its channel
+ * slice (slice index c sampled iff c % stride == 0; the slice's Dynamic range or the
+ * Fixed range), raw entropies averaged over positions in order.  bin_count <= 4096.
+ *
+ * One call: d_out (4 doubles) = {raw_nats, normalized, sample_count, nonfinite (0/1,
+ * any element)}; scratch belongs to the context. */
+int cl_token_entropy_f32(cl_ctx* ctx, const float* d_values, uint64_t channels, uint64_t length,
+                         const cl_hist_spec* spec, double* d_out, void* stream);
+/* The same as stages, for row-sharded tensors (channel_offset = global index of this
+ * rank's first channel; every rank holds all L positions):
+ *   cl_token_range_init(d_trange)         d_trange: 2*length + 1 doubles
+ *   cl_token_minmax_f32(...)              -> ncclAllReduce(d_trange, 2L+1, ncclDouble, MAX)
+ *   zero d_counts (length * bin_count u32)
+ *   cl_token_histogram_f32(...)           -> ncclAllReduce(d_counts, L*K, ncclUint32, SUM)
+ *   cl_token_entropy_counts(..., samples_per_position = ceil(total_channels / stride)) */
+int cl_token_range_init(cl_ctx* ctx, double* d_trange, uint64_t length, void* stream);
+int cl_token_minmax_f32(cl_ctx* ctx, const float* d_values, uint64_t channels, uint64_t length,
+                        uint64_t channel_offset, uint64_t stride, double* d_trange,
+                        void* stream);
+int cl_token_histogram_f32(cl_ctx* ctx, const float* d_values, uint64_t channels, uint64_t length,
+                           uint64_t channel_offset, const cl_hist_spec* spec,
+                           const double* d_trange, uint32_t* d_counts, void* stream);
+int cl_token_entropy_counts(cl_ctx* ctx, const uint32_t* d_counts, const double* d_trange,
+                            uint64_t length, uint64_t samples_per_position,
+                            const cl_hist_spec* spec, double* d_out, void* stream);
+/* Device decision from cl_token_entropy_f32's output for rule kind CL_POL_TOKEN_HIST or
+ * CL_POL_GUARDED with inner CL_POL_TOKEN_HIST (and any entropy-free kind).  Deferred
+ * errors (non-finite input, negative signal) as for cl_decide. */
+int cl_decide_token(cl_ctx* ctx, const double* d_token, const cl_hist_spec* spec,
+                    const cl_rule_spec* rule, uint64_t seq_len, cl_decision* d_out, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Host path (synchronous; used by include/chunklab/*.hpp)                    */
 /* ------------------------------------------------------------------------ */
@@ -231,10 +264,18 @@ int cl_scan_f64(cl_ctx* ctx, const cl_scan_params_f64* d_params, const double* d
 int cl_validate_hist_spec(cl_ctx* ctx, const cl_hist_spec* spec);
 int cl_validate_rule(cl_ctx* ctx, const cl_rule_spec* rule);
 
-/* compute_histogram(span, spec) (entropy.hpp:101-138) on the GPU. */
+/* all_finite over every value (validate_tensor, entropy.hpp:42), on the GPU. */
+int cl_all_finite_host(cl_ctx* ctx, const double* h_values, uint64_t n, int* h_all_finite);
+/* compute_histogram(span, spec) (entropy.hpp:101-138) on the GPU.  Like the reference's
+ * span overload, only the sampled values (index % stride == 0) are checked for
+ * finiteness; the tensor overload adds cl_all_finite_host first. */
 int cl_compute_histogram_host(cl_ctx* ctx, const double* h_values, uint64_t n,
                               const cl_hist_spec* spec, uint64_t* h_counts, double* h_masses,
                               double* h_lo, double* h_hi, uint64_t* h_sample_count);
+/* token_entropy(tensor, spec) (entropy.hpp:180-210) on the GPU, host fp64 values. */
+int cl_token_entropy_host(cl_ctx* ctx, const double* h_values, uint64_t channels,
+                          uint64_t length, const cl_hist_spec* spec, double* h_raw,
+                          double* h_normalized, uint64_t* h_sample_count);
 /* estimate_entropy(hist, eps) (entropy.hpp:149-164) on the GPU. */
 int cl_estimate_entropy_host(cl_ctx* ctx, const double* h_masses, int bin_count, double epsilon,
                              double* h_raw, double* h_normalized);
@@ -248,6 +289,8 @@ typedef struct {
   double sampled_entropy_nats;
   int has_seq_len;
   uint64_t seq_len;
+  int has_token_entropy; /* ScheduleFeatures::token_entropy (chunk.hpp:188) */
+  double token_entropy_nats;
 } cl_features;
 int cl_schedule_host(cl_ctx* ctx, const cl_rule_spec* rule, const cl_features* features,
                      cl_decision* h_out);

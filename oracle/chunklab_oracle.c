@@ -219,6 +219,41 @@ int or_compute_histogram(const double* values, size_t n_values, const or_hist_sp
   return OR_OK;
 }
 
+int or_token_entropy(const double* values, size_t channels, size_t length,
+                     const or_hist_spec* spec, double* raw_nats, double* normalized,
+                     uint64_t* sample_count) {
+  /* entropy.hpp:182-186: validate_tensor, validate_spec; the caller passes the shape */
+  for (size_t i = 0; i < channels * length; ++i)
+    if (!isfinite(values[i])) return OR_NON_FINITE;
+  int rc = or_validate_spec(spec);
+  if (rc) return rc;
+  const int k = spec->bin_count;
+  double* slice = (double*)malloc(sizeof(double) * (channels ? channels : 1));
+  uint64_t* counts = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)k);
+  double* masses = (double*)malloc(sizeof(double) * (size_t)k);
+  double raw_sum = 0.0;
+  uint64_t samples = 0;
+  for (size_t t = 0; t < length && rc == OR_OK; ++t) {
+    for (size_t c = 0; c < channels; ++c) slice[c] = values[c * length + t];
+    double lo, hi, raw, norm;
+    uint64_t n;
+    rc = or_compute_histogram(slice, channels, spec, counts, masses, &lo, &hi, &n);
+    if (rc == OR_OK) rc = or_estimate_entropy(masses, k, spec->epsilon, &raw, &norm);
+    if (rc == OR_OK) {
+      raw_sum += raw;
+      samples += n;
+    }
+  }
+  free(slice);
+  free(counts);
+  free(masses);
+  if (rc) return rc;
+  *raw_nats = raw_sum / (double)length;
+  *normalized = *raw_nats / log((double)k);
+  *sample_count = samples;
+  return OR_OK;
+}
+
 int or_compute_histogram_f32(const float* values, size_t n_values, const or_hist_spec* spec,
                              uint64_t* counts, double* lo_out, double* hi_out,
                              uint64_t* sample_count) {

@@ -95,6 +95,14 @@ int or_compute_histogram(const double* values, size_t n_values, const or_hist_sp
 int or_estimate_entropy(const double* masses, int k, double epsilon, double* raw_nats,
                         double* normalized);
 
+/* token_entropy (entropy.hpp:180-210): values as (channels, length), length contiguous;
+ * per position t the slice values[c*length + t], c = 0..channels-1, through
+ * compute_histogram + estimate_entropy; raw entropies averaged in position order.
+ * The whole tensor is validated first (validate_tensor: every value finite). */
+int or_token_entropy(const double* values, size_t channels, size_t length,
+                     const or_hist_spec* spec, double* raw_nats, double* normalized,
+                     uint64_t* sample_count);
+
 /* ---- chunk rule + scheduler family (chunk.hpp) ---- */
 int or_log2_exact(uint64_t v);                                     /* common.hpp:25-32 */
 double or_round_half_up(double x);                                 /* common.hpp:35 */

@@ -116,6 +116,17 @@ class Port(_Lib):
         self._check(rc)
         return counts, lo.value, hi.value, n.value
 
+    def token_entropy(self, values, bin_count=256, epsilon=1e-8, stride=1, fixed=None):
+        """values (channels, length) -> (raw_nats, normalized, sample_count)."""
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        channels, length = values.shape
+        spec = HistSpec(bin_count, epsilon, 1 if fixed else 0,
+                        fixed[0] if fixed else 0.0, fixed[1] if fixed else 0.0, stride)
+        raw, norm, n = C.c_double(), C.c_double(), C.c_uint64()
+        self._check(self.lib.or_token_entropy(_ptr(values, _dp), C.c_size_t(channels), C.c_size_t(length),
+                                       C.byref(spec), C.byref(raw), C.byref(norm), C.byref(n)))
+        return raw.value, norm.value, n.value
+
     def entropy(self, masses, epsilon=1e-8):
         masses = np.ascontiguousarray(masses, dtype=np.float64)
         raw, norm = C.c_double(), C.c_double()
@@ -235,6 +246,17 @@ class Reference(_Lib):
                                                 C.byref(hi), C.byref(n))
         self._check(rc)
         return masses, lo.value, hi.value, n.value
+
+    def token_entropy(self, values, bin_count=256, epsilon=1e-8, stride=1, fixed=None):
+        """values (channels, length) -> (raw_nats, normalized, sample_count)."""
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        channels, length = values.shape
+        spec = HistSpec(bin_count, epsilon, 1 if fixed else 0,
+                        fixed[0] if fixed else 0.0, fixed[1] if fixed else 0.0, stride)
+        raw, norm, n = C.c_double(), C.c_double(), C.c_uint64()
+        self._check(self.lib.ref_token_entropy(_ptr(values, _dp), C.c_uint64(channels), C.c_uint64(length),
+                                       C.byref(spec), C.byref(raw), C.byref(norm), C.byref(n)))
+        return raw.value, norm.value, n.value
 
     def entropy(self, masses, epsilon=1e-8):
         masses = np.ascontiguousarray(masses, dtype=np.float64)

@@ -149,6 +149,20 @@ int ref_compute_histogram_f32(const float* values, uint64_t n, const RefHistSpec
   });
 }
 
+// token_entropy(tensor (channels, length), spec) (entropy.hpp:180-210).
+int ref_token_entropy(const double* values, uint64_t channels, uint64_t length,
+                      const RefHistSpec* spec, double* raw, double* norm, uint64_t* count) {
+  return guarded([&] {
+    ActivationTensor t;
+    t.values.assign(values, values + channels * length);
+    t.shape = {static_cast<std::size_t>(channels), static_cast<std::size_t>(length)};
+    EntropyEstimate e = token_entropy(t, to_spec(spec));
+    *raw = e.raw_nats;
+    *norm = e.normalized;
+    *count = e.sample_count;
+  });
+}
+
 int ref_estimate_entropy(const double* masses, int k, double eps, double* raw, double* norm) {
   return guarded([&] {
     Histogram h;

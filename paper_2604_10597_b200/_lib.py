@@ -16,12 +16,12 @@ LIB_PATH = os.environ.get("CHUNKLAB_LIB", os.path.join(PKG, "libchunklab_b200.so
 CL_OK, CL_E_INVALID, CL_E_CUDA, CL_E_DEVICE, CL_E_NOMEM = range(5)
 CL_RANGE_DYNAMIC, CL_RANGE_FIXED = 0, 1
 (CL_POL_STATIC, CL_POL_MIDPOINT, CL_POL_FULL_HIST, CL_POL_SAMPLED_HIST, CL_POL_LEARNED_TABLE,
- CL_POL_GUARDED, CL_POL_RULE) = range(7)
+ CL_POL_GUARDED, CL_POL_RULE, CL_POL_TOKEN_HIST) = range(8)
 CL_SRC_GUARDED, CL_SRC_GUARDED_FALLBACK = 16, 32
 CL_SCAN_AUTO, CL_SCAN_ROWSEQ_TMA, CL_SCAN_GENERIC = 0, 1, 2
 
 SOURCE_NAMES = {0: "static", 1: "no_entropy_midpoint", 2: "full_histogram",
-                3: "sampled_histogram", 4: "learned_table", 6: "rule"}
+                3: "sampled_histogram", 4: "learned_table", 6: "rule", 7: "token_histogram"}
 
 
 def source_tag(code: int) -> str:
@@ -57,7 +57,8 @@ class cl_decision(C.Structure):
 class cl_features(C.Structure):
     _fields_ = [("has_full_entropy", C.c_int), ("full_entropy_nats", C.c_double),
                 ("has_sampled_entropy", C.c_int), ("sampled_entropy_nats", C.c_double),
-                ("has_seq_len", C.c_int), ("seq_len", C.c_uint64)]
+                ("has_seq_len", C.c_int), ("seq_len", C.c_uint64),
+                ("has_token_entropy", C.c_int), ("token_entropy_nats", C.c_double)]
 
 
 class cl_mamba1_args(C.Structure):
@@ -97,15 +98,28 @@ SIGNATURES = {
     "cl_histogram_f64": (C.c_int, [_P, _P, _u64, _u64, C.POINTER(cl_hist_spec), _P, _P, _P]),
     "cl_decide": (C.c_int, [_P, _P, _P, C.POINTER(cl_hist_spec), _u64, C.POINTER(cl_rule_spec),
                             _u64, _P, _P]),
+    "cl_token_entropy_f32": (C.c_int, [_P, _P, _u64, _u64, C.POINTER(cl_hist_spec), _P, _P]),
+    "cl_token_range_init": (C.c_int, [_P, _P, _u64, _P]),
+    "cl_token_minmax_f32": (C.c_int, [_P, _P, _u64, _u64, _u64, _u64, _P, _P]),
+    "cl_token_histogram_f32": (C.c_int, [_P, _P, _u64, _u64, _u64, C.POINTER(cl_hist_spec), _P,
+                                         _P, _P]),
+    "cl_token_entropy_counts": (C.c_int, [_P, _P, _P, _u64, _u64, C.POINTER(cl_hist_spec), _P,
+                                          _P]),
+    "cl_decide_token": (C.c_int, [_P, _P, C.POINTER(cl_hist_spec), C.POINTER(cl_rule_spec), _u64,
+                                  _P, _P]),
     "cl_selective_scan_f32": (C.c_int, [_P, C.POINTER(cl_mamba1_args), _P, C.c_int, C.c_int,
                                         _P]),
     "cl_prefill_f32": (C.c_int, [_P, C.POINTER(cl_mamba1_args), C.POINTER(cl_hist_spec),
                                  C.POINTER(cl_rule_spec), _P, _P, _P, _P]),
     "cl_decision_check": (C.c_int, [_P, _P, C.POINTER(cl_decision), _P]),
     "cl_scan_f64": (C.c_int, [_P, C.POINTER(cl_scan_params_f64), _P, _u64, _P, _P, _P]),
+    "cl_all_finite_host": (C.c_int, [_P, _P, _u64, C.POINTER(C.c_int)]),
     "cl_compute_histogram_host": (C.c_int, [_P, _P, _u64, C.POINTER(cl_hist_spec), _P, _P,
                                             C.POINTER(C.c_double), C.POINTER(C.c_double),
                                             C.POINTER(C.c_uint64)]),
+    "cl_token_entropy_host": (C.c_int, [_P, _P, _u64, _u64, C.POINTER(cl_hist_spec),
+                                        C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                        C.POINTER(C.c_uint64)]),
     "cl_estimate_entropy_host": (C.c_int, [_P, _P, C.c_int, C.c_double, C.POINTER(C.c_double),
                                            C.POINTER(C.c_double)]),
     "cl_schedule_host": (C.c_int, [_P, C.POINTER(cl_rule_spec), C.POINTER(cl_features),

@@ -31,6 +31,7 @@ from ._lib import Context, InvalidInput
 __all__ = [
     "InvalidInput", "RangeMode", "HistogramSpec", "ActivationTensor", "Histogram",
     "EntropyEstimate", "compute_histogram", "estimate_entropy", "estimate_tensor_entropy",
+    "token_entropy", "EmaState", "update_ema", "TokenHistogramPolicy",
     "ChunkBounds", "CalibrationRef", "ChunkDecision", "select_chunk", "kernel_calls",
     "StaticPolicy", "NoEntropyMidpointPolicy", "FullHistogramPolicy", "SampledHistogramPolicy",
     "GuardedPolicy", "LearnedTablePolicy", "SchedulerPolicy", "ScheduleFeatures", "Scheduler",
@@ -133,6 +134,14 @@ def _as_f64(values) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(values, dtype=np.float64).reshape(-1))
 
 
+def _require_all_finite(v: np.ndarray, ctx: Context) -> None:
+    """validate_tensor's value check (entropy.hpp:42) over every value, on the device."""
+    ok = C.c_int()
+    ctx.call("cl_all_finite_host", v.ctypes.data_as(C.c_void_p), v.size, C.byref(ok))
+    if not ok.value:
+        raise InvalidInput("non-finite input")
+
+
 def compute_histogram(values: Union[ActivationTensor, Sequence[float], np.ndarray],
                       spec: HistogramSpec, ctx: Optional[Context] = None) -> Histogram:
     """compute_histogram (entropy.hpp:101-145) on the GPU; counts bit-exact."""
@@ -142,6 +151,7 @@ def compute_histogram(values: Union[ActivationTensor, Sequence[float], np.ndarra
             raise InvalidInput("no samples")
         validate_tensor(values)
         v = _as_f64(values.values)
+        _require_all_finite(v, ctx)
     else:
         v = _as_f64(values)
     cspec = spec.to_c()
@@ -169,6 +179,46 @@ def estimate_entropy(hist: Histogram, epsilon: float, ctx: Optional[Context] = N
              float(epsilon), C.byref(raw), C.byref(norm))
     return EntropyEstimate(raw_nats=raw.value, normalized=norm.value, bin_count=int(m.size),
                            epsilon=float(epsilon), sample_count=int(hist.sample_count))
+
+
+def token_entropy(tensor: ActivationTensor, spec: HistogramSpec,
+                  ctx: Optional[Context] = None) -> EntropyEstimate:
+    """token_entropy (entropy.hpp:180-210) on the GPU: one histogram per position of the
+    last axis over that position's channel values, raw entropies averaged."""
+    ctx = ctx or Context.get()
+    if tensor.size() == 0:
+        raise InvalidInput("no samples")
+    validate_tensor(tensor)
+    v = _as_f64(tensor.values)
+    _require_all_finite(v, ctx)
+    cspec = spec.to_c()
+    ctx.call("cl_validate_hist_spec", C.byref(cspec))
+    if len(tensor.shape) < 2:
+        raise InvalidInput("token entropy needs a (channels, length) tensor")
+    length = int(tensor.shape[-1])
+    channels = v.size // length
+    raw, norm, n = C.c_double(), C.c_double(), C.c_uint64()
+    ctx.call("cl_token_entropy_host", v.ctypes.data_as(C.c_void_p), channels, length,
+             C.byref(cspec), C.byref(raw), C.byref(norm), C.byref(n))
+    return EntropyEstimate(raw_nats=raw.value, normalized=norm.value,
+                           bin_count=int(spec.bin_count), epsilon=float(spec.epsilon),
+                           sample_stride=int(spec.sample_stride), sample_count=int(n.value))
+
+
+@dataclass
+class EmaState:
+    """entropy.hpp:214-218."""
+    current: float = 0.0
+    decay: float = 0.85
+    update_count: int = 0
+
+
+def update_ema(state: EmaState, new_h: float) -> EmaState:
+    """entropy.hpp:220-227: H_t = decay * H_{t-1} + (1 - decay) * H_new (a host scalar)."""
+    if not (0.0 <= state.decay < 1.0):
+        raise InvalidInput("ema decay must lie in [0,1)")
+    return EmaState(state.decay * state.current + (1.0 - state.decay) * float(new_h),
+                    state.decay, state.update_count + 1)
 
 
 def estimate_tensor_entropy(tensor: ActivationTensor, spec: HistogramSpec,
@@ -255,6 +305,11 @@ class SampledHistogramPolicy:
 
 
 @dataclass
+class TokenHistogramPolicy:
+    """chunk.hpp:119 / :311-315: the rule on token_entropy."""
+
+
+@dataclass
 class LearnedTablePolicy:
     threshold_tokens: int = 50
     short_chunk: int = 128
@@ -280,12 +335,14 @@ class ScheduleFeatures:
     full_entropy: Optional[EntropyEstimate] = None
     sampled_entropy: Optional[EntropyEstimate] = None
     seq_len: Optional[int] = None
+    token_entropy: Optional[EntropyEstimate] = None
 
 
 _KIND = {StaticPolicy: _lib.CL_POL_STATIC, NoEntropyMidpointPolicy: _lib.CL_POL_MIDPOINT,
          FullHistogramPolicy: _lib.CL_POL_FULL_HIST,
          SampledHistogramPolicy: _lib.CL_POL_SAMPLED_HIST,
-         LearnedTablePolicy: _lib.CL_POL_LEARNED_TABLE, GuardedPolicy: _lib.CL_POL_GUARDED}
+         LearnedTablePolicy: _lib.CL_POL_LEARNED_TABLE, GuardedPolicy: _lib.CL_POL_GUARDED,
+         TokenHistogramPolicy: _lib.CL_POL_TOKEN_HIST}
 
 
 def _fill_simple(spec: _lib.cl_rule_spec, v, inner: bool):
@@ -380,6 +437,9 @@ class Scheduler:
         if features.seq_len is not None:
             f.has_seq_len = 1
             f.seq_len = int(features.seq_len)
+        if features.token_entropy is not None:
+            f.has_token_entropy = 1
+            f.token_entropy_nats = float(features.token_entropy.raw_nats)
         out = _lib.cl_decision()
         self.ctx.call("cl_schedule_host", C.byref(self._spec), C.byref(f), C.byref(out))
         return _decision_from_c(out)

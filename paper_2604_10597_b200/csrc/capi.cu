@@ -85,7 +85,7 @@ int validate_rule(cl_ctx* ctx, const cl_rule_spec* r) {
       break;
     case CL_POL_GUARDED:
       if (r->inner_kind == CL_POL_GUARDED || r->inner_kind == CL_POL_RULE ||
-          r->inner_kind < 0 || r->inner_kind > CL_POL_LEARNED_TABLE)
+          r->inner_kind < 0 || r->inner_kind > CL_POL_TOKEN_HIST)
         return fail(ctx, CL_E_INVALID, "guarded policy needs an inner policy");
       if (!member(r, r->safe_chunk)) return fail(ctx, CL_E_INVALID, "safe chunk not in bucket_set");
       if (r->min_delta_buckets < 0)
@@ -103,6 +103,7 @@ int validate_rule(cl_ctx* ctx, const cl_rule_spec* r) {
     case CL_POL_MIDPOINT:
     case CL_POL_FULL_HIST:
     case CL_POL_SAMPLED_HIST:
+    case CL_POL_TOKEN_HIST:
     case CL_POL_RULE:
       break;
     default:
@@ -199,6 +200,10 @@ int cl_ctx_destroy(cl_ctx* ctx) {
   cudaFree(ctx->d_work);
   cudaFree(ctx->d_carry);
   cudaFree(ctx->d_bct);
+  cudaFree(ctx->d_token_raw);
+  cudaFree(ctx->d_token_range);
+  cudaFree(ctx->d_token_counts);
+  cudaFree(ctx->d_token_out);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return CL_OK;
@@ -316,6 +321,163 @@ int cl_decide(cl_ctx* ctx, const uint64_t* d_counts, const double* d_range,
                       "decide");
 }
 
+extern "C++" {
+namespace {
+int validate_token(cl_ctx* ctx, const cl_hist_spec* spec, uint64_t channels, uint64_t length) {
+  int rc = validate_spec(ctx, spec);
+  if (rc) return rc;
+  if (channels == 0 || length == 0) return fail(ctx, CL_E_INVALID, "no samples");
+  if (spec->bin_count > 4096)
+    return fail(ctx, CL_E_INVALID, "token entropy supports bin_count <= 4096");
+  return CL_OK;
+}
+
+template <typename P>
+int grow_bytes(cl_ctx* ctx, P** ptr, size_t* have, size_t need) {
+  if (*have >= need) return CL_OK;
+  cudaFree(*ptr);
+  *ptr = nullptr;
+  *have = 0;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), need);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(token entropy scratch)");
+  *have = need;
+  return CL_OK;
+}
+
+int grow_token(cl_ctx* ctx, uint64_t length, int k) {
+  int rc = grow_bytes(ctx, &ctx->d_token_raw, &ctx->token_raw_bytes, length * sizeof(double));
+  if (!rc)
+    rc = grow_bytes(ctx, &ctx->d_token_range, &ctx->token_range_bytes,
+                    (2 * length + 1) * sizeof(double));
+  if (!rc)
+    rc = grow_bytes(ctx, &ctx->d_token_counts, &ctx->token_counts_bytes,
+                    length * static_cast<size_t>(k) * sizeof(unsigned int));
+  return rc;
+}
+
+// the four stages over one device tensor with the context's scratch
+template <typename T>
+cudaError_t token_pipeline(cl_ctx* ctx, const T* d_values, uint64_t channels, uint64_t length,
+                           const cl_hist_spec& spec, double* d_out, cudaStream_t s) {
+  double* trange = ctx->d_token_range;
+  double* flag = ctx->d_token_range + 2 * length;
+  cudaError_t e = launch_token_range_init(trange, flag, length, s);
+  if (e == cudaSuccess)
+    e = launch_token_minmax<T>(d_values, channels, length, 0, spec.sample_stride, trange, flag,
+                               ctx->num_sms, s);
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(ctx->d_token_counts, 0,
+                        length * static_cast<size_t>(spec.bin_count) * sizeof(unsigned int), s);
+  if (e == cudaSuccess)
+    e = launch_token_hist<T>(d_values, channels, length, 0, spec, trange, ctx->d_token_counts,
+                             ctx->num_sms, s);
+  if (e == cudaSuccess)
+    e = launch_token_entropy(ctx->d_token_counts, length, samples_of(channels, spec.sample_stride),
+                             spec, flag, ctx->d_token_raw, d_out, s);
+  ctx->launches += 5;
+  return e;
+}
+}  // namespace
+}  // extern "C++"
+
+int cl_token_range_init(cl_ctx* ctx, double* d_trange, uint64_t length, void* stream) {
+  if (!ctx || !d_trange) return fail(ctx, CL_E_INVALID, "null argument");
+  DeviceGuard g(ctx->device);
+  ++ctx->launches;
+  return check_launch(ctx,
+                      launch_token_range_init(d_trange, d_trange + 2 * length, length,
+                                              static_cast<cudaStream_t>(stream)),
+                      "token_range_init");
+}
+
+int cl_token_minmax_f32(cl_ctx* ctx, const float* d_values, uint64_t channels, uint64_t length,
+                        uint64_t channel_offset, uint64_t stride, double* d_trange,
+                        void* stream) {
+  if (!ctx || !d_trange || (!d_values && channels && length))
+    return fail(ctx, CL_E_INVALID, "null argument");
+  if (stride < 1) return fail(ctx, CL_E_INVALID, "stride must be >= 1");
+  if (channels == 0 || length == 0) return CL_OK;
+  DeviceGuard g(ctx->device);
+  ++ctx->launches;
+  return check_launch(ctx,
+                      launch_token_minmax<float>(d_values, channels, length, channel_offset,
+                                                 stride, d_trange, d_trange + 2 * length,
+                                                 ctx->num_sms,
+                                                 static_cast<cudaStream_t>(stream)),
+                      "token_minmax_f32");
+}
+
+int cl_token_histogram_f32(cl_ctx* ctx, const float* d_values, uint64_t channels, uint64_t length,
+                           uint64_t channel_offset, const cl_hist_spec* spec,
+                           const double* d_trange, uint32_t* d_counts, void* stream) {
+  if (!ctx) return CL_E_INVALID;
+  int rc = validate_spec(ctx, spec);
+  if (rc) return rc;
+  if (spec->bin_count > 4096)
+    return fail(ctx, CL_E_INVALID, "token entropy supports bin_count <= 4096");
+  if (!d_trange || !d_counts || (!d_values && channels && length))
+    return fail(ctx, CL_E_INVALID, "null argument");
+  if (channels == 0 || length == 0) return CL_OK;
+  DeviceGuard g(ctx->device);
+  ++ctx->launches;
+  return check_launch(ctx,
+                      launch_token_hist<float>(d_values, channels, length, channel_offset, *spec,
+                                               d_trange, d_counts, ctx->num_sms,
+                                               static_cast<cudaStream_t>(stream)),
+                      "token_histogram_f32");
+}
+
+int cl_token_entropy_counts(cl_ctx* ctx, const uint32_t* d_counts, const double* d_trange,
+                            uint64_t length, uint64_t samples_per_position,
+                            const cl_hist_spec* spec, double* d_out, void* stream) {
+  if (!ctx) return CL_E_INVALID;
+  int rc = validate_spec(ctx, spec);
+  if (rc) return rc;
+  if (!d_counts || !d_trange || !d_out) return fail(ctx, CL_E_INVALID, "null argument");
+  if (length == 0 || samples_per_position == 0) return fail(ctx, CL_E_INVALID, "no samples");
+  DeviceGuard g(ctx->device);
+  if ((rc = grow_bytes(ctx, &ctx->d_token_raw, &ctx->token_raw_bytes, length * sizeof(double))))
+    return rc;
+  ctx->launches += 2;
+  return check_launch(ctx,
+                      launch_token_entropy(d_counts, length, samples_per_position, *spec,
+                                           d_trange + 2 * length, ctx->d_token_raw, d_out,
+                                           static_cast<cudaStream_t>(stream)),
+                      "token_entropy");
+}
+
+int cl_token_entropy_f32(cl_ctx* ctx, const float* d_values, uint64_t channels, uint64_t length,
+                         const cl_hist_spec* spec, double* d_out, void* stream) {
+  if (!ctx) return CL_E_INVALID;
+  int rc = validate_token(ctx, spec, channels, length);
+  if (rc) return rc;
+  if (!d_values || !d_out) return fail(ctx, CL_E_INVALID, "null argument");
+  DeviceGuard g(ctx->device);
+  if ((rc = grow_token(ctx, length, spec->bin_count))) return rc;
+  return check_launch(ctx,
+                      token_pipeline<float>(ctx, d_values, channels, length, *spec, d_out,
+                                            static_cast<cudaStream_t>(stream)),
+                      "token_entropy_f32");
+}
+
+int cl_decide_token(cl_ctx* ctx, const double* d_token, const cl_hist_spec* spec,
+                    const cl_rule_spec* rule, uint64_t seq_len, cl_decision* d_out,
+                    void* stream) {
+  int rc = validate_spec(ctx, spec);
+  if (rc) return rc;
+  if ((rc = validate_rule(ctx, rule))) return rc;
+  if (!d_token || !d_out) return fail(ctx, CL_E_INVALID, "null argument");
+  const int kind = rule->kind == CL_POL_GUARDED ? rule->inner_kind : rule->kind;
+  if (kind == CL_POL_FULL_HIST || kind == CL_POL_SAMPLED_HIST || kind == CL_POL_RULE)
+    return fail(ctx, CL_E_INVALID, "token decision needs a token_histogram policy");
+  DeviceGuard g(ctx->device);
+  ++ctx->launches;
+  return check_launch(ctx,
+                      launch_decide_token(d_token, *spec, *rule, seq_len, d_out,
+                                          static_cast<cudaStream_t>(stream)),
+                      "decide_token");
+}
+
 int cl_selective_scan_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_decision* d_decision,
                           int fixed_chunk, int variant, void* stream) {
   if (!ctx || !args) return fail(ctx, CL_E_INVALID, "null argument");
@@ -383,6 +545,31 @@ int cl_scan_f64(cl_ctx* ctx, const cl_scan_params_f64* p, const double* d_h0, ui
 }
 
 // ------------------------------------------------------------------ host path
+int cl_all_finite_host(cl_ctx* ctx, const double* h_values, uint64_t n, int* h_all_finite) {
+  if (!ctx) return CL_E_INVALID;
+  if ((n && !h_values) || !h_all_finite) return fail(ctx, CL_E_INVALID, "null argument");
+  *h_all_finite = 1;
+  if (n == 0) return CL_OK;
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = ctx->own_stream;
+  DevBuf<double> dv;
+  cudaError_t e = dv.alloc(n);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc");
+  if ((e = cudaMemcpyAsync(dv.p, h_values, n * sizeof(double), cudaMemcpyHostToDevice, s)) !=
+      cudaSuccess)
+    return cuda_fail(ctx, e, "cudaMemcpyAsync");
+  int rc;
+  if ((rc = cl_range_init(ctx, ctx->d_scratch_range, s))) return rc;
+  if ((rc = cl_minmax_f64(ctx, dv.p, n, 0, 1, ctx->d_scratch_range, s))) return rc;
+  double range[4];
+  if ((e = cudaMemcpyAsync(range, ctx->d_scratch_range, sizeof range, cudaMemcpyDeviceToHost,
+                           s)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(s)) != cudaSuccess)
+    return cuda_fail(ctx, e, "finite readback");
+  *h_all_finite = range[2] == 0.0;
+  return CL_OK;
+}
+
 int cl_compute_histogram_host(cl_ctx* ctx, const double* h_values, uint64_t n,
                               const cl_hist_spec* spec, uint64_t* h_counts, double* h_masses,
                               double* h_lo, double* h_hi, uint64_t* h_sample_count) {
@@ -390,6 +577,18 @@ int cl_compute_histogram_host(cl_ctx* ctx, const double* h_values, uint64_t n,
   int rc = validate_spec(ctx, spec);
   if (rc) return rc;
   if (n == 0) return fail(ctx, CL_E_INVALID, "no samples");
+  // The span overload visits values[0], values[stride], ... only (entropy.hpp:108-114):
+  // gather that subsequence so the device pass -- including its finite check -- sees
+  // exactly the values the reference visits; binning then runs at stride 1.
+  std::vector<double> gathered;
+  cl_hist_spec sp = *spec;
+  if (spec->sample_stride > 1) {
+    gathered.reserve(samples_of(n, spec->sample_stride));
+    for (uint64_t i = 0; i < n; i += spec->sample_stride) gathered.push_back(h_values[i]);
+    h_values = gathered.data();
+    n = gathered.size();
+    sp.sample_stride = 1;
+  }
   DeviceGuard g(ctx->device);
   cudaStream_t s = ctx->own_stream;
   DevBuf<double> dv;
@@ -401,33 +600,65 @@ int cl_compute_histogram_host(cl_ctx* ctx, const double* h_values, uint64_t n,
   double* d_range = ctx->d_scratch_range;
   uint64_t* d_counts = ctx->d_scratch_counts;
   if ((rc = cl_range_init(ctx, d_range, s))) return rc;
-  if ((rc = cl_minmax_f64(ctx, dv.p, n, 0, spec->sample_stride, d_range, s))) return rc;
+  if ((rc = cl_minmax_f64(ctx, dv.p, n, 0, 1, d_range, s))) return rc;
   double range[4];
   if ((e = cudaMemcpyAsync(range, d_range, sizeof range, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
       (e = cudaStreamSynchronize(s)) != cudaSuccess)
     return cuda_fail(ctx, e, "minmax readback");
-  // entropy.hpp:110: the reference throws on the first non-finite sample; the
-  // tensor overload (:140-145) validates every value first.
+  // entropy.hpp:110: the reference throws on the first non-finite sampled value
   if (range[2] != 0.0) return fail(ctx, CL_E_INVALID, "non-finite input");
-  if ((rc = cl_counts_zero(ctx, d_counts, spec->bin_count, s))) return rc;
-  if ((rc = cl_histogram_f64(ctx, dv.p, n, 0, spec, d_range, d_counts, s))) return rc;
-  std::vector<uint64_t> counts(spec->bin_count);
+  if ((rc = cl_counts_zero(ctx, d_counts, sp.bin_count, s))) return rc;
+  if ((rc = cl_histogram_f64(ctx, dv.p, n, 0, &sp, d_range, d_counts, s))) return rc;
+  std::vector<uint64_t> counts(sp.bin_count);
   if ((e = cudaMemcpyAsync(counts.data(), d_counts, counts.size() * sizeof(uint64_t),
                            cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
       (e = cudaStreamSynchronize(s)) != cudaSuccess)
     return cuda_fail(ctx, e, "counts readback");
-  const uint64_t ns = samples_of(n, spec->sample_stride);
+  const uint64_t ns = n;
   if (h_counts) std::memcpy(h_counts, counts.data(), counts.size() * sizeof(uint64_t));
   if (h_masses) {
     // masses[b] = counts[b] * (1/n) (entropy.hpp:130-133); exact IEEE ops on the host
     // are identical to the device's, kept here to avoid another round trip.
     const double inv_n = 1.0 / static_cast<double>(ns);
-    for (int b = 0; b < spec->bin_count; ++b)
-      h_masses[b] = static_cast<double>(counts[b]) * inv_n;
+    for (int b = 0; b < sp.bin_count; ++b) h_masses[b] = static_cast<double>(counts[b]) * inv_n;
   }
-  if (h_lo) *h_lo = spec->range_mode == CL_RANGE_FIXED ? spec->fixed_lo : -range[0];
-  if (h_hi) *h_hi = spec->range_mode == CL_RANGE_FIXED ? spec->fixed_hi : range[1];
+  if (h_lo) *h_lo = sp.range_mode == CL_RANGE_FIXED ? sp.fixed_lo : -range[0];
+  if (h_hi) *h_hi = sp.range_mode == CL_RANGE_FIXED ? sp.fixed_hi : range[1];
   if (h_sample_count) *h_sample_count = ns;
+  return CL_OK;
+}
+
+int cl_token_entropy_host(cl_ctx* ctx, const double* h_values, uint64_t channels,
+                          uint64_t length, const cl_hist_spec* spec, double* h_raw,
+                          double* h_normalized, uint64_t* h_sample_count) {
+  if (!ctx) return CL_E_INVALID;
+  int rc = validate_token(ctx, spec, channels, length);
+  if (rc) return rc;
+  if (!h_values) return fail(ctx, CL_E_INVALID, "null argument");
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = ctx->own_stream;
+  const uint64_t n = channels * length;
+  DevBuf<double> dv;
+  cudaError_t e = dv.alloc(n);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc");
+  if ((rc = grow_bytes(ctx, &ctx->d_token_out, &ctx->token_out_bytes, 4 * sizeof(double))))
+    return rc;
+  if ((rc = grow_token(ctx, length, spec->bin_count))) return rc;
+  if ((e = cudaMemcpyAsync(dv.p, h_values, n * sizeof(double), cudaMemcpyHostToDevice, s)) !=
+      cudaSuccess)
+    return cuda_fail(ctx, e, "cudaMemcpyAsync");
+  if ((e = token_pipeline<double>(ctx, dv.p, channels, length, *spec, ctx->d_token_out, s)) !=
+      cudaSuccess)
+    return cuda_fail(ctx, e, "token_entropy_f64");
+  double out[4];
+  if ((e = cudaMemcpyAsync(out, ctx->d_token_out, sizeof out, cudaMemcpyDeviceToHost, s)) !=
+          cudaSuccess ||
+      (e = cudaStreamSynchronize(s)) != cudaSuccess)
+    return cuda_fail(ctx, e, "token entropy readback");
+  if (out[3] != 0.0) return fail(ctx, CL_E_INVALID, "non-finite input");
+  if (h_raw) *h_raw = out[0];
+  if (h_normalized) *h_normalized = out[1];
+  if (h_sample_count) *h_sample_count = static_cast<uint64_t>(out[2]);
   return CL_OK;
 }
 
@@ -473,6 +704,8 @@ int cl_schedule_host(cl_ctx* ctx, const cl_rule_spec* rule, const cl_features* f
     return fail(ctx, CL_E_INVALID, "missing feature: full_entropy");
   if (kind == CL_POL_LEARNED_TABLE && !features->has_seq_len)
     return fail(ctx, CL_E_INVALID, "missing feature: seq_len");
+  if (kind == CL_POL_TOKEN_HIST && !features->has_token_entropy)
+    return fail(ctx, CL_E_INVALID, "missing feature: token_entropy");
   DeviceGuard g(ctx->device);
   cudaStream_t s = ctx->own_stream;
   cl_hist_spec spec{256, 1e-8, 0, 0.0, 0.0, 1};

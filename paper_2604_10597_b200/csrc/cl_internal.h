@@ -23,6 +23,16 @@ struct cl_ctx {
   size_t carry_bytes = 0;
   float* d_bct = nullptr;  // B^T / C^T (b, L, N) for the TMA scan (grown on demand)
   size_t bct_bytes = 0;
+  // token_entropy scratch (grown on demand): per-position raw entropies [L], ranges
+  // [2L] + the finite flag, counts [L][K]; and the host path's 4-double result
+  double* d_token_raw = nullptr;
+  size_t token_raw_bytes = 0;
+  double* d_token_range = nullptr;
+  size_t token_range_bytes = 0;
+  unsigned int* d_token_counts = nullptr;
+  size_t token_counts_bytes = 0;
+  double* d_token_out = nullptr;
+  size_t token_out_bytes = 0;
   cudaStream_t own_stream = nullptr;
 };
 
@@ -53,6 +63,23 @@ cudaError_t launch_decide(const uint64_t* d_counts, const double* d_range,
                           const cl_hist_spec& spec, uint64_t n_samples, const cl_rule_spec& rule,
                           uint64_t seq_len, const cl_features* features_or_null,
                           cl_decision* d_out, cudaStream_t s);
+cudaError_t launch_decide_token(const double* d_token, const cl_hist_spec& spec,
+                                const cl_rule_spec& rule, uint64_t seq_len, cl_decision* d_out,
+                                cudaStream_t s);
+cudaError_t launch_token_range_init(double* d_trange, double* d_flag, uint64_t length,
+                                    cudaStream_t s);
+template <typename T>
+cudaError_t launch_token_minmax(const T* v, uint64_t channels, uint64_t length, uint64_t offset,
+                                uint64_t stride, double* d_trange, double* d_flag, int num_sms,
+                                cudaStream_t s);
+template <typename T>
+cudaError_t launch_token_hist(const T* v, uint64_t channels, uint64_t length, uint64_t offset,
+                              const cl_hist_spec& spec, const double* d_trange,
+                              unsigned int* d_counts, int num_sms, cudaStream_t s);
+cudaError_t launch_token_entropy(const unsigned int* d_counts, uint64_t length,
+                                 uint64_t n_per_pos, const cl_hist_spec& spec,
+                                 const double* d_flag, double* d_raw_t, double* d_out,
+                                 cudaStream_t s);
 cudaError_t launch_entropy_from_masses(const double* d_masses, int k, double eps, double* d_out,
                                        cudaStream_t s);
 // conv1d.cu

@@ -67,17 +67,8 @@ struct BinParams {
   int exact_only;    // fast path unusable (pathological fixed range)
 };
 
-__device__ BinParams make_bin_params(const double* d_range, int range_mode, double fixed_lo,
-                                     double fixed_hi, int k) {
+__device__ BinParams make_bin_params_lohi(double lo, double hi, int k) {
   BinParams p;
-  double lo, hi;
-  if (range_mode == CL_RANGE_FIXED) {
-    lo = fixed_lo;
-    hi = fixed_hi;
-  } else {
-    lo = -d_range[0];
-    hi = d_range[1];
-  }
   p.lo = lo;
   p.width = __dsub_rn(hi, lo);
   p.k = k;
@@ -102,6 +93,12 @@ __device__ BinParams make_bin_params(const double* d_range, int range_mode, doub
   p.thr = static_cast<float>(0.5 - delta);
   p.exact_only = ok ? 0 : 1;
   return p;
+}
+
+__device__ BinParams make_bin_params(const double* d_range, int range_mode, double fixed_lo,
+                                     double fixed_hi, int k) {
+  if (range_mode == CL_RANGE_FIXED) return make_bin_params_lohi(fixed_lo, fixed_hi, k);
+  return make_bin_params_lohi(-d_range[0], d_range[1], k);
 }
 
 // Fast bin: returns n = round(x') and sets *slow when the sample must take the exact
@@ -658,8 +655,9 @@ struct DecideArgs {
   uint64_t n_samples;
   cl_rule_spec rule;
   uint64_t seq_len;
-  int features_mode;  // 0: entropy from counts; 1: host features
+  int features_mode;  // 0: entropy from counts; 1: host features; 2: token entropy
   cl_features f;
+  const double* token;  // mode 2: cl_token_entropy output {raw, normalized, n, nonfinite}
 };
 
 __device__ __forceinline__ int ilog2_pow2(int v) { return 31 - __clz(v); }
@@ -722,6 +720,7 @@ __device__ int decide_simple(const DecideArgs& a, int kind, int static_chunk, do
     }
     case CL_POL_FULL_HIST:
     case CL_POL_SAMPLED_HIST:
+    case CL_POL_TOKEN_HIST:
     case CL_POL_RULE: {
       int c;
       double r;
@@ -731,11 +730,11 @@ __device__ int decide_simple(const DecideArgs& a, int kind, int static_chunk, do
       out.chunk = kind == CL_POL_RULE ? c : device_snap(c, rule);
       out.r = r;
       out.signal_nats = entropy;
-      out.source = kind == CL_POL_RULE ? 6 : (kind == CL_POL_FULL_HIST ? 2 : 3);
+      out.source = kind;  // CL_POL_* doubles as the source_policy tag code
       return 0;
     }
     case CL_POL_LEARNED_TABLE: {
-      const uint64_t L = a.features_mode ? a.f.seq_len : a.seq_len;
+      const uint64_t L = a.features_mode == 1 ? a.f.seq_len : a.seq_len;
       out.chunk = L < rule.threshold_tokens ? rule.short_chunk : rule.long_chunk;
       out.signal_nats = static_cast<double>(L);
       out.source = 4;
@@ -788,6 +787,15 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(DecideArgs a, cl_decis
     entropy = raw;
     if (bad) status = CL_DEV_NON_FINITE;
     else if (a.n_samples == 0) status = CL_DEV_NO_SAMPLES;
+  } else if (a.features_mode == 2) {
+    if (threadIdx.x != 0) return;
+    entropy = a.token[0];
+    out.raw_nats = a.token[0];
+    out.normalized = a.token[1];
+    out.sample_count = static_cast<uint64_t>(a.token[2]);
+    out.bin_count = a.k;
+    out.lo = out.hi = 0.0;  // one range per position: none to report
+    if (a.token[3] != 0.0) status = CL_DEV_NON_FINITE;
   } else {
     if (threadIdx.x != 0) return;
   }
@@ -795,9 +803,11 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(DecideArgs a, cl_decis
   if (status == 0) {
     const cl_rule_spec& rule = a.rule;
     double e_inner = entropy;
-    if (a.features_mode) {
+    if (a.features_mode == 1) {
       const int kind = rule.kind == CL_POL_GUARDED ? rule.inner_kind : rule.kind;
-      e_inner = kind == CL_POL_SAMPLED_HIST ? a.f.sampled_entropy_nats : a.f.full_entropy_nats;
+      e_inner = kind == CL_POL_SAMPLED_HIST ? a.f.sampled_entropy_nats
+                : kind == CL_POL_TOKEN_HIST ? a.f.token_entropy_nats
+                                            : a.f.full_entropy_nats;
     }
     if (rule.kind != CL_POL_GUARDED) {
       status = decide_simple(a, rule.kind, rule.static_chunk, e_inner, out);
@@ -818,6 +828,274 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(DecideArgs a, cl_decis
   }
   out.status = status;
   *d_out = out;
+}
+
+// ---------------------------------------------------------------------------
+// token_entropy (entropy.hpp:180-210): the tensor read as (channels, length), one
+// compute_histogram per position t over its channel slice (slice index c sampled iff
+// c % stride == 0; Dynamic range of the slice's samples or the Fixed range), and the
+// per-position raw entropies averaged in position order.
+//
+// Four stream-ordered stages (the multi-GPU protocol inserts its two collectives
+// between them, exactly as for the global histogram):
+//   1. token_minmax: blocks own a tile of kTokTile positions x a share of the channels;
+//      a thread loads 16 contiguous bytes of one channel row per step (a warp covers 4
+//      channel rows x 128 B), keeps per-position min/max + the finite flag, and the
+//      block folds them into trange [2][L] = {-lo, hi} with fp64 atomic max.
+//   2. token_hist: same tiling, per-position bin parameters from trange, an
+//      [kTokTile][K] u32 shared-memory histogram flushed into counts [L][K] (global
+//      atomics straight into counts when the tile does not fit shared memory).
+//   3. token_entropy: a warp per position, estimate_entropy in fp64, bin order.
+//   4. token_finalize: the ordered mean over positions.
+// Channel indices are global (channel_offset + c) so a row-sharded tensor samples the
+// same slice entries as the whole one.
+// ---------------------------------------------------------------------------
+constexpr int kTokTile = 32;  // positions per block tile (8 threads x float4)
+constexpr int kTokMaxSmemHist = 64 * 1024;
+
+template <typename T>
+struct TokVec {
+  static constexpr int kV = 16 / sizeof(T);  // elements per 16-byte load
+};
+
+struct TokArgs {
+  uint64_t channels, length, offset, stride;
+  int k;
+  int vec;  // 1: vector loads (length % kV == 0, aligned), 0: scalar
+};
+
+// Per-thread walk over this block's channel share with the sampled test kept as an
+// incremental c_global % stride.
+struct ChanWalk {
+  uint64_t c, end, cm, step_mod, stride;
+  __device__ ChanWalk(uint64_t c0, uint64_t end_, uint64_t offset, uint64_t step, uint64_t st)
+      : c(c0), end(end_), cm((offset + c0) % st), step_mod(step % st), stride(st) {}
+  __device__ __forceinline__ bool ok() const { return c < end; }
+  __device__ __forceinline__ bool sampled() const { return cm == 0; }
+  __device__ __forceinline__ void next(uint64_t step) {
+    c += step;
+    cm += step_mod;
+    if (cm >= stride) cm -= stride;
+  }
+};
+
+__device__ __forceinline__ void tok_channel_share(uint64_t channels, uint64_t* c0,
+                                                  uint64_t* c1) {
+  const uint64_t per = (channels + gridDim.y - 1) / gridDim.y;
+  *c0 = per * blockIdx.y;
+  *c1 = umin64(channels, *c0 + per);
+}
+
+// thread -> (position group g of 8, channel lane cl of 32); a group is kV positions for
+// vector loads (8 x kV = kTokTile for fp32) or 1 position for scalar loads.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kThreads) token_minmax_kernel(const T* __restrict__ v,
+                                                                TokArgs a, double* trange,
+                                                                double* flag) {
+  constexpr int kV = VEC ? TokVec<T>::kV : 1;
+  constexpr int kTile = 8 * kV;
+  const int g = threadIdx.x % 8, cl = threadIdx.x / 8;
+  const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kTile + g * kV;
+  uint64_t c0, c1;
+  tok_channel_share(a.channels, &c0, &c1);
+  double lo[kV], hi[kV];
+#pragma unroll
+  for (int e = 0; e < kV; ++e) {
+    lo[e] = INFINITY;
+    hi[e] = -INFINITY;
+  }
+  bool bad = false;
+  if (t0 < a.length) {
+    for (ChanWalk w(c0 + cl, c1, a.offset, kThreads / 8, a.stride); w.ok(); w.next(kThreads / 8)) {
+      const T* row = v + w.c * a.length + t0;
+      T x[kV];
+      if (VEC) {
+        *reinterpret_cast<typename Vec4<T>::type*>(x) =
+            __ldcs(reinterpret_cast<const typename Vec4<T>::type*>(row));
+      } else {
+        x[0] = row[0];
+      }
+#pragma unroll
+      for (int e = 0; e < kV; ++e) {
+        const double d = static_cast<double>(x[e]);
+        bad |= !finite_f64(d);
+        if (w.sampled()) {
+          lo[e] = fmin(lo[e], d);
+          hi[e] = fmax(hi[e], d);
+        }
+      }
+    }
+  }
+  // lanes g, g+8, g+16, g+24 of a warp share positions: fold them, then across warps
+#pragma unroll
+  for (int e = 0; e < kV; ++e) {
+    for (int o = 8; o < 32; o <<= 1) {
+      lo[e] = fmin(lo[e], __shfl_xor_sync(0xffffffffu, lo[e], o));
+      hi[e] = fmax(hi[e], __shfl_xor_sync(0xffffffffu, hi[e], o));
+    }
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  __shared__ double s_lo[kThreads / 32][kTile], s_hi[kThreads / 32][kTile];
+  __shared__ int s_bad[kThreads / 32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (lane < 8) {
+#pragma unroll
+    for (int e = 0; e < kV; ++e) {
+      s_lo[warp][lane * kV + e] = lo[e];
+      s_hi[warp][lane * kV + e] = hi[e];
+    }
+  }
+  if (lane == 0) s_bad[warp] = bad;
+  __syncthreads();
+  if (threadIdx.x < kTile) {
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * kTile + threadIdx.x;
+    double l = s_lo[0][threadIdx.x], h = s_hi[0][threadIdx.x];
+    for (int w = 1; w < kThreads / 32; ++w) {
+      l = fmin(l, s_lo[w][threadIdx.x]);
+      h = fmax(h, s_hi[w][threadIdx.x]);
+    }
+    if (t < a.length && h >= l) {
+      atomic_max_f64(trange + t, -l);
+      atomic_max_f64(trange + a.length + t, h);
+    }
+  }
+  if (threadIdx.x == 0) {
+    int b = 0;
+    for (int w = 0; w < kThreads / 32; ++w) b |= s_bad[w];
+    if (b) atomic_max_f64(flag, 1.0);
+  }
+}
+
+template <typename T, int VEC, bool FIXED, bool SMEM>
+__global__ void __launch_bounds__(kThreads) token_hist_kernel(const T* __restrict__ v,
+                                                              TokArgs a, const double* trange,
+                                                              double fixed_lo, double fixed_hi,
+                                                              unsigned int* counts) {
+  constexpr int kV = VEC ? TokVec<T>::kV : 1;
+  constexpr int kTile = 8 * kV;
+  extern __shared__ unsigned int thist[];  // [kTile][k] when SMEM
+  __shared__ BinParams bp[kTile];
+  const int k = a.k;
+  const uint64_t tb = static_cast<uint64_t>(blockIdx.x) * kTile;
+  if (SMEM)
+    for (int i = threadIdx.x; i < kTile * k; i += kThreads) thist[i] = 0u;
+  if (threadIdx.x < kTile) {
+    const uint64_t t = tb + threadIdx.x;
+    bp[threadIdx.x] = FIXED ? make_bin_params_lohi(fixed_lo, fixed_hi, k)
+                    : t < a.length ? make_bin_params_lohi(-trange[t], trange[a.length + t], k)
+                                   : make_bin_params_lohi(0.0, 0.0, k);
+  }
+  __syncthreads();
+  const int g = threadIdx.x % 8, cl = threadIdx.x / 8;
+  const uint64_t t0 = tb + g * kV;
+  uint64_t c0, c1;
+  tok_channel_share(a.channels, &c0, &c1);
+  if (t0 < a.length) {
+    BinParams P[kV];
+#pragma unroll
+    for (int e = 0; e < kV; ++e) P[e] = bp[g * kV + e];
+    for (ChanWalk w(c0 + cl, c1, a.offset, kThreads / 8, a.stride); w.ok(); w.next(kThreads / 8)) {
+      if (!w.sampled()) continue;
+      const T* row = v + w.c * a.length + t0;
+      T x[kV];
+      if (VEC) {
+        *reinterpret_cast<typename Vec4<T>::type*>(x) =
+            __ldcs(reinterpret_cast<const typename Vec4<T>::type*>(row));
+      } else {
+        x[0] = row[0];
+      }
+#pragma unroll
+      for (int e = 0; e < kV; ++e) {
+        int bin;
+        if (sizeof(T) == 4)
+          bin = bin_f32(static_cast<float>(x[e]), P[e], FIXED);
+        else
+          bin = bin_index_exact(static_cast<double>(x[e]), P[e].lo, P[e].width, k);
+        if (SMEM)
+          atomicAdd(thist + (g * kV + e) * k + bin, 1u);
+        else
+          atomicAdd(counts + (t0 + e) * k + bin, 1u);
+      }
+    }
+  }
+  if (!SMEM) return;
+  __syncthreads();
+  for (int i = threadIdx.x; i < kTile * k; i += kThreads) {
+    const uint64_t t = tb + i / k;
+    if (t < a.length && thist[i]) atomicAdd(counts + t * k + (i % k), thist[i]);
+  }
+}
+
+// estimate_entropy per position (entropy.hpp:149-164): warp w of the block -> position
+// blockIdx.x * 8 + w; masses = count * (1/n), terms subtracted in bin order.
+__global__ void __launch_bounds__(kThreads) token_entropy_kernel(const unsigned int* counts,
+                                                                 uint64_t length, int k,
+                                                                 uint64_t n_per_pos, double eps,
+                                                                 double* raw_t) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * (kThreads / 32) + warp;
+  if (t >= length) return;
+  const double inv_n = __ddiv_rn(1.0, static_cast<double>(n_per_pos));
+  const unsigned int* hw = counts + t * k;
+  double raw = 0.0;
+  for (int base = 0; base < k; base += 32) {
+    const int b = base + lane;
+    const unsigned int cnt = b < k ? hw[b] : 0u;
+    double term = 0.0;
+    if (cnt) {
+      const double pm = __dmul_rn(static_cast<double>(cnt), inv_n);
+      term = __dmul_rn(pm, log(__dadd_rn(pm, eps)));
+    }
+    const int m = min(32, k - base);
+    for (int i = 0; i < m; ++i) {
+      const double ti = __shfl_sync(0xffffffffu, term, i);
+      const unsigned ci = __shfl_sync(0xffffffffu, cnt, i);
+      if (ci) raw = __dsub_rn(raw, ti);
+    }
+  }
+  if (lane == 0) raw_t[t] = raw;
+}
+
+// raw_nats = (sum_t raw_t in position order) / L; normalized = raw_nats / log K.  The sum
+// must be the reference's left-to-right fp64 chain, so one thread adds; the block stages
+// raw_t through shared memory so those adds wait on shared-memory loads, not DRAM.
+constexpr int kFinThreads = 1024;
+constexpr int kFinChunk = 4096;  // doubles per staged chunk (32 KB)
+
+__global__ void __launch_bounds__(kFinThreads) token_finalize_kernel(
+    const double* __restrict__ raw_t, uint64_t length, uint64_t samples_per_pos, int k,
+    const double* flag, double* out) {
+  __shared__ double buf[kFinChunk];
+  double sum = 0.0;
+  for (uint64_t base = 0; base < length; base += kFinChunk) {
+    const int m = static_cast<int>(umin64(kFinChunk, length - base));
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += kFinThreads) buf[i] = raw_t[base + i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int i = 0;
+      for (; i + 8 <= m; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = buf[i + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sum = __dadd_rn(sum, v[j]);
+      }
+      for (; i < m; ++i) sum = __dadd_rn(sum, buf[i]);
+    }
+  }
+  if (threadIdx.x != 0) return;
+  const double raw = __ddiv_rn(sum, static_cast<double>(length));
+  out[0] = raw;
+  out[1] = __ddiv_rn(raw, log(static_cast<double>(k)));
+  out[2] = static_cast<double>(samples_per_pos * length);
+  out[3] = flag ? *flag : 0.0;
+}
+
+__global__ void token_range_init_kernel(double* trange, uint64_t length) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < 2 * length;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    trange[i] = -INFINITY;
 }
 
 __global__ void entropy_masses_kernel(const double* masses, int k, double eps, double* out) {
@@ -1017,10 +1295,128 @@ cudaError_t launch_decide(const uint64_t* d_counts, const double* d_range,
   return cudaGetLastError();
 }
 
+cudaError_t launch_decide_token(const double* d_token, const cl_hist_spec& spec,
+                                const cl_rule_spec& rule, uint64_t seq_len, cl_decision* d_out,
+                                cudaStream_t s) {
+  DecideArgs a{};
+  a.k = spec.bin_count;
+  a.epsilon = spec.epsilon;
+  a.range_mode = spec.range_mode;
+  a.rule = rule;
+  a.seq_len = seq_len;
+  a.features_mode = 2;
+  a.token = d_token;
+  decide_kernel<<<1, kThreads, 0, s>>>(a, d_out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_entropy_from_masses(const double* d_masses, int k, double eps, double* d_out,
                                        cudaStream_t s) {
   entropy_masses_kernel<<<1, kThreads, 0, s>>>(d_masses, k, eps, d_out);
   return cudaGetLastError();
 }
+
+namespace {
+template <typename T>
+bool tok_vec_ok(const T* v, uint64_t length) {
+  return length % TokVec<T>::kV == 0 && (reinterpret_cast<uintptr_t>(v) & 15u) == 0;
+}
+
+template <typename T>
+dim3 tok_grid(uint64_t channels, uint64_t length, bool vec, int num_sms) {
+  const uint64_t tile = vec ? 8 * TokVec<T>::kV : 8;
+  const uint64_t tiles = (length + tile - 1) / tile;
+  // channel shares so the grid covers ~4 blocks per SM, each share >= 64 channels
+  uint64_t splits = (static_cast<uint64_t>(num_sms) * 4 + tiles - 1) / tiles;
+  const uint64_t max_splits = (channels + 63) / 64;
+  if (splits > max_splits) splits = max_splits;
+  if (splits < 1) splits = 1;
+  if (splits > 65535) splits = 65535;
+  return dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(splits));
+}
+}  // namespace
+
+cudaError_t launch_token_range_init(double* d_trange, double* d_flag, uint64_t length,
+                                    cudaStream_t s) {
+  token_range_init_kernel<<<64, kThreads, 0, s>>>(d_trange, length);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cudaMemsetAsync(d_flag, 0, sizeof(double), s);
+}
+
+template <typename T>
+cudaError_t launch_token_minmax(const T* v, uint64_t channels, uint64_t length, uint64_t offset,
+                                uint64_t stride, double* d_trange, double* d_flag, int num_sms,
+                                cudaStream_t s) {
+  const bool vec = tok_vec_ok(v, length);
+  const TokArgs a{channels, length, offset, stride, 0, vec ? 1 : 0};
+  const dim3 grid = tok_grid<T>(channels, length, vec, num_sms);
+  if (vec)
+    token_minmax_kernel<T, 1><<<grid, kThreads, 0, s>>>(v, a, d_trange, d_flag);
+  else
+    token_minmax_kernel<T, 0><<<grid, kThreads, 0, s>>>(v, a, d_trange, d_flag);
+  return cudaGetLastError();
+}
+
+template <typename T, int VEC, bool FIXED>
+cudaError_t launch_token_hist_v(const T* v, const TokArgs& a, const double* d_trange,
+                                const cl_hist_spec& spec, unsigned int* d_counts, dim3 grid,
+                                cudaStream_t s) {
+  constexpr int kTile = 8 * (VEC ? TokVec<T>::kV : 1);
+  const size_t smem = static_cast<size_t>(kTile) * a.k * sizeof(unsigned int);
+  if (smem <= kTokMaxSmemHist) {
+    auto kern = token_hist_kernel<T, VEC, FIXED, true>;
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, kThreads, smem, s>>>(v, a, d_trange, spec.fixed_lo, spec.fixed_hi, d_counts);
+  } else {
+    token_hist_kernel<T, VEC, FIXED, false><<<grid, kThreads, 0, s>>>(
+        v, a, d_trange, spec.fixed_lo, spec.fixed_hi, d_counts);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_token_hist(const T* v, uint64_t channels, uint64_t length, uint64_t offset,
+                              const cl_hist_spec& spec, const double* d_trange,
+                              unsigned int* d_counts, int num_sms, cudaStream_t s) {
+  const bool vec = tok_vec_ok(v, length);
+  const TokArgs a{channels, length, offset, spec.sample_stride, spec.bin_count, vec ? 1 : 0};
+  const dim3 grid = tok_grid<T>(channels, length, vec, num_sms);
+  const bool fixed = spec.range_mode == CL_RANGE_FIXED;
+  if (vec)
+    return fixed ? launch_token_hist_v<T, 1, true>(v, a, d_trange, spec, d_counts, grid, s)
+                 : launch_token_hist_v<T, 1, false>(v, a, d_trange, spec, d_counts, grid, s);
+  return fixed ? launch_token_hist_v<T, 0, true>(v, a, d_trange, spec, d_counts, grid, s)
+               : launch_token_hist_v<T, 0, false>(v, a, d_trange, spec, d_counts, grid, s);
+}
+
+cudaError_t launch_token_entropy(const unsigned int* d_counts, uint64_t length,
+                                 uint64_t n_per_pos, const cl_hist_spec& spec,
+                                 const double* d_flag, double* d_raw_t, double* d_out,
+                                 cudaStream_t s) {
+  const uint64_t blocks = (length + kThreads / 32 - 1) / (kThreads / 32);
+  token_entropy_kernel<<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(
+      d_counts, length, spec.bin_count, n_per_pos, spec.epsilon, d_raw_t);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  token_finalize_kernel<<<1, kFinThreads, 0, s>>>(d_raw_t, length, n_per_pos, spec.bin_count,
+                                                  d_flag, d_out);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_token_minmax<float>(const float*, uint64_t, uint64_t, uint64_t,
+                                                uint64_t, double*, double*, int, cudaStream_t);
+template cudaError_t launch_token_minmax<double>(const double*, uint64_t, uint64_t, uint64_t,
+                                                 uint64_t, double*, double*, int, cudaStream_t);
+template cudaError_t launch_token_hist<float>(const float*, uint64_t, uint64_t, uint64_t,
+                                              const cl_hist_spec&, const double*, unsigned int*,
+                                              int, cudaStream_t);
+template cudaError_t launch_token_hist<double>(const double*, uint64_t, uint64_t, uint64_t,
+                                               const cl_hist_spec&, const double*,
+                                               unsigned int*, int, cudaStream_t);
 
 }  // namespace cl

@@ -182,6 +182,10 @@ class Prefill:
         self.range = torch.zeros(4, dtype=torch.float64, device=self.device)
         self.decision_buf = torch.zeros(C.sizeof(_lib.cl_decision), dtype=torch.uint8,
                                         device=self.device)
+        # TokenHistogram (or Guarded{inner TokenHistogram}): per-position entropy instead
+        kind = self.rule.inner_kind if self.rule.kind == _lib.CL_POL_GUARDED else self.rule.kind
+        self.token = kind == _lib.CL_POL_TOKEN_HIST
+        self.token_buf = torch.zeros(4, dtype=torch.float64, device=self.device)
 
     # -- stages (exposed for the sharded path and for per-stage timing) --
     def stage_minmax(self, u_flat: torch.Tensor, global_offset: int = 0, init: bool = True):
@@ -206,6 +210,17 @@ class Prefill:
         self.ctx.call("cl_histogram_f32", u_flat.data_ptr(), u_flat.numel(), int(global_offset),
                       C.byref(self.cspec), self.range.data_ptr(), self.counts.data_ptr(), s)
 
+    def stage_token(self, u: torch.Tensor):
+        """token_entropy over u viewed as (channels = B*D, length = L)."""
+        L = u.shape[-1]
+        self.ctx.call("cl_token_entropy_f32", u.data_ptr(), u.numel() // L, L,
+                      C.byref(self.cspec), self.token_buf.data_ptr(), _stream_ptr(self.device))
+
+    def stage_decide_token(self, seq_len: int):
+        self.ctx.call("cl_decide_token", self.token_buf.data_ptr(), C.byref(self.cspec),
+                      C.byref(self.rule), int(seq_len), self.decision_buf.data_ptr(),
+                      _stream_ptr(self.device))
+
     def stage_decide(self, n_samples_total: int, seq_len: int):
         self.ctx.call("cl_decide", self.counts.data_ptr(), self.range.data_ptr(),
                       C.byref(self.cspec), int(n_samples_total), C.byref(self.rule),
@@ -225,10 +240,14 @@ class Prefill:
                  out=None, return_last_state=False, h0=None) -> PrefillResult:
         if u.numel() == 0:
             raise InvalidInput("no samples")
-        uf = u.reshape(-1)
-        self.stage_minmax(uf)
-        self.stage_histogram(uf)
-        self.stage_decide(self.n_samples(uf.numel()), u.shape[-1])
+        if self.token:
+            self.stage_token(u)
+            self.stage_decide_token(u.shape[-1])
+        else:
+            uf = u.reshape(-1)
+            self.stage_minmax(uf)
+            self.stage_histogram(uf)
+            self.stage_decide(self.n_samples(uf.numel()), u.shape[-1])
         res = self.stage_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, out,
                               return_last_state, h0)
         if return_last_state:

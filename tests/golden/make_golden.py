@@ -47,6 +47,15 @@ HIST_CASES = [
     ("normal_s3", O.DIST_NORMAL, 5, 100003, 128, 3, {}),
 ]
 
+TOKEN_CASES = [
+    # name, dist, seed, channels, length, K, stride, fixed, kwargs
+    ("tok_normal", O.DIST_NORMAL, 8, 96, 50, 256, 1, None, {}),
+    ("tok_normal_s3_k64", O.DIST_NORMAL, 9, 200, 33, 64, 3, None, {}),
+    ("tok_uniform_fixed", O.DIST_UNIFORM, 10, 64, 17, 16, 1, (-0.5, 1.5), {}),
+    ("tok_laplace", O.DIST_LAPLACE, 11, 1024, 24, 256, 1, None, {}),
+    ("tok_sparse_s8", O.DIST_SPARSE, 12, 777, 40, 128, 8, None, {"nonzero_fraction": 0.1}),
+]
+
 SCAN_CASES = [  # seed, D, N, L, time_varying
     (2026, 64, 16, 4096, True),
     (42, 16, 8, 1000, True),
@@ -89,6 +98,22 @@ def hist_fixtures(R: O.Reference, P: O.Port):
                           normalized_f32=norm32, chunks_f32=chunks32,
                           values_fnv=P.fnv1a64(v), values_f32_fnv=P.fnv1a64(v32))
     return out, meta
+
+
+def token_fixtures(R: O.Reference, P: O.Port):
+    """token_entropy (entropy.hpp:180-210) of generated (channels, length) tensors, fp64
+    and fp32-rounded values; the tests regenerate the values with the same generator."""
+    meta = {}
+    for name, dist, seed, ch, L, k, stride, fixed, kw in TOKEN_CASES:
+        v = R.generate(dist, ch * L, seed, **kw).reshape(ch, L)
+        v32 = v.astype(np.float32).astype(np.float64)
+        raw, norm, n = R.token_entropy(v, k, 1e-8, stride, fixed)
+        raw32, norm32, n32 = R.token_entropy(v32, k, 1e-8, stride, fixed)
+        meta[name] = dict(dist=dist, seed=seed, channels=ch, length=L, k=k, stride=stride,
+                          fixed=list(fixed) if fixed else None, kwargs=kw, raw_nats=raw,
+                          normalized=norm, sample_count=n, raw_nats_f32=raw32,
+                          normalized_f32=norm32, values_fnv=P.fnv1a64(v.reshape(-1)))
+    return meta
 
 
 def scan_fixtures(R: O.Reference, P: O.Port):
@@ -171,6 +196,7 @@ def main():
     a, m = hist_fixtures(R, P)
     arrays.update(a)
     meta["hist"] = m
+    meta["token"] = token_fixtures(R, P)
     a, m = scan_fixtures(R, P)
     arrays.update(a)
     meta["scan"] = m

@@ -140,3 +140,32 @@ def test_oracle_error_strings(port):
     c, lo, hi, n = port.histogram(np.full(1000, 3.0), 256)
     raw, _ = port.entropy(c.astype(np.float64) / n)
     assert raw == -9.9999998892252911e-09
+
+
+def test_token_entropy_port_golden(port, golden):
+    """The port's token_entropy (entropy.hpp:180-210) equals the reference build's on the
+    golden token cases, bit for bit (same glibc log, -ffp-contract=off)."""
+    meta, _ = golden
+    for name, m in meta["token"].items():
+        v = port.generate(m["dist"], m["channels"] * m["length"], m["seed"], **m["kwargs"])
+        v = v.reshape(m["channels"], m["length"])
+        assert port.fnv1a64(v.reshape(-1)) == m["values_fnv"], name
+        fixed = tuple(m["fixed"]) if m["fixed"] else None
+        raw, norm, n = port.token_entropy(v, m["k"], 1e-8, m["stride"], fixed)
+        assert (raw, norm, n) == (m["raw_nats"], m["normalized"], m["sample_count"]), name
+        if O.reference_available():
+            assert O.Reference().token_entropy(v, m["k"], 1e-8, m["stride"], fixed) == (raw, norm, n)
+
+
+def test_ema_host_mirror():
+    """test_entropy.cpp:144-172 against the Python mirror (a host scalar recurrence)."""
+    import paper_2604_10597_b200 as cl
+    nx = cl.update_ema(cl.EmaState(4.0, 0.85, 3), 5.0)
+    assert abs(nx.current - 4.15) <= 1e-12 and nx.update_count == 4
+    assert cl.update_ema(cl.EmaState(123.0, 0.0), 7.5).current == 7.5
+    with pytest.raises(cl.InvalidInput, match=r"ema decay must lie in \[0,1\)"):
+        cl.update_ema(cl.EmaState(0.0, 1.0), 1.0)
+    s = cl.EmaState(0.0, 0.85)
+    for _ in range(7):
+        s = cl.update_ema(s, 5.0)
+    assert abs(s.current - 5.0 * (1.0 - 0.85 ** 7)) <= 1e-12
