@@ -14,6 +14,13 @@ Every rank then runs the identical device decision on identical inputs, so every
 rank derives the identical chunk with no broadcast.  Stride sampling uses each
 row's GLOBAL flat index, so sharded counts equal single-GPU counts bit for bit.
 
+The TokenHistogram policy (token_entropy, entropy.hpp:180-210: one histogram per
+position over all channels) has the same two-collective shape with per-position
+buffers: MAX-allreduce of the [2L+1] per-position range {-lo[L], hi[L], nonfinite},
+then SUM-allreduce of the [L][K] counts (uint32, carried as int32: counts per
+position are at most the total channel count, < 2^31).  Channels are sampled by
+GLOBAL row index.
+
 The protocol is written against a small stage interface so that the same host
 logic runs with the B200 kernels (`DeviceStages`) and, in the CPU tests, with a
 test-only implementation over gloo.
@@ -120,8 +127,40 @@ def sharded_entropy_decision(stages: Stages, u_local_flat: torch.Tensor, plan: S
     stages.decide(n_samples(plan.global_numel, stride), plan.seq_len)
 
 
+class TokenStages(Protocol):
+    """Per-rank token_entropy stage kernels (device path: DeviceStages)."""
+    trange: torch.Tensor   # float64[2L + 1]
+    tcounts: torch.Tensor  # int32[L * K]
+
+    def token_range_init(self) -> None: ...
+    def token_minmax(self, flat: torch.Tensor, channels: int, channel_offset: int) -> None: ...
+    def token_counts_zero(self) -> None: ...
+    def token_histogram(self, flat: torch.Tensor, channels: int, channel_offset: int) -> None: ...
+    def token_decide(self, samples_per_position: int, seq_len: int) -> None: ...
+
+
+def sharded_token_decision(stages: TokenStages, u_local_flat: torch.Tensor, plan: ShardPlan,
+                           stride: int, group=None) -> None:
+    """token_entropy over the ranks of `group` (channels = rows of (batch*d_inner), sampled
+    by GLOBAL row index) + the identical device decision on every rank."""
+    L = plan.seq_len
+    stages.token_range_init()
+    for s in plan.segments:
+        stages.token_minmax(u_local_flat[s.local_offset:s.local_offset + s.numel], s.numel // L,
+                            s.global_offset // L)
+    if plan.world > 1:
+        dist.all_reduce(stages.trange, op=dist.ReduceOp.MAX, group=group)
+    stages.token_counts_zero()
+    for s in plan.segments:
+        stages.token_histogram(u_local_flat[s.local_offset:s.local_offset + s.numel],
+                               s.numel // L, s.global_offset // L)
+    if plan.world > 1:
+        dist.all_reduce(stages.tcounts, op=dist.ReduceOp.SUM, group=group)
+    stages.token_decide(n_samples(plan.batch * plan.dim, stride), L)
+
+
 class DeviceStages:
-    """The B200 kernels behind the Stages interface (wraps mamba1.Prefill)."""
+    """The B200 kernels behind the Stages / TokenStages interfaces (wraps mamba1.Prefill)."""
 
     def __init__(self, prefill):
         self.pf = prefill
@@ -147,6 +186,41 @@ class DeviceStages:
     def decide(self, n_samples_total, seq_len):
         self.pf.stage_decide(n_samples_total, seq_len)
 
+    # -- token_entropy stages (buffers sized on first use for this seq_len) --
+    def _token_buffers(self, L):
+        k = int(self.pf.spec.bin_count)
+        if getattr(self, "trange", None) is None or self.trange.numel() != 2 * L + 1:
+            self.trange = torch.empty(2 * L + 1, dtype=torch.float64, device=self.pf.device)
+            self.tcounts = torch.zeros(L * k, dtype=torch.int32, device=self.pf.device)
+            self._L = L
+
+    def _s(self):
+        return torch.cuda.current_stream(self.pf.device).cuda_stream
+
+    def token_range_init(self):
+        self.pf.ctx.call("cl_token_range_init", self.trange.data_ptr(), self._L, self._s())
+
+    def token_minmax(self, flat, channels, channel_offset):
+        self.pf.ctx.call("cl_token_minmax_f32", flat.data_ptr(), int(channels), self._L,
+                         int(channel_offset), int(self.pf.spec.sample_stride),
+                         self.trange.data_ptr(), self._s())
+
+    def token_counts_zero(self):
+        self.tcounts.zero_()
+
+    def token_histogram(self, flat, channels, channel_offset):
+        import ctypes as C
+        self.pf.ctx.call("cl_token_histogram_f32", flat.data_ptr(), int(channels), self._L,
+                         int(channel_offset), C.byref(self.pf.cspec), self.trange.data_ptr(),
+                         self.tcounts.data_ptr(), self._s())
+
+    def token_decide(self, samples_per_position, seq_len):
+        import ctypes as C
+        self.pf.ctx.call("cl_token_entropy_counts", self.tcounts.data_ptr(),
+                         self.trange.data_ptr(), self._L, int(samples_per_position),
+                         C.byref(self.pf.cspec), self.pf.token_buf.data_ptr(), self._s())
+        self.pf.stage_decide_token(seq_len)
+
 
 class ShardedPrefill:
     """One layer's prefill over all ranks: global entropy -> identical decision ->
@@ -165,7 +239,12 @@ class ShardedPrefill:
                  out=None, return_last_state=False):
         if tuple(u.shape) != (self.plan.local_batch, self.plan.local_dim, self.plan.seq_len):
             raise ValueError("u does not match the shard plan")
-        sharded_entropy_decision(self.stages, u.reshape(-1), self.plan,
-                                 int(self.pf.spec.sample_stride), self.group)
+        if self.pf.token:
+            self.stages._token_buffers(self.plan.seq_len)
+            sharded_token_decision(self.stages, u.reshape(-1), self.plan,
+                                   int(self.pf.spec.sample_stride), self.group)
+        else:
+            sharded_entropy_decision(self.stages, u.reshape(-1), self.plan,
+                                     int(self.pf.spec.sample_stride), self.group)
         return self.pf.stage_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, out,
                                   return_last_state)

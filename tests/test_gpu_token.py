@@ -171,3 +171,25 @@ def test_host_schedule_token_feature(cuda):
     d = cl.schedule(policy, cl.ScheduleFeatures(token_entropy=cl.EntropyEstimate(5.0)), bounds,
                     cal)
     assert d.chunk == 2048 and d.source_policy == "token_histogram"
+
+
+def test_sharded_stages_world1_equal_one_call(cuda):
+    """The staged token path behind ShardedPrefill (the multi-GPU protocol's device
+    stages, collectives skipped at world 1) equals the one-call path exactly."""
+    from paper_2604_10597_b200.sharded import ShardedPrefill, plan_rows
+    x = mamba_inputs(8, 2, 160, 16, 96)
+    d = {k: torch.from_numpy(np.ascontiguousarray(a)).to(cuda) for k, a in x.items()}
+    policy = cl.SchedulerPolicy(cl.TokenHistogramPolicy(), ROUTED)
+    for stride in (1, 3):
+        spec = cl.HistogramSpec(sample_stride=stride)
+        pf1 = Prefill(spec, policy, cl.ChunkBounds(128, 2048), device=cuda)
+        sp = ShardedPrefill(pf1, plan_rows(2, 160, 96, 0, 1))
+        out1 = sp(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"])
+        r1 = pf1.decision()
+        pf2 = Prefill(spec, policy, cl.ChunkBounds(128, 2048), device=cuda)
+        res2 = pf2(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"])
+        r2 = pf2.decision()
+        assert r1.entropy.raw_nats == r2.entropy.raw_nats
+        assert r1.entropy.sample_count == r2.entropy.sample_count
+        assert r1.decision.chunk == r2.decision.chunk
+        assert torch.equal(out1, res2.out)

@@ -16,7 +16,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2604_10597_b200.sharded import n_samples, plan_rows, sharded_entropy_decision
+from paper_2604_10597_b200.sharded import (n_samples, plan_rows, sharded_entropy_decision,
+                                           sharded_token_decision)
 
 
 class OracleStages:
@@ -64,6 +65,77 @@ class OracleStages:
         raw, _ = self.port.entropy(masses)
         self.raw = raw
         self.chunk, _ = self.port.select_chunk(raw, 32, 512, math.log(self.k))
+
+
+class OracleTokenStages:
+    """Test-only token_entropy stages over the CPU oracle (per-position histograms)."""
+
+    def __init__(self, port, k, stride, L):
+        self.port, self.k, self.stride, self.L = port, k, stride, L
+        self.trange = torch.zeros(2 * L + 1, dtype=torch.float64)
+        self.tcounts = torch.zeros(L * k, dtype=torch.int32)
+        self.raw = None
+
+    def _rows(self, flat, channels, off):
+        v = flat.numpy().reshape(channels, self.L).astype(np.float64)
+        keep = (np.arange(channels) + off) % self.stride == 0
+        return v, v[keep]
+
+    def token_range_init(self):
+        self.trange[:2 * self.L] = -math.inf
+        self.trange[2 * self.L] = 0.0
+
+    def token_minmax(self, flat, channels, off):
+        v, samp = self._rows(flat, channels, off)
+        t = self.trange.numpy()
+        if not np.isfinite(v).all():
+            t[2 * self.L] = 1.0
+        if samp.shape[0]:
+            t[:self.L] = np.maximum(t[:self.L], -samp.min(axis=0))
+            t[self.L:2 * self.L] = np.maximum(t[self.L:2 * self.L], samp.max(axis=0))
+
+    def token_counts_zero(self):
+        self.tcounts.zero_()
+
+    def token_histogram(self, flat, channels, off):
+        _, samp = self._rows(flat, channels, off)
+        if not samp.shape[0]:
+            return
+        t = self.trange.numpy()
+        c = self.tcounts.numpy().reshape(self.L, self.k)
+        for p in range(self.L):
+            lo, hi = -t[p], t[self.L + p]
+            if hi > lo:
+                h, *_ = self.port.histogram(np.ascontiguousarray(samp[:, p]), self.k, 1e-8, 1,
+                                            fixed=(lo, hi))
+            else:
+                h = np.zeros(self.k, dtype=np.uint64)
+                h[0] = samp.shape[0]
+            c[p] += h.astype(np.int32)
+
+    def token_decide(self, samples_per_position, seq_len):
+        c = self.tcounts.numpy().reshape(self.L, self.k)
+        raw_sum = 0.0
+        for p in range(self.L):
+            raw, _ = self.port.entropy(c[p].astype(np.float64) * (1.0 / samples_per_position))
+            raw_sum += raw
+        self.raw = raw_sum / self.L
+
+
+def _token_worker(rank, world, port_no, batch, dim, L, stride, k, seed, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    port = O.Port()
+    rng = np.random.default_rng(seed)
+    u = rng.standard_normal((batch, dim, L)).astype(np.float32)
+    plan = plan_rows(batch, dim, L, rank, world)
+    local = u[plan.b0:plan.b1, plan.d0:plan.d1, :].copy()
+    st = OracleTokenStages(port, k, stride, L)
+    sharded_token_decision(st, torch.from_numpy(local).reshape(-1), plan, stride)
+    out_q.put((rank, st.tcounts.numpy().copy(), st.raw))
+    dist.destroy_process_group()
 
 
 def _worker(rank, world, port_no, batch, dim, L, stride, k, seed, out_q):
@@ -128,3 +200,30 @@ def test_plan_rows_covers_every_row_once():
                 seen[rows] += 1
                 assert s.numel % ((s.d1 - s.d0) * L) == 0
         assert (seen == 1).all()
+
+
+@pytest.mark.parametrize("batch,dim,L,stride", [(2, 12, 9, 1), (1, 16, 7, 3), (3, 8, 5, 4)])
+def test_two_rank_token_entropy_equals_single(port, batch, dim, L, stride):
+    """token_entropy sharded over 2 ranks (rows of batch*d_inner) equals the oracle's
+    token_entropy of the whole (batch*d_inner, L) tensor bit for bit."""
+    world, k, seed = 2, 64, 17
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pn = _free_port()
+    procs = [ctx.Process(target=_token_worker,
+                         args=(r, world, pn, batch, dim, L, stride, k, seed, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(seed)
+    u = rng.standard_normal((batch, dim, L)).astype(np.float32)
+    raw, _, n = port.token_entropy(u.reshape(batch * dim, L).astype(np.float64), k, 1e-8, stride)
+    assert n == L * ((batch * dim + stride - 1) // stride)
+    counts0 = res[0][1]
+    for rank, counts, r in res:
+        assert (counts == counts0).all(), rank
+        assert r == raw, (rank, r, raw)
