@@ -225,6 +225,29 @@ typedef struct {
 int cl_scan_f64(cl_ctx* ctx, const cl_scan_params_f64* d_params, const double* d_h0,
                 uint64_t chunk, double* d_y, double* d_h, void* stream);
 
+/* Decode step: one token per (b, d) row through the Mamba-1
+ * recurrence, state updated in place -- mamba_ssm selective_state_update(state, x, dt,
+ * A, B, C, D, z, dt_bias, dt_softplus).  state (batch, dim, d_state); x, dt, z, out
+ * (batch, dim); A (dim, d_state); B, C (batch, d_state); D, dt_bias (dim) or NULL.
+ * Same elementwise math and (d_state 16) the same C.h order as cl_selective_scan_f32,
+ * so a prefill over L tokens followed by k decode steps equals a prefill over L + k
+ * tokens bit for bit. */
+typedef struct {
+  float* state;
+  const float* x;
+  const float* dt;
+  const float* A;
+  const float* B;
+  const float* C;
+  const float* D;       /* may be NULL */
+  const float* z;       /* may be NULL */
+  const float* dt_bias; /* may be NULL */
+  float* out;
+  uint64_t batch, dim, d_state;
+  int dt_softplus;
+} cl_state_update_args;
+int cl_selective_state_update_f32(cl_ctx* ctx, const cl_state_update_args* args, void* stream);
+
 /* token_entropy (entropy.hpp:180-210) of a (channels, length) tensor, length contiguous
  * (Mamba u (B, D, L) is channels = B*D): one histogram per position t over its channel
  * slice (slice index c sampled iff c % stride == 0; the slice's Dynamic range or the

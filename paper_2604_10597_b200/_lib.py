@@ -69,6 +69,13 @@ class cl_mamba1_args(C.Structure):
                 ("seq_len", C.c_uint64), ("d_state", C.c_uint64), ("delta_softplus", C.c_int)]
 
 
+class cl_state_update_args(C.Structure):
+    _fields_ = [("state", C.c_void_p), ("x", C.c_void_p), ("dt", C.c_void_p), ("A", C.c_void_p),
+                ("B", C.c_void_p), ("C", C.c_void_p), ("D", C.c_void_p), ("z", C.c_void_p),
+                ("dt_bias", C.c_void_p), ("out", C.c_void_p), ("batch", C.c_uint64),
+                ("dim", C.c_uint64), ("d_state", C.c_uint64), ("dt_softplus", C.c_int)]
+
+
 class cl_scan_params_f64(C.Structure):
     _fields_ = [("channels", C.c_uint64), ("state_dim", C.c_uint64), ("seq_len", C.c_uint64),
                 ("a", C.c_void_p), ("b", C.c_void_p), ("c", C.c_void_p), ("d", C.c_void_p),
@@ -109,6 +116,7 @@ SIGNATURES = {
                                   _P, _P]),
     "cl_selective_scan_f32": (C.c_int, [_P, C.POINTER(cl_mamba1_args), _P, C.c_int, C.c_int,
                                         _P]),
+    "cl_selective_state_update_f32": (C.c_int, [_P, C.POINTER(cl_state_update_args), _P]),
     "cl_prefill_f32": (C.c_int, [_P, C.POINTER(cl_mamba1_args), C.POINTER(cl_hist_spec),
                                  C.POINTER(cl_rule_spec), _P, _P, _P, _P]),
     "cl_decision_check": (C.c_int, [_P, _P, C.POINTER(cl_decision), _P]),

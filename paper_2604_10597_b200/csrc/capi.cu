@@ -491,6 +491,17 @@ int cl_selective_scan_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_deci
   return scan_mamba1(ctx, a, d_decision, fixed_chunk, variant, static_cast<cudaStream_t>(stream));
 }
 
+int cl_selective_state_update_f32(cl_ctx* ctx, const cl_state_update_args* args, void* stream) {
+  if (!ctx || !args) return fail(ctx, CL_E_INVALID, "null argument");
+  const cl_state_update_args& a = *args;
+  if (a.batch == 0 || a.dim == 0 || a.d_state == 0) return fail(ctx, CL_E_INVALID, "shape mismatch");
+  if (a.d_state > 64) return fail(ctx, CL_E_INVALID, "d_state must lie in [1, 64]");
+  if (!a.state || !a.x || !a.dt || !a.A || !a.B || !a.C || !a.out)
+    return fail(ctx, CL_E_INVALID, "null argument");
+  DeviceGuard g(ctx->device);
+  return state_update_f32(ctx, a, static_cast<cudaStream_t>(stream));
+}
+
 int cl_prefill_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_hist_spec* spec,
                    const cl_rule_spec* rule, uint64_t* d_counts, double* d_range,
                    cl_decision* d_decision, void* stream) {

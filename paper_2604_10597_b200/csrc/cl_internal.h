@@ -93,5 +93,6 @@ cudaError_t launch_scan_f64(const cl_scan_params_f64& p, const double* d_h0, uin
 // scan_mamba1.cu
 int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decision,
                 int fixed_chunk, int variant, cudaStream_t s);
+int state_update_f32(cl_ctx* ctx, const cl_state_update_args& a, cudaStream_t s);
 
 }  // namespace cl

@@ -42,11 +42,62 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-__device__ __forceinline__ float softplus_f32(float x) {
-  return x <= 20.f ? log1pf(__expf(x)) : x;
+// ---- canonical elementwise math ----
+// Every Mamba-1 path (generic scan, TMA scans, decode) evaluates softplus, SiLU and, for
+// N = 16, C.h with exactly these operation sequences, so the paths agree bit for bit
+// and a prefill followed by decode steps equals a longer prefill bit for bit (the
+// paper's passive-vs-routed claim is bitwise output equality).  The
+// FFMA2 versions further down (softplus2 / silu2 / the lane-pair C.h) are these
+// functions applied per lane of a register pair.
+
+// softplus(x) = max(x,0) + log1p(exp(-|x|)): one MUFU.EX2 and a degree-9 minimax
+// polynomial for log1p on [0,1] (max rel err 2e-7; equals x to fp32 above 20).
+__device__ __forceinline__ float softplus_canon(float a) {
+  const float e = ex2_approx(-fabsf(a) * kLog2e);
+  float q = 0.005253826278033571f;
+  q = fmaf(q, e, -0.02959069552080005f);
+  q = fmaf(q, e, 0.07836660226277938f);
+  q = fmaf(q, e, -0.13675328086246433f);
+  q = fmaf(q, e, 0.19111774195698683f);
+  q = fmaf(q, e, -0.24844483411506615f);
+  q = fmaf(q, e, 0.33319289806287417f);
+  q = fmaf(q, e, -0.49999502673812024f);
+  q = fmaf(q, e, 0.9999999706625772f);
+  return fmaf(q, e, fmaxf(a, 0.f));
 }
 
-__device__ __forceinline__ float silu_f32(float z) { return __fdividef(z, 1.f + __expf(-z)); }
+// z * sigmoid(z): one MUFU.EX2, reciprocal by 3 Newton steps from the bit-trick seed.
+__device__ __forceinline__ float silu_canon(float z) {
+  const float e = ex2_approx(fmaxf(z, -80.f) * -kLog2e);
+  const float d = e + 1.f;
+  float r = __int_as_float(0x7EF311C7 - __float_as_int(d));
+  const float nd = d * -1.f;
+#pragma unroll
+  for (int it = 0; it < 3; ++it) {
+    const float en = fmaf(nd, r, 1.f);
+    r = fmaf(r, en, r);
+  }
+  return z * r;
+}
+
+// y = sum_s c[s] h[s] for N = 16 in the lane-pair kernel's order: lane half hf holds
+// states 8hf..8hf+7 and accumulates ya over (0,1),(4,5) and yb over (2,3),(6,7) with
+// FFMA2, then (ya.lo+yb.lo) + (ya.hi+yb.hi); the halves are added last.
+__device__ __forceinline__ float cdot16_canon(const float* c, const float* h) {
+  float p[2];
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+    const float* cc = c + 8 * hf;
+    const float* hh = h + 8 * hf;
+    // first term as fma(c, h, +0) like the FFMA2 chain started from 0 (sign of zero)
+    const float ya_lo = fmaf(cc[4], hh[4], fmaf(cc[0], hh[0], 0.f));
+    const float ya_hi = fmaf(cc[5], hh[5], fmaf(cc[1], hh[1], 0.f));
+    const float yb_lo = fmaf(cc[6], hh[6], fmaf(cc[2], hh[2], 0.f));
+    const float yb_hi = fmaf(cc[7], hh[7], fmaf(cc[3], hh[3], 0.f));
+    p[hf] = (ya_lo + yb_lo) + (ya_hi + yb_hi);
+  }
+  return p[0] + p[1];
+}
 
 __device__ __forceinline__ int read_chunk(const cl_decision* d, int fixed_chunk, int* status) {
   if (d) {
@@ -92,19 +143,30 @@ __global__ void __launch_bounds__(128) generic_kernel(GenericArgs a) {
   for (uint64_t t = 0; t < a.L; ++t) {
     const float u = a.u[row * a.L + t];
     float dt = a.delta[row * a.L + t] + bias;
-    if (a.softplus) dt = softplus_f32(dt);
+    if (a.softplus) dt = softplus_canon(dt);
     const float x = dt * u;
     float y = 0.f;
+    if (NS == 16) {
+      float cv[16];
 #pragma unroll
-    for (int s = 0; s < (NS > 0 ? NS : 64); ++s) {
-      if (s < N) {
-        const float dA = ex2_approx(dt * A2[s]);
+      for (int s = 0; s < 16; ++s) {
+        const float dA = ex2_approx(A2[s] * dt);
         h[s] = fmaf(dA, h[s], Bb[s * a.L + t] * x);
-        y = fmaf(Cb[s * a.L + t], h[s], y);
+        cv[s] = Cb[s * a.L + t];
+      }
+      y = cdot16_canon(cv, h);
+    } else {
+#pragma unroll
+      for (int s = 0; s < (NS > 0 ? NS : 64); ++s) {
+        if (s < N) {
+          const float dA = ex2_approx(A2[s] * dt);
+          h[s] = fmaf(dA, h[s], Bb[s * a.L + t] * x);
+          y = fmaf(Cb[s * a.L + t], h[s], y);
+        }
       }
     }
     y = fmaf(Dc, u, y);
-    if (a.z) y *= silu_f32(a.z[row * a.L + t]);
+    if (a.z) y *= silu_canon(a.z[row * a.L + t]);
     a.out[row * a.L + t] = y;
   }
   if (a.h_last) {
@@ -112,6 +174,59 @@ __global__ void __launch_bounds__(128) generic_kernel(GenericArgs a) {
     for (int s = 0; s < (NS > 0 ? NS : 64); ++s)
       if (s < N) a.h_last[row * N + s] = h[s];
   }
+}
+
+// ---------------------------------------------------------------------------
+// Decode step: one token through the recurrence, state updated in
+// place -- mamba_ssm's selective_state_update(state, x, dt, A, B, C, D, z, dt_bias,
+// dt_softplus) semantics, with the canonical math above so that prefill(L) followed by
+// decode steps reproduces prefill(L + k) bit for bit.  One thread per (b, d) row.
+// ---------------------------------------------------------------------------
+struct DecodeArgs {
+  float* state;  // (batch, dim, N), in/out
+  const float *x, *dt, *A, *B, *C, *D, *z, *dt_bias;
+  float* out;  // (batch, dim)
+  uint64_t batch, dim;
+  int N;
+  int softplus;
+};
+
+template <int NS>
+__global__ void __launch_bounds__(128) decode_kernel(DecodeArgs a) {
+  const uint64_t row = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= a.batch * a.dim) return;
+  const int N = NS > 0 ? NS : a.N;
+  const uint64_t b = row / a.dim, c = row - b * a.dim;
+  float dt = a.dt[row] + (a.dt_bias ? a.dt_bias[c] : 0.f);
+  if (a.softplus) dt = softplus_canon(dt);
+  const float u = a.x[row];
+  const float xx = dt * u;
+  float* st = a.state + row * N;
+  const float* Bb = a.B + b * N;
+  const float* Cb = a.C + b * N;
+  float y = 0.f;
+  if (NS == 16) {
+    float h[16], cv[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const float dA = ex2_approx((a.A[c * 16 + s] * kLog2e) * dt);
+      h[s] = fmaf(dA, st[s], Bb[s] * xx);
+      cv[s] = Cb[s];
+    }
+    y = cdot16_canon(cv, h);
+#pragma unroll
+    for (int s = 0; s < 16; ++s) st[s] = h[s];
+  } else {
+    for (int s = 0; s < N; ++s) {
+      const float dA = ex2_approx((a.A[c * N + s] * kLog2e) * dt);
+      const float h = fmaf(dA, st[s], Bb[s] * xx);
+      y = fmaf(Cb[s], h, y);
+      st[s] = h;
+    }
+  }
+  y = fmaf(a.D ? a.D[c] : 0.f, u, y);
+  if (a.z) y *= silu_canon(a.z[row]);
+  a.out[row] = y;
 }
 
 // ---------------------------------------------------------------------------
@@ -1114,6 +1229,22 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
   if (e != cudaSuccess) return cuda_fail(ctx, e, "generic_kernel launch");
   ++ctx->launches;
   (void)fixed_chunk;
+  return CL_OK;
+}
+
+int state_update_f32(cl_ctx* ctx, const cl_state_update_args& a, cudaStream_t s) {
+  DecodeArgs d{a.state, a.x, a.dt, a.A, a.B, a.C, a.D, a.z, a.dt_bias, a.out,
+               a.batch, a.dim, static_cast<int>(a.d_state), a.dt_softplus};
+  const uint64_t rows = a.batch * a.dim;
+  if (rows == 0) return CL_OK;
+  const unsigned grid = static_cast<unsigned>((rows + 127) / 128);
+  if (a.d_state == 16)
+    decode_kernel<16><<<grid, 128, 0, s>>>(d);
+  else
+    decode_kernel<0><<<grid, 128, 0, s>>>(d);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "decode_kernel launch");
+  ++ctx->launches;
   return CL_OK;
 }
 

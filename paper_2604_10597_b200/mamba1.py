@@ -96,6 +96,36 @@ def selective_scan_fn(u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_
     return (out, h_last) if return_last_state else out
 
 
+def selective_state_update(state, x, dt, A, B, C, D=None, z=None, dt_bias=None,
+                           dt_softplus=False, out: Optional[torch.Tensor] = None):
+    """mamba_ssm.selective_state_update semantics (decode: one token), fp32, state updated
+    in place.  state (batch, dim, N); x, dt, z (batch, dim); A (dim, N); B, C (batch, N).
+    Bitwise consistent with selective_scan_fn: prefill(L) + k steps == prefill(L + k)."""
+    dev = state.device
+    batch, dim, N = state.shape
+    for name, t in (("state", state), ("x", x), ("dt", dt), ("A", A), ("B", B), ("C", C),
+                    ("D", D), ("z", z), ("dt_bias", dt_bias), ("out", out)):
+        _check_f32(name, t, dev)
+    if tuple(x.shape) != (batch, dim) or tuple(dt.shape) != (batch, dim):
+        raise InvalidInput("shape mismatch")
+    if tuple(A.shape) != (dim, N) or tuple(B.shape) != (batch, N) or tuple(C.shape) != (batch, N):
+        raise InvalidInput("shape mismatch")
+    if z is not None and tuple(z.shape) != (batch, dim):
+        raise InvalidInput("shape mismatch")
+    for t in (D, dt_bias):
+        if t is not None and t.numel() != dim:
+            raise InvalidInput("shape mismatch")
+    out = torch.empty_like(x) if out is None else out
+    a = _lib.cl_state_update_args()
+    a.state, a.x, a.dt, a.A, a.B, a.C = (state.data_ptr(), x.data_ptr(), dt.data_ptr(),
+                                         A.data_ptr(), B.data_ptr(), C.data_ptr())
+    a.D, a.z, a.dt_bias, a.out = _ptr(D), _ptr(z), _ptr(dt_bias), out.data_ptr()
+    a.batch, a.dim, a.d_state, a.dt_softplus = batch, dim, N, int(bool(dt_softplus))
+    # (the parameter C shadows the ctypes module here: C_byref is module level)
+    Context.get(dev.index).call("cl_selective_state_update_f32", C_byref(a), _stream_ptr(dev))
+    return out
+
+
 def causal_conv1d_fn(x, weight, bias=None, activation: Optional[str] = "silu",
                      out: Optional[torch.Tensor] = None, range_buf: Optional[torch.Tensor] = None,
                      global_offset: int = 0, stride: int = 1):
