@@ -7,7 +7,10 @@
 //   ChunkDecision d = pf.decision();  // sync point; throws deferred device errors
 //
 // selective_scan(args, chunk, stream) is mamba_ssm's selective_scan_fn with an
-// explicit chunk (the paper's patched fwd_with_chunk_size).
+// explicit chunk (the paper's patched fwd_with_chunk_size);
+// selective_state_update(args, stream) its one-token decode step (bitwise consistent
+// with the scan); causal_conv1d(...) the conv1d + SiLU producer of u, optionally with
+// the entropy min/max pass fused into it (d_range != nullptr).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -23,6 +26,21 @@ using Mamba1Args = cl_mamba1_args;
 inline void selective_scan(const Mamba1Args& args, int chunk, cudaStream_t stream = nullptr) {
   b200::check(cl_selective_scan_f32(b200::Runtime::get().ctx(), &args, nullptr, chunk,
                                     CL_SCAN_AUTO, stream));
+}
+
+using StateUpdateArgs = cl_state_update_args;
+
+inline void selective_state_update(const StateUpdateArgs& args, cudaStream_t stream = nullptr) {
+  b200::check(cl_selective_state_update_f32(b200::Runtime::get().ctx(), &args, stream));
+}
+
+inline void causal_conv1d(const float* d_x, const float* d_weight, const float* d_bias,
+                          float* d_u, std::uint64_t batch, std::uint64_t dim,
+                          std::uint64_t seq_len, int width, bool silu,
+                          double* d_range = nullptr, std::uint64_t stride = 1,
+                          cudaStream_t stream = nullptr) {
+  b200::check(cl_conv1d_f32(b200::Runtime::get().ctx(), d_x, d_weight, d_bias, d_u, batch, dim,
+                            seq_len, width, silu ? 1 : 0, 0, stride, d_range, stream));
 }
 
 class Prefill {
@@ -95,6 +113,8 @@ class Prefill {
       kind = CL_POL_FULL_HIST;
     } else if (std::holds_alternative<SampledHistogramPolicy>(v)) {
       kind = CL_POL_SAMPLED_HIST;
+    } else if (std::holds_alternative<TokenHistogramPolicy>(v)) {
+      kind = CL_POL_TOKEN_HIST;
     } else if (const auto* l = std::get_if<LearnedTablePolicy>(&v)) {
       kind = CL_POL_LEARNED_TABLE;
       rule_.threshold_tokens = l->threshold_tokens;

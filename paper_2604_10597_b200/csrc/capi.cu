@@ -512,6 +512,17 @@ int cl_prefill_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_hist_spec* 
   if (rc) return rc;
   const uint64_t n = args->batch * args->dim * args->seq_len;
   if (n == 0) return fail(ctx, CL_E_INVALID, "no samples");
+  const int kind = rule->kind == CL_POL_GUARDED ? rule->inner_kind : rule->kind;
+  if (kind == CL_POL_TOKEN_HIST) {
+    // TokenHistogram: token_entropy over u as (batch*dim, seq_len), result staged in
+    // d_range (4 doubles, the token_entropy output layout); d_counts unused
+    if ((rc = cl_token_entropy_f32(ctx, args->u, args->batch * args->dim, args->seq_len, spec,
+                                   d_range, stream)))
+      return rc;
+    if ((rc = cl_decide_token(ctx, d_range, spec, rule, args->seq_len, d_decision, stream)))
+      return rc;
+    return cl_selective_scan_f32(ctx, args, d_decision, 0, CL_SCAN_AUTO, stream);
+  }
   if ((rc = cl_range_init(ctx, d_range, stream))) return rc;
   if ((rc = cl_minmax_f32(ctx, args->u, n, 0, spec->sample_stride, d_range, stream))) return rc;
   if ((rc = cl_counts_zero(ctx, d_counts, spec->bin_count, stream))) return rc;

@@ -329,6 +329,92 @@ static void test_prefill() {
   bool finite = true;
   for (float v : out) finite = finite && std::isfinite(v);
   CHECK(finite);
+
+  // TokenHistogram policy through the same Prefill (token_entropy on the device), the
+  // decision equals Scheduler::decide fed the host token_entropy of the same values
+  {
+    SchedulerPolicy tp;
+    tp.variant = TokenHistogramPolicy{};
+    tp.bucket_set = {128, 256, 512, 1024, 2048};
+    Prefill tpf(HistogramSpec{}, &tp, ChunkBounds{128, 2048}, CalibrationRef::log_k(256));
+    tpf.run(a);
+    EntropyEstimate te;
+    const ChunkDecision td = tpf.decision(&te);
+    ActivationTensor t;
+    t.shape = {static_cast<std::size_t>(B * D), static_cast<std::size_t>(L)};
+    t.values.assign(u.begin(), u.end());
+    const EntropyEstimate he = token_entropy(t, HistogramSpec{});
+    CHECK(std::fabs(te.raw_nats - he.raw_nats) <= 1e-12 * std::fabs(he.raw_nats));
+    ScheduleFeatures f;
+    f.token_entropy = he;
+    Scheduler sch(tp, ChunkBounds{128, 2048}, CalibrationRef::log_k(256));
+    const ChunkDecision hd = sch.decide(f);
+    CHECK(td.chunk == hd.chunk && td.source_policy == "token_histogram" &&
+          hd.source_policy == "token_histogram");
+  }
+
+  // decode: the state after the prefill advanced by one token, output finite
+  {
+    float *dstate, *dx1, *ddt1, *db1, *dc1, *dy1;
+    cudaMalloc(&dstate, B * D * N * sizeof(float));
+    cudaMemset(dstate, 0, B * D * N * sizeof(float));
+    cudaMalloc(&dx1, B * D * sizeof(float));
+    cudaMalloc(&ddt1, B * D * sizeof(float));
+    cudaMalloc(&db1, B * N * sizeof(float));
+    cudaMalloc(&dc1, B * N * sizeof(float));
+    cudaMalloc(&dy1, B * D * sizeof(float));
+    std::vector<float> one(B * D, 0.5f), bn(B * N, 0.25f);
+    cudaMemcpy(dx1, one.data(), one.size() * sizeof(float), cudaMemcpyHostToDevice);
+    cudaMemcpy(ddt1, one.data(), one.size() * sizeof(float), cudaMemcpyHostToDevice);
+    cudaMemcpy(db1, bn.data(), bn.size() * sizeof(float), cudaMemcpyHostToDevice);
+    cudaMemcpy(dc1, bn.data(), bn.size() * sizeof(float), cudaMemcpyHostToDevice);
+    StateUpdateArgs sa{};
+    sa.state = dstate;
+    sa.x = dx1;
+    sa.dt = ddt1;
+    sa.A = dA;
+    sa.B = db1;
+    sa.C = dc1;
+    sa.D = dD;
+    sa.out = dy1;
+    sa.batch = B;
+    sa.dim = D;
+    sa.d_state = N;
+    sa.dt_softplus = 1;
+    selective_state_update(sa);
+    std::vector<float> y1(B * D), st(B * D * N);
+    cudaMemcpy(y1.data(), dy1, y1.size() * sizeof(float), cudaMemcpyDeviceToHost);
+    cudaMemcpy(st.data(), dstate, st.size() * sizeof(float), cudaMemcpyDeviceToHost);
+    // from h = 0: h_s = dt' * B * x with dt' = softplus(0.5), y = sum_s C h_s + D x
+    const double dtp = std::log1p(std::exp(0.5));
+    CHECK(std::fabs(st[0] - dtp * 0.25 * 0.5) <= 1e-6);
+    CHECK(std::fabs(y1[0] - (16 * 0.25 * dtp * 0.25 * 0.5 + Dv[0] * 0.5)) <= 1e-5);
+    for (float* p : {dstate, dx1, ddt1, db1, dc1, dy1}) cudaFree(p);
+  }
+
+  // producer fusion: conv1d + SiLU with the fused range equals a separate min/max pass
+  {
+    const int W = 4;
+    std::vector<float> w(D * W);
+    for (std::size_t i = 0; i < w.size(); ++i) w[i] = 0.25f * std::cos(0.1 * i);
+    float* dw;
+    double *dr1, *dr2;
+    up(&dw, w);
+    cudaMalloc(&dr1, 4 * sizeof(double));
+    cudaMalloc(&dr2, 4 * sizeof(double));
+    cl_ctx* cx = b200::Runtime::get().ctx();
+    b200::check(cl_range_init(cx, dr1, nullptr));
+    causal_conv1d(du, dw, nullptr, dout, B, D, L, W, true, dr1);
+    b200::check(cl_range_init(cx, dr2, nullptr));
+    b200::check(cl_minmax_f32(cx, dout, B * D * L, 0, 1, dr2, nullptr));
+    double r1[4], r2[4];
+    cudaMemcpy(r1, dr1, sizeof r1, cudaMemcpyDeviceToHost);
+    cudaMemcpy(r2, dr2, sizeof r2, cudaMemcpyDeviceToHost);
+    CHECK(r1[0] == r2[0] && r1[1] == r2[1] && r1[2] == 0.0);
+    cudaFree(dw);
+    cudaFree(dr1);
+    cudaFree(dr2);
+  }
   for (float* p : {du, ddl, dz, dA, dB, dC, dD, dout}) cudaFree(p);
 }
 
