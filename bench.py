@@ -236,7 +236,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-producer", action="store_true",
                     help="skip the side measurements (conv1d producer fusion, token entropy)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -507,41 +507,67 @@ def token_entropy_measure(torch, device, x, reps=10):
 
 
 def e2e_measure(torch, dist, world, device, x, pf, L, global_batch, steps):
-    """Same metric through the public API (Prefill) with the step's inputs copied
-    from pinned host memory and the output read back, inside the timed region."""
+    """Same metric through the public API (Prefill) with every step's inputs copied from
+    pinned host memory and its output read back, inside the timed region.
+
+    Serving-style pipeline over three streams: H2D of step i+1 (copy engine 1), the prefill
+    of step i (SMs) and the D2H of step i-1 (copy engine 2) overlap; device inputs and
+    outputs are double-buffered and ordered by events (PCIe is full duplex, so the
+    readback hides under the next step's upload).  Timed with device events from the
+    first copy to the last readback."""
     host = {k: v.cpu().pin_memory() for k, v in x.items()}
     h_out = torch.empty_like(host["u"]).pin_memory()
-    dev = {k: torch.empty_like(v) for k, v in x.items()}
-    out = torch.empty_like(x["u"])
+    bufs = [{k: torch.empty_like(v) for k, v in x.items()} for _ in range(2)]
+    outs = [torch.empty_like(x["u"]) for _ in range(2)]
     h2d = sum(v.numel() * 4 for v in host.values())
     d2h = h_out.numel() * 4
+    s_in, s_run, s_out = (torch.cuda.Stream(device) for _ in range(3))
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    in_done, run_done, out_done = ([ev() for _ in range(2)] for _ in range(3))
+    used = [False, False]
 
-    def one():
-        for k in dev:
-            dev[k].copy_(host[k], non_blocking=True)
-        pf(dev["u"], dev["delta"], dev["A"], dev["B"], dev["C"], dev["D"], dev["z"],
-           dev["delta_bias"], True, out=out)
-        h_out.copy_(out, non_blocking=True)
+    def step(i):
+        j = i % 2
+        with torch.cuda.stream(s_in):
+            if used[j]:
+                s_in.wait_event(run_done[j])  # buffer j's previous prefill has read it
+            for k in bufs[j]:
+                bufs[j][k].copy_(host[k], non_blocking=True)
+            in_done[j].record(s_in)
+        with torch.cuda.stream(s_run):
+            s_run.wait_event(in_done[j])
+            if used[j]:
+                s_run.wait_event(out_done[j])  # output j has been read back
+            d = bufs[j]
+            pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"],
+               True, out=outs[j])
+            run_done[j].record(s_run)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(run_done[j])
+            h_out.copy_(outs[j], non_blocking=True)
+            out_done[j].record(s_out)
+        used[j] = True
 
-    one()
+    step(0)
+    step(1)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(steps):
-        one()
-    e.record()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(s_in)
+    for i in range(steps):
+        step(i)
+    end.record(s_out)
     torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / steps
+    ms = start.elapsed_time(end) / steps
     if world > 1:
         t = torch.tensor([ms], device=device, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    del dev, out
+    del bufs, outs
     return {"value": global_batch * L / (ms / 1e3), "unit": "tokens/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms,
-            "steps": steps}
+            "steps": steps, "pipeline": "H2D(i+1) | prefill(i) | D2H(i-1) on 3 streams"}
 
 
 if __name__ == "__main__":
