@@ -80,23 +80,22 @@ __device__ __forceinline__ float silu_canon(float z) {
   return z * r;
 }
 
-// y = sum_s c[s] h[s] for N = 16 in the lane-pair kernel's order: lane half hf holds
-// states 8hf..8hf+7 and accumulates ya over (0,1),(4,5) and yb over (2,3),(6,7) with
-// FFMA2, then (ya.lo+yb.lo) + (ya.hi+yb.hi); the halves are added last.
+// y = sum_s c[s] h[s] for N = 16 by a fixed tree over the products p_s = c_s h_s:
+//   L_half = ((p0 + p2) + (p4 + p6)) + ((p1 + p3) + (p5 + p7))   over the half's 8 states
+//   y      = L_0 + L_1
+// The lane-pair kernel evaluates it with ADD2 on register pairs (P_k = (p_2k, p_2k+1)),
+// the state-parallel kernel with an xor-2, 4, 1, 8 butterfly: IEEE addition is
+// commutative, so every lane order of the same tree gives the same bits.
 __device__ __forceinline__ float cdot16_canon(const float* c, const float* h) {
-  float p[2];
+  float L[2];
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf) {
-    const float* cc = c + 8 * hf;
-    const float* hh = h + 8 * hf;
-    // first term as fma(c, h, +0) like the FFMA2 chain started from 0 (sign of zero)
-    const float ya_lo = fmaf(cc[4], hh[4], fmaf(cc[0], hh[0], 0.f));
-    const float ya_hi = fmaf(cc[5], hh[5], fmaf(cc[1], hh[1], 0.f));
-    const float yb_lo = fmaf(cc[6], hh[6], fmaf(cc[2], hh[2], 0.f));
-    const float yb_hi = fmaf(cc[7], hh[7], fmaf(cc[3], hh[3], 0.f));
-    p[hf] = (ya_lo + yb_lo) + (ya_hi + yb_hi);
+    float p[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i] = c[8 * hf + i] * h[8 * hf + i];
+    L[hf] = ((p[0] + p[2]) + (p[4] + p[6])) + ((p[1] + p[3]) + (p[5] + p[7]));
   }
-  return p[0] + p[1];
+  return L[0] + L[1];
 }
 
 __device__ __forceinline__ int read_chunk(const cl_decision* d, int fixed_chunk, int* status) {
@@ -594,19 +593,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + t * kN * 4);
         const ulonglong2* Ct = reinterpret_cast<const ulonglong2*>(sC + t * kN * 4);
         const f2_t xx = pk(xs[k], xs[k]);
-        f2_t ya = 0ull, yb = 0ull;
+        f2_t P[kN / 2];  // products c*h as register pairs
 #pragma unroll
         for (int q = 0; q < kN / 4; ++q) {
           const ulonglong2 bq = Bt[q];
           const ulonglong2 cq = Ct[q];
           h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
           h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
-          ya = fma2(cq.x, h2[2 * q], ya);
-          yb = fma2(cq.y, h2[2 * q + 1], yb);
+          P[2 * q] = mul2(cq.x, h2[2 * q]);
+          P[2 * q + 1] = mul2(cq.y, h2[2 * q + 1]);
         }
-        float a0, a1;
-        upk(add2(ya, yb), a0, a1);
-        yy[k] = a0 + a1;
+        // the canonical tree (cdot16_canon): L_0 over pairs 0-3, L_1 over pairs 4-7
+        float l0a, l0b, l1a, l1b;
+        upk(add2(add2(P[0], P[1]), add2(P[2], P[3])), l0a, l0b);
+        upk(add2(add2(P[4], P[5]), add2(P[6], P[7])), l1a, l1b);
+        yy[k] = (l0a + l0b) + (l1a + l1b);
       }
       const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
       f2_t y01 = fma2(pk(Dc, Dc), pk(uu[0], uu[1]), pk(yy[0], yy[1]));
@@ -744,18 +745,19 @@ __device__ __forceinline__ void pair_box(const unsigned char* st, float* ydst, i
       const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + t * kBCRow);
       const ulonglong2* Ct = reinterpret_cast<const ulonglong2*>(sC + t * kBCRow);
       const f2_t xx = pk(xs[k], xs[k]);
-      f2_t ya = 0ull, yb = 0ull;
+      f2_t P[kP];  // products c*h as register pairs
 #pragma unroll
       for (int q = 0; q < kP / 2; ++q) {
         const ulonglong2 bq = Bt[q];
         const ulonglong2 cq = Ct[q];
         h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
         h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
-        ya = fma2(cq.x, h2[2 * q], ya);
-        yb = fma2(cq.y, h2[2 * q + 1], yb);
+        P[2 * q] = mul2(cq.x, h2[2 * q]);
+        P[2 * q + 1] = mul2(cq.y, h2[2 * q + 1]);
       }
+      // this half's L of the canonical tree (cdot16_canon)
       float a0, a1;
-      upk(add2(ya, yb), a0, a1);
+      upk(add2(add2(P[0], P[1]), add2(P[2], P[3])), a0, a1);
       yp[k] = a0 + a1;
     }
     // lane hf finalises timesteps (2hf, 2hf+1): swap the partial sums it does not own
