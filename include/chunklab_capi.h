@@ -195,7 +195,7 @@ typedef struct {
   int delta_softplus;
 } cl_mamba1_args;
 
-/* Scan variants: CL_SCAN_AUTO picks by shape. */
+/* Scan variants (all bit-identical): CL_SCAN_AUTO picks by shape. */
 enum { CL_SCAN_AUTO = 0, CL_SCAN_ROWSEQ_TMA = 1, CL_SCAN_GENERIC = 2 };
 int cl_selective_scan_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_decision* d_decision,
                           int fixed_chunk /* used when d_decision == NULL */, int variant,

@@ -80,7 +80,7 @@ __device__ __forceinline__ float silu_canon(float z) {
   return z * r;
 }
 
-// y = sum_s c[s] h[s] for N = 16 by a fixed tree over the products p_s = c_s h_s:
+// y = sum_s c[s] h[s] for N = 16 by a fixed tree over the products p_s = fma(c_s, h_s, +0):
 //   L_half = ((p0 + p2) + (p4 + p6)) + ((p1 + p3) + (p5 + p7))   over the half's 8 states
 //   y      = L_0 + L_1
 // The lane-pair kernel evaluates it with ADD2 on register pairs (P_k = (p_2k, p_2k+1)),
@@ -90,12 +90,16 @@ __device__ __forceinline__ float cdot16_canon(const float* c, const float* h) {
   float L[2];
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf) {
+    // products as fma(c, h, +0) and adds as __fadd_rn: neither can be contracted, so
+    // ptxas cannot fuse a product into the tree's first add on any path (it does fuse
+    // f32x2 mul/add pairs in the FFMA2 code otherwise)
     float p[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) p[i] = c[8 * hf + i] * h[8 * hf + i];
-    L[hf] = ((p[0] + p[2]) + (p[4] + p[6])) + ((p[1] + p[3]) + (p[5] + p[7]));
+    for (int i = 0; i < 8; ++i) p[i] = fmaf(c[8 * hf + i], h[8 * hf + i], 0.f);
+    L[hf] = __fadd_rn(__fadd_rn(__fadd_rn(p[0], p[2]), __fadd_rn(p[4], p[6])),
+                      __fadd_rn(__fadd_rn(p[1], p[3]), __fadd_rn(p[5], p[7])));
   }
-  return L[0] + L[1];
+  return __fadd_rn(L[0], L[1]);
 }
 
 __device__ __forceinline__ int read_chunk(const cl_decision* d, int fixed_chunk, int* status) {
@@ -143,14 +147,14 @@ __global__ void __launch_bounds__(128) generic_kernel(GenericArgs a) {
     const float u = a.u[row * a.L + t];
     float dt = a.delta[row * a.L + t] + bias;
     if (a.softplus) dt = softplus_canon(dt);
-    const float x = dt * u;
+    const float x = __fmul_rn(dt, u);
     float y = 0.f;
     if (NS == 16) {
       float cv[16];
 #pragma unroll
       for (int s = 0; s < 16; ++s) {
         const float dA = ex2_approx(A2[s] * dt);
-        h[s] = fmaf(dA, h[s], Bb[s * a.L + t] * x);
+        h[s] = fmaf(dA, h[s], __fmul_rn(Bb[s * a.L + t], x));
         cv[s] = Cb[s * a.L + t];
       }
       y = cdot16_canon(cv, h);
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(128) generic_kernel(GenericArgs a) {
       for (int s = 0; s < (NS > 0 ? NS : 64); ++s) {
         if (s < N) {
           const float dA = ex2_approx(A2[s] * dt);
-          h[s] = fmaf(dA, h[s], Bb[s * a.L + t] * x);
+          h[s] = fmaf(dA, h[s], __fmul_rn(Bb[s * a.L + t], x));
           y = fmaf(Cb[s * a.L + t], h[s], y);
         }
       }
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(128) decode_kernel(DecodeArgs a) {
   float dt = a.dt[row] + (a.dt_bias ? a.dt_bias[c] : 0.f);
   if (a.softplus) dt = softplus_canon(dt);
   const float u = a.x[row];
-  const float xx = dt * u;
+  const float xx = __fmul_rn(dt, u);
   float* st = a.state + row * N;
   const float* Bb = a.B + b * N;
   const float* Cb = a.C + b * N;
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(128) decode_kernel(DecodeArgs a) {
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
       const float dA = ex2_approx((a.A[c * 16 + s] * kLog2e) * dt);
-      h[s] = fmaf(dA, st[s], Bb[s] * xx);
+      h[s] = fmaf(dA, st[s], __fmul_rn(Bb[s], xx));
       cv[s] = Cb[s];
     }
     y = cdot16_canon(cv, h);
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(128) decode_kernel(DecodeArgs a) {
   } else {
     for (int s = 0; s < N; ++s) {
       const float dA = ex2_approx((a.A[c * N + s] * kLog2e) * dt);
-      const float h = fmaf(dA, st[s], Bb[s] * xx);
+      const float h = fmaf(dA, st[s], __fmul_rn(Bb[s], xx));
       y = fmaf(Cb[s], h, y);
       st[s] = h;
     }
@@ -600,8 +604,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
           const ulonglong2 cq = Ct[q];
           h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
           h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
-          P[2 * q] = mul2(cq.x, h2[2 * q]);
-          P[2 * q + 1] = mul2(cq.y, h2[2 * q + 1]);
+          P[2 * q] = fma2(cq.x, h2[2 * q], 0ull);  // fma(c, h, +0): not contractible
+          P[2 * q + 1] = fma2(cq.y, h2[2 * q + 1], 0ull);
         }
         // the canonical tree (cdot16_canon): L_0 over pairs 0-3, L_1 over pairs 4-7
         float l0a, l0b, l1a, l1b;
@@ -752,8 +756,8 @@ __device__ __forceinline__ void pair_box(const unsigned char* st, float* ydst, i
         const ulonglong2 cq = Ct[q];
         h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
         h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
-        P[2 * q] = mul2(cq.x, h2[2 * q]);
-        P[2 * q + 1] = mul2(cq.y, h2[2 * q + 1]);
+        P[2 * q] = fma2(cq.x, h2[2 * q], 0ull);  // fma(c, h, +0): not contractible
+        P[2 * q + 1] = fma2(cq.y, h2[2 * q + 1], 0ull);
       }
       // this half's L of the canonical tree (cdot16_canon)
       float a0, a1;
@@ -1055,13 +1059,24 @@ struct ScanCfg {
   int kind, box, warps, stages;
 };
 constexpr ScanCfg kCfgs[] = {
-    {kWarpSpecPair, 16, 14, 2},  // default: 14 consumer + 2 producer warps per SM
+    {kWarpSpecPair, 16, 14, 2},  // 14 consumer + 2 producer warps per SM (C3, C4)
     {kRowSeq, 32, 4, 3},         // 32-row tiles, self-fed TMA rings
     {kRowSeq, 16, 8, 3},
     {kRowSeq, 16, 7, 3},
+    // few 16-row tiles (C1: 96, C2: 128): fewer consumers per CTA so the tiles spread over
+    // all SMs instead of packing 14 to an SM (one producer, deeper ring)
+    {kWarpSpecPair, 16, 1, 4},
+    {kWarpSpecPair, 16, 2, 4},
+    {kWarpSpecPair, 16, 4, 4},
+    {kWarpSpecPair, 16, 7, 3},
 };
 constexpr int kDefaultCfg = 0;
-constexpr int kProducers = 2;
+
+// producers per CTA: two keep up with 14 consumers, one with up to 7
+template <int WARPS>
+constexpr int producers_for() {
+  return WARPS >= 8 ? 2 : 1;
+}
 
 template <typename K>
 cudaError_t set_smem(K kern, size_t smem) {
@@ -1076,6 +1091,7 @@ int grid_for(int n_tiles, int warps, int num_sms) {
 
 template <int BOX, int WARPS, int STAGES, bool SP, bool HZ>
 cudaError_t launch_ws(const CUtensorMap (&m)[6], const TmaArgs& t, int num_sms, cudaStream_t s) {
+  constexpr int kProducers = producers_for<WARPS>();
   auto kern = rowpair_ws_kernel<BOX, WARPS, STAGES, SP, HZ, kProducers>;
   const size_t smem = size_t(WARPS) * STAGES * GeoP<BOX>::kStageBytes + 1024 +
                       size_t(WARPS) * STAGES * (16 + 8);
@@ -1102,26 +1118,36 @@ cudaError_t launch_rowseq(const CUtensorMap (&m)[6], const TmaArgs& t, int num_s
 template <bool WS, int BOX, int WARPS, int STAGES>
 cudaError_t dispatch(bool sp, bool hz, const CUtensorMap (&m)[6], const TmaArgs& t, int n,
                      cudaStream_t s) {
-  if (WS) {
+  if constexpr (WS) {
     if (sp && hz) return launch_ws<BOX, WARPS, STAGES, true, true>(m, t, n, s);
     if (sp) return launch_ws<BOX, WARPS, STAGES, true, false>(m, t, n, s);
     if (hz) return launch_ws<BOX, WARPS, STAGES, false, true>(m, t, n, s);
     return launch_ws<BOX, WARPS, STAGES, false, false>(m, t, n, s);
+  } else {
+    if (sp && hz) return launch_rowseq<BOX, WARPS, STAGES, true, true>(m, t, n, s);
+    if (sp) return launch_rowseq<BOX, WARPS, STAGES, true, false>(m, t, n, s);
+    if (hz) return launch_rowseq<BOX, WARPS, STAGES, false, true>(m, t, n, s);
+    return launch_rowseq<BOX, WARPS, STAGES, false, false>(m, t, n, s);
   }
-  if (sp && hz) return launch_rowseq<BOX, WARPS, STAGES, true, true>(m, t, n, s);
-  if (sp) return launch_rowseq<BOX, WARPS, STAGES, true, false>(m, t, n, s);
-  if (hz) return launch_rowseq<BOX, WARPS, STAGES, false, true>(m, t, n, s);
-  return launch_rowseq<BOX, WARPS, STAGES, false, false>(m, t, n, s);
 }
 
-int scan_cfg_index() {
-  static int idx = [] {
+// CL_SCAN_CFG=<row> forces a kCfgs row (experiments); otherwise the warp-specialised
+// kernel with the fewest consumers per CTA that still puts every 16-row tile on its own
+// SM (14 consumers once there are >= 7 tiles per SM's worth).
+int scan_cfg_index(uint64_t pair_tiles, int num_sms) {
+  static const int forced = [] {
     const char* e = getenv("CL_SCAN_CFG");
-    int v = e ? atoi(e) : kDefaultCfg;
-    if (v < 0 || v >= static_cast<int>(sizeof(kCfgs) / sizeof(kCfgs[0]))) v = kDefaultCfg;
-    return v;
+    if (!e) return -1;
+    const int v = atoi(e);
+    return v >= 0 && v < static_cast<int>(sizeof(kCfgs) / sizeof(kCfgs[0])) ? v : -1;
   }();
-  return idx;
+  if (forced >= 0) return forced;
+  const uint64_t per_sm = (pair_tiles + num_sms - 1) / num_sms;
+  if (per_sm <= 1) return 4;
+  if (per_sm <= 2) return 5;
+  if (per_sm <= 4) return 6;
+  if (per_sm <= 7) return 7;
+  return kDefaultCfg;
 }
 
 }  // namespace
@@ -1133,7 +1159,8 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     return fail(ctx, CL_E_INVALID, "scan variant rowseq_tma needs d_state 16, L % 4 == 0 and 16-byte aligned buffers");
   const bool use_tma = variant == CL_SCAN_ROWSEQ_TMA || (variant == CL_SCAN_AUTO && tma_ok);
   if (use_tma) {
-    const int cfg_idx = scan_cfg_index();
+    const uint64_t pair_tiles = ((a.dim + kRowsP - 1) / kRowsP) * a.batch;
+    const int cfg_idx = scan_cfg_index(pair_tiles, ctx->num_sms);
     const ScanCfg cfg = kCfgs[cfg_idx];
     const bool ws = cfg.kind == kWarpSpecPair;
     const uint64_t L = a.seq_len, D = a.dim, Bt = a.batch;
@@ -1195,6 +1222,10 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       case 1: e = dispatch<false, 32, 4, 3>(sp, hz, m, t, n, s); break;
       case 2: e = dispatch<false, 16, 8, 3>(sp, hz, m, t, n, s); break;
       case 3: e = dispatch<false, 16, 7, 3>(sp, hz, m, t, n, s); break;
+      case 4: e = dispatch<true, 16, 1, 4>(sp, hz, m, t, n, s); break;
+      case 5: e = dispatch<true, 16, 2, 4>(sp, hz, m, t, n, s); break;
+      case 6: e = dispatch<true, 16, 4, 4>(sp, hz, m, t, n, s); break;
+      case 7: e = dispatch<true, 16, 7, 3>(sp, hz, m, t, n, s); break;
       default: e = dispatch<true, 16, 14, 2>(sp, hz, m, t, n, s); break;
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
