@@ -80,24 +80,23 @@ __device__ __forceinline__ float silu_canon(float z) {
   return z * r;
 }
 
-// y = sum_s c[s] h[s] for N = 16 by a fixed tree over the products p_s = fma(c_s, h_s, +0):
-//   L_half = ((p0 + p2) + (p4 + p6)) + ((p1 + p3) + (p5 + p7))   over the half's 8 states
-//   y      = L_0 + L_1
-// The lane-pair kernel evaluates it with ADD2 on register pairs (P_k = (p_2k, p_2k+1)),
-// the state-parallel kernel with an xor-2, 4, 1, 8 butterfly: IEEE addition is
-// commutative, so every lane order of the same tree gives the same bits.
+// y = sum_s c[s] h[s] for N = 16 in the lane-pair kernel's order: lane half hf holds
+// states 8hf..8hf+7 and accumulates, as FFMA2 chains started from +0,
+//   ya = (s0,s1) then (s4,s5),   yb = (s2,s3) then (s6,s7)
+// then L_hf = (ya.lo + yb.lo) + (ya.hi + yb.hi); y = L_0 + L_1.  Every step is an
+// explicit fused multiply-add or a plain add of two values that are not products, so no
+// compiler can contract it differently on different paths.
 __device__ __forceinline__ float cdot16_canon(const float* c, const float* h) {
   float L[2];
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf) {
-    // products as fma(c, h, +0) and adds as __fadd_rn: neither can be contracted, so
-    // ptxas cannot fuse a product into the tree's first add on any path (it does fuse
-    // f32x2 mul/add pairs in the FFMA2 code otherwise)
-    float p[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) p[i] = fmaf(c[8 * hf + i], h[8 * hf + i], 0.f);
-    L[hf] = __fadd_rn(__fadd_rn(__fadd_rn(p[0], p[2]), __fadd_rn(p[4], p[6])),
-                      __fadd_rn(__fadd_rn(p[1], p[3]), __fadd_rn(p[5], p[7])));
+    const float* cc = c + 8 * hf;
+    const float* hh = h + 8 * hf;
+    const float ya_lo = fmaf(cc[4], hh[4], fmaf(cc[0], hh[0], 0.f));
+    const float ya_hi = fmaf(cc[5], hh[5], fmaf(cc[1], hh[1], 0.f));
+    const float yb_lo = fmaf(cc[6], hh[6], fmaf(cc[2], hh[2], 0.f));
+    const float yb_hi = fmaf(cc[7], hh[7], fmaf(cc[3], hh[3], 0.f));
+    L[hf] = __fadd_rn(__fadd_rn(ya_lo, yb_lo), __fadd_rn(ya_hi, yb_hi));
   }
   return __fadd_rn(L[0], L[1]);
 }
@@ -597,20 +596,25 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + t * kN * 4);
         const ulonglong2* Ct = reinterpret_cast<const ulonglong2*>(sC + t * kN * 4);
         const f2_t xx = pk(xs[k], xs[k]);
-        f2_t P[kN / 2];  // products c*h as register pairs
+        // canonical FFMA2 chains per half (cdot16_canon): pairs 0,2 / 1,3 and 4,6 / 5,7
+        f2_t ya0 = 0ull, yb0 = 0ull, ya1 = 0ull, yb1 = 0ull;
 #pragma unroll
         for (int q = 0; q < kN / 4; ++q) {
           const ulonglong2 bq = Bt[q];
           const ulonglong2 cq = Ct[q];
           h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
           h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
-          P[2 * q] = fma2(cq.x, h2[2 * q], 0ull);  // fma(c, h, +0): not contractible
-          P[2 * q + 1] = fma2(cq.y, h2[2 * q + 1], 0ull);
+          if (q < 2) {
+            ya0 = fma2(cq.x, h2[2 * q], ya0);
+            yb0 = fma2(cq.y, h2[2 * q + 1], yb0);
+          } else {
+            ya1 = fma2(cq.x, h2[2 * q], ya1);
+            yb1 = fma2(cq.y, h2[2 * q + 1], yb1);
+          }
         }
-        // the canonical tree (cdot16_canon): L_0 over pairs 0-3, L_1 over pairs 4-7
         float l0a, l0b, l1a, l1b;
-        upk(add2(add2(P[0], P[1]), add2(P[2], P[3])), l0a, l0b);
-        upk(add2(add2(P[4], P[5]), add2(P[6], P[7])), l1a, l1b);
+        upk(add2(ya0, yb0), l0a, l0b);
+        upk(add2(ya1, yb1), l1a, l1b);
         yy[k] = (l0a + l0b) + (l1a + l1b);
       }
       const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
@@ -749,19 +753,18 @@ __device__ __forceinline__ void pair_box(const unsigned char* st, float* ydst, i
       const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + t * kBCRow);
       const ulonglong2* Ct = reinterpret_cast<const ulonglong2*>(sC + t * kBCRow);
       const f2_t xx = pk(xs[k], xs[k]);
-      f2_t P[kP];  // products c*h as register pairs
+      f2_t ya = 0ull, yb = 0ull;  // canonical FFMA2 chains (cdot16_canon)
 #pragma unroll
       for (int q = 0; q < kP / 2; ++q) {
         const ulonglong2 bq = Bt[q];
         const ulonglong2 cq = Ct[q];
         h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
         h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
-        P[2 * q] = fma2(cq.x, h2[2 * q], 0ull);  // fma(c, h, +0): not contractible
-        P[2 * q + 1] = fma2(cq.y, h2[2 * q + 1], 0ull);
+        ya = fma2(cq.x, h2[2 * q], ya);
+        yb = fma2(cq.y, h2[2 * q + 1], yb);
       }
-      // this half's L of the canonical tree (cdot16_canon)
       float a0, a1;
-      upk(add2(add2(P[0], P[1]), add2(P[2], P[3])), a0, a1);
+      upk(add2(ya, yb), a0, a1);
       yp[k] = a0 + a1;
     }
     // lane hf finalises timesteps (2hf, 2hf+1): swap the partial sums it does not own
