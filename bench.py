@@ -407,7 +407,18 @@ def main():
 
     # ---- e2e through the public API with host buffers (pinned), H2D/D2H timed
     if not args.no_e2e:
-        result["e2e"] = e2e_measure(torch, dist, world, device, x, pf, L, global_batch,
+        if world > 1:  # the public multi-GPU API: global entropy over all ranks' rows
+            from paper_2604_10597_b200.sharded import ShardedPrefill
+            sp = ShardedPrefill(pf, plan)
+
+            def run_prefill(d, o):
+                sp(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"],
+                   True, out=o)
+        else:
+            def run_prefill(d, o):
+                pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"],
+                   True, out=o)
+        result["e2e"] = e2e_measure(torch, dist, world, device, x, run_prefill, L, global_batch,
                                     args.e2e_steps)
     del x, out
     torch.cuda.empty_cache()
@@ -506,7 +517,7 @@ def token_entropy_measure(torch, device, x, reps=10):
                         f"length={u.shape[-1]}), K=256, two passes over u"}
 
 
-def e2e_measure(torch, dist, world, device, x, pf, L, global_batch, steps):
+def e2e_measure(torch, dist, world, device, x, run_prefill, L, global_batch, steps):
     """Same metric through the public API (Prefill) with every step's inputs copied from
     pinned host memory and its output read back, inside the timed region.
 
@@ -538,9 +549,7 @@ def e2e_measure(torch, dist, world, device, x, pf, L, global_batch, steps):
             s_run.wait_event(in_done[j])
             if used[j]:
                 s_run.wait_event(out_done[j])  # output j has been read back
-            d = bufs[j]
-            pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"],
-               True, out=outs[j])
+            run_prefill(bufs[j], outs[j])
             run_done[j].record(s_run)
         with torch.cuda.stream(s_out):
             s_out.wait_event(run_done[j])
