@@ -545,94 +545,6 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
     if (cta_hist[b]) atomicAdd(d_counts + b, static_cast<unsigned long long>(cta_hist[b]));
 }
 
-// Variant (CL_HIST_VARIANT=1): same TMA bulk ring, but per-warp u32 histograms in
-// shared memory updated with shared atomics (ATOMS); 1 KB per warp.
-template <bool FIXED>
-__global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
-    hist_f32_atoms_kernel(const float* __restrict__ v, uint64_t n, int range_mode,
-                          double fixed_lo, double fixed_hi, int k,
-                          const double* __restrict__ d_range, unsigned long long* d_counts) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* ring = smem;
-  uint32_t* whist = reinterpret_cast<uint32_t*>(ring + size_t(kStages) * kChunkBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(whist + kHistWarps * kLaneBins);
-  uint64_t* empty = full + kStages;
-  __shared__ BinParams sp;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (threadIdx.x == 0) {
-    sp = make_bin_params(d_range, range_mode, fixed_lo, fixed_hi, k);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, kHistWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int i = threadIdx.x; i < kHistWarps * kLaneBins; i += blockDim.x) whist[i] = 0;
-  __syncthreads();
-  const BinParams p = sp;
-  const uint64_t head = umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
-  const uint64_t body_n = ((n - head) / 4) * 4;
-  const float* body = v + head;
-  const uint64_t n_chunks = (body_n + kChunkFloats - 1) / kChunkFloats;
-  if (warp == kHistWarps) {
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
-        const int s = it % kStages;
-        const uint32_t phase = (it / kStages) & 1;
-        if (it >= kStages) mbar_wait(empty + s, phase ^ 1);
-        const uint64_t off = c * kChunkFloats;
-        const uint32_t bytes = static_cast<uint32_t>(umin64(kChunkFloats, body_n - off) * 4);
-        mbar_expect_tx(full + s, bytes);
-        bulk_g2s(ring + size_t(s) * kChunkBytes, body + off, bytes, full + s);
-      }
-    }
-    return;
-  }
-  uint32_t* h = whist + warp * kLaneBins;
-  if (blockIdx.x == 0 && warp == 0) {
-    for (uint64_t i = lane; i < head; i += 32) atomicAdd(h + bin_f32(v[i], p, FIXED), 1u);
-    for (uint64_t i = head + body_n + lane; i < n; i += 32)
-      atomicAdd(h + bin_f32(v[i], p, FIXED), 1u);
-  }
-  uint32_t it = 0;
-  for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
-    const int s = it % kStages;
-    const uint32_t phase = (it / kStages) & 1;
-    mbar_wait(full + s, phase);
-    const float4* tile = reinterpret_cast<const float4*>(ring + size_t(s) * kChunkBytes);
-    const uint64_t off = c * kChunkFloats;
-    const int valid4 = static_cast<int>(umin64(kChunkFloats, body_n - off) / 4);
-    float val[16];
-    bool ok[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int idx = j * (kHistWarps * 32) + warp * 32 + lane;
-      ok[j] = idx < valid4;
-      const float4 q = ok[j] ? tile[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
-      val[4 * j] = q.x;
-      val[4 * j + 1] = q.y;
-      val[4 * j + 2] = q.z;
-      val[4 * j + 3] = q.w;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + s);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      if (!ok[e / 4]) continue;
-      bool sl;
-      int b = bin_fast<FIXED>(val[e], p, &sl);
-      if (sl || p.exact_only) b = bin_index_exact(static_cast<double>(val[e]), p.lo, p.width, p.k);
-      atomicAdd(h + b, 1u);
-    }
-  }
-  named_bar(1, kHistWarps * 32);
-  for (int b = threadIdx.x; b < k; b += kHistWarps * 32) {
-    uint32_t sum = 0;
-    for (int w = 0; w < kHistWarps; ++w) sum += whist[w * kLaneBins + b];
-    if (sum) atomicAdd(d_counts + b, static_cast<unsigned long long>(sum));
-  }
-}
 
 // K > 256 (or f64 input): shared-memory atomics on a CTA histogram.
 template <typename T, int MODE>
@@ -1219,17 +1131,7 @@ cudaError_t launch_histogram_f32(const float* v, uint64_t n, uint64_t g0,
                                                  spec.fixed_lo, spec.fixed_hi, k, d_range,
                                                  counts);
     };
-    static const int variant = [] {
-      const char* e = getenv("CL_HIST_VARIANT");
-      return e ? atoi(e) : 0;
-    }();
-    if (variant == 1 && mode == 0) {
-      const size_t smem = size_t(kStages) * kChunkBytes + kHistWarps * kLaneBins * 4 + 2 * kStages * 8 + 64;
-      auto kern = fixed ? hist_f32_atoms_kernel<true> : hist_f32_atoms_kernel<false>;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      kern<<<grid, kHistThreads, smem, s>>>(v, n, spec.range_mode, spec.fixed_lo, spec.fixed_hi, k,
-                                            d_range, counts);
-    } else if (fixed) {
+    if (fixed) {
       if (mode == 0) launch(hist_f32_lane_kernel<0, true>);
       else if (mode == 1) launch(hist_f32_lane_kernel<1, true>);
       else launch(hist_f32_lane_kernel<2, true>);
