@@ -349,6 +349,25 @@ __device__ __forceinline__ void flush_warp(uint16_t* cnt, uint32_t* cta_hist, in
   __syncwarp();
 }
 
+// Which of 4 consecutive samples starting at global index gi are taken (gi % stride ==
+// 0), given r = gi % stride: bit e set iff (r + e) % stride == 0.
+__device__ __forceinline__ uint32_t sample_mask4(uint64_t r, uint64_t stride) {
+  const uint64_t e0 = r == 0 ? 0 : stride - r;  // first sampled offset
+  uint32_t m = e0 < 4 ? 1u << e0 : 0u;
+  if (stride < 4) {  // kernel argument: warp-uniform
+#pragma unroll
+    for (uint64_t k = 1; k < 4; ++k) {
+      const uint64_t e = e0 + k * stride;
+      m |= e < 4 ? 1u << e : 0u;
+    }
+  }
+  return m;
+}
+__device__ __forceinline__ uint64_t add_mod(uint64_t r, uint64_t d, uint64_t stride) {
+  r += d;  // r, d < stride
+  return r >= stride ? r - stride : r;
+}
+
 template <int MODE, bool FIXED>
 __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
     hist_f32_lane_kernel(const float* __restrict__ v, uint64_t n, uint64_t g0, uint64_t stride,
@@ -422,8 +441,18 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
 
   // byte address of this lane's counter for bin 0; bin b lives at + b*64
   const uint32_t cbase = smem_u32(counters + warp * kLaneBins * 32 + lane);
+  // strided sampling (MODE != 0): residue of this lane's first sample index in the
+  // current chunk, advanced incrementally (no per-sample 64-bit modulo)
+  const uint64_t lane_off = 4ull * static_cast<uint64_t>(warp * 32 + lane);
+  uint64_t r_chunk = 0, step_chunk = 0, step_j = 0;
+  if (MODE != 0) {
+    r_chunk = (g0 + head + static_cast<uint64_t>(blockIdx.x) * kChunkFloats + lane_off) % stride;
+    step_chunk = (static_cast<uint64_t>(gridDim.x) * kChunkFloats) % stride;
+    step_j = (4ull * kHistWarps * 32) % stride;
+  }
   uint32_t it = 0, since_flush = 0;
-  for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+  for (uint64_t c = blockIdx.x; c < n_chunks;
+       c += gridDim.x, ++it, r_chunk = MODE != 0 ? add_mod(r_chunk, step_chunk, stride) : 0) {
     const int s = it % kStages;
     const uint32_t phase = (it / kStages) & 1;
     mbar_wait(full + s, phase);
@@ -483,17 +512,16 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
     }
     float val[16];
     uint32_t inc = 0;  // bit e: sample e is valid and sampled
+    uint64_t r_j = r_chunk;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int idx = j * (kHistWarps * 32) + warp * 32 + lane;
       float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
       if (idx < valid4) {
         q = tile[idx];
-        const uint64_t gi = g0 + head + off + static_cast<uint64_t>(idx) * 4;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (sampled<MODE>(gi + e, stride)) inc |= 1u << (4 * j + e);
+        inc |= (MODE == 0 ? 0xfu : sample_mask4(r_j, stride)) << (4 * j);
       }
+      if (MODE != 0) r_j = add_mod(r_j, step_j, stride);
       val[4 * j] = q.x;
       val[4 * j + 1] = q.y;
       val[4 * j + 2] = q.z;
@@ -501,6 +529,27 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);
+
+    if (MODE != 0 && stride >= 4) {
+      // sparse sampling (e.g. the sampled-histogram policy's stride 8): each float4 holds
+      // at most one sample -- pick it with selects, then one predicated bin + RMW per
+      // float4, in order (no dynamic register indexing, no data-dependent loops)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t mj = (inc >> (4 * j)) & 0xfu;
+        const float v = (mj & 1u) ? val[4 * j] : (mj & 2u) ? val[4 * j + 1]
+                                                : (mj & 4u) ? val[4 * j + 2] : val[4 * j + 3];
+        if (mj) {
+          const int b = bin_f32(v, p, FIXED);
+          cnt[b * 32] = static_cast<uint16_t>(cnt[b * 32] + 1u);
+        }
+      }
+      if (++since_flush == kFlushChunks) {
+        flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+        since_flush = 0;
+      }
+      continue;
+    }
 
     int bin[16];
     uint32_t slow = 0;
