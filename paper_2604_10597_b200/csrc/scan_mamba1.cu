@@ -785,10 +785,108 @@ __device__ __forceinline__ void pair_box(const unsigned char* st, float* ydst, i
   }
 }
 
+// pair_box for a full box (valid == BOX), software-pipelined by one 4-timestep group:
+// group j+1's serial prologue (LDS of u / delta, bias add, softplus -- one MUFU then a
+// 9-deep FFMA2 chain -- and the partner-lane shuffle) is issued between group j's
+// exponentials and its recurrence, so its latency hides under group j's MUFU work
+// instead of stalling the MUFU pipe at every group boundary.  Same operations on the
+// same values as pair_box, so the outputs are bit-identical.
+template <int BOX, bool SP, bool HZ>
+__device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* ydst, int r,
+                                              int hf, float bias, float Dc,
+                                              const f2_t (&A2p)[kN / 4], f2_t (&h2)[kN / 4]) {
+  using G = GeoP<BOX>;
+  constexpr int kP = kN / 4;
+  constexpr int kG = BOX / 4;
+  constexpr int kBCRow = 2 * kN * 4;
+  const unsigned char* sB = st + 3 * G::kTileBytes + 32 * hf;
+  const unsigned char* sC = sB + kN * 4;
+  const f2_t bias2 = pk(bias, bias);
+  // prologue of group j: dt (4 timesteps, softplus'd), x = dt*u, and this lane's u pair
+  auto prep = [&](int j, float (&dt)[4], float (&xs)[4], f2_t& u2) {
+    const int off = Geo<BOX>::swz(r, j);
+    const float4 u4 = *reinterpret_cast<const float4*>(st + off);
+    const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
+    f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
+    if (SP) mine = softplus2(mine);
+    const f2_t other = shfl_xor2(mine, 1);
+    const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
+    const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
+    upk(dt01, dt[0], dt[1]);
+    upk(dt23, dt[2], dt[3]);
+    upk(x01, xs[0], xs[1]);
+    upk(x23, xs[2], xs[3]);
+    u2 = hf ? pk(u4.z, u4.w) : pk(u4.x, u4.y);
+  };
+  float dt[4], xs[4];
+  f2_t u2;
+  prep(0, dt, xs, u2);
+#pragma unroll
+  for (int j = 0; j < kG; ++j) {
+    f2_t dA[4][kP];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const f2_t dd = pk(dt[k], dt[k]);
+#pragma unroll
+      for (int i = 0; i < kP; ++i) {
+        float al, ah;
+        upk(mul2(A2p[i], dd), al, ah);
+        dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+      }
+    }
+    float ndt[4], nxs[4];
+    f2_t nu2 = 0ull;
+    if (j + 1 < kG) prep(j + 1, ndt, nxs, nu2);
+    float yp[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = 4 * j + k;
+      const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + t * kBCRow);
+      const ulonglong2* Ct = reinterpret_cast<const ulonglong2*>(sC + t * kBCRow);
+      const f2_t xx = pk(xs[k], xs[k]);
+      f2_t ya = 0ull, yb = 0ull;  // canonical FFMA2 chains (cdot16_canon)
+#pragma unroll
+      for (int q = 0; q < kP / 2; ++q) {
+        const ulonglong2 bq = Bt[q];
+        const ulonglong2 cq = Ct[q];
+        h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
+        h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
+        ya = fma2(cq.x, h2[2 * q], ya);
+        yb = fma2(cq.y, h2[2 * q + 1], yb);
+      }
+      float a0, a1;
+      upk(add2(ya, yb), a0, a1);
+      yp[k] = a0 + a1;
+    }
+    const f2_t keep = hf ? pk(yp[2], yp[3]) : pk(yp[0], yp[1]);
+    const f2_t give = hf ? pk(yp[0], yp[1]) : pk(yp[2], yp[3]);
+    const f2_t ysum = add2(keep, shfl_xor2(give, 1));
+    f2_t yo = fma2(pk(Dc, Dc), u2, ysum);
+    if (HZ) {
+      const float4 z4 =
+          *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + Geo<BOX>::swz(r, j));
+      yo = mul2(yo, silu2(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y)));
+    }
+    if (ydst) {
+      float y0, y1;
+      upk(yo, y0, y1);
+      __stcs(reinterpret_cast<float2*>(ydst + 4 * j + 2 * hf), make_float2(y0, y1));
+    }
+    if (j + 1 < kG) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        dt[k] = ndt[k];
+        xs[k] = nxs[k];
+      }
+      u2 = nu2;
+    }
+  }
+}
+
 // Per consumer warp and stage: full[s] (producer arrive.expect_tx + TMA bytes) and
 // empty[s] (consumer lane 0 arrive after its last shared-memory read of the stage).
 // The meta words (item, box) travel through shared memory under full[s]'s release.
-template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int NPROD>
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int NPROD, bool PIPE>
 __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     rowpair_ws_kernel(const __grid_constant__ CUtensorMap map_u,
                       const __grid_constant__ CUtensorMap map_dt,
@@ -937,9 +1035,12 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     }
 
     const int tbox = cur.t0 + box * BOX;
-    pair_box<BOX, SP, HZ>(wbase + slot * G::kStageBytes,
-                          row_valid ? a.out + size_t(row) * a.L + tbox : nullptr, r, hf,
-                          min(BOX, L - tbox), bias, Dc, A2p, h2);
+    float* ydst = row_valid ? a.out + size_t(row) * a.L + tbox : nullptr;
+    if (PIPE && tbox + BOX <= L)
+      pair_box_pipe<BOX, SP, HZ>(wbase + slot * G::kStageBytes, ydst, r, hf, bias, Dc, A2p, h2);
+    else
+      pair_box<BOX, SP, HZ>(wbase + slot * G::kStageBytes, ydst, r, hf, min(BOX, L - tbox), bias,
+                            Dc, A2p, h2);
     __syncwarp();
     if (lane == 0) mbar_arrive(wempty + slot);  // stage consumed: producer may refill
 
@@ -1057,7 +1158,7 @@ int grow(cl_ctx* ctx, T** ptr, size_t* have, size_t need, const char* what) {
 }
 
 // ---- kernel table (CL_SCAN_CFG=<index> selects a row, for experiments) ----
-enum ScanKind { kWarpSpecPair = 0, kRowSeq = 1 };
+enum ScanKind { kWarpSpecPair = 0, kRowSeq = 1, kWarpSpecPairNoPipe = 2 };
 struct ScanCfg {
   int kind, box, warps, stages;
 };
@@ -1072,6 +1173,7 @@ constexpr ScanCfg kCfgs[] = {
     {kWarpSpecPair, 16, 2, 4},
     {kWarpSpecPair, 16, 4, 4},
     {kWarpSpecPair, 16, 7, 3},
+    {kWarpSpecPairNoPipe, 16, 14, 2},  // 8: row 0 without the group software pipeline (A/B)
 };
 constexpr int kDefaultCfg = 0;
 
@@ -1092,10 +1194,10 @@ int grid_for(int n_tiles, int warps, int num_sms) {
   return max_useful < num_sms ? (max_useful < 1 ? 1 : max_useful) : num_sms;
 }
 
-template <int BOX, int WARPS, int STAGES, bool SP, bool HZ>
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, bool PIPE = true>
 cudaError_t launch_ws(const CUtensorMap (&m)[6], const TmaArgs& t, int num_sms, cudaStream_t s) {
   constexpr int kProducers = producers_for<WARPS>();
-  auto kern = rowpair_ws_kernel<BOX, WARPS, STAGES, SP, HZ, kProducers>;
+  auto kern = rowpair_ws_kernel<BOX, WARPS, STAGES, SP, HZ, kProducers, PIPE>;
   const size_t smem = size_t(WARPS) * STAGES * GeoP<BOX>::kStageBytes + 1024 +
                       size_t(WARPS) * STAGES * (16 + 8);
   cudaError_t e = set_smem(kern, smem);
@@ -1165,7 +1267,7 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     const uint64_t pair_tiles = ((a.dim + kRowsP - 1) / kRowsP) * a.batch;
     const int cfg_idx = scan_cfg_index(pair_tiles, ctx->num_sms);
     const ScanCfg cfg = kCfgs[cfg_idx];
-    const bool ws = cfg.kind == kWarpSpecPair;
+    const bool ws = cfg.kind != kRowSeq;
     const uint64_t L = a.seq_len, D = a.dim, Bt = a.batch;
     const int rows_per_tile = ws ? kRowsP : kRows;
     const int tiles_per_batch = static_cast<int>((D + rows_per_tile - 1) / rows_per_tile);
@@ -1229,6 +1331,10 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       case 5: e = dispatch<true, 16, 2, 4>(sp, hz, m, t, n, s); break;
       case 6: e = dispatch<true, 16, 4, 4>(sp, hz, m, t, n, s); break;
       case 7: e = dispatch<true, 16, 7, 3>(sp, hz, m, t, n, s); break;
+      case 8:
+        e = sp && hz ? launch_ws<16, 14, 2, true, true, false>(m, t, n, s)
+                     : dispatch<true, 16, 14, 2>(sp, hz, m, t, n, s);
+        break;
       default: e = dispatch<true, 16, 14, 2>(sp, hz, m, t, n, s); break;
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
