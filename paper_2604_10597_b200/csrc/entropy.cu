@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "cl_internal.h"
 #include "range.cuh"
@@ -248,43 +249,70 @@ __global__ void range_init_kernel(double* range) {
 }
 
 // ---------------------------------------------------------------------------
-// Stage 2: histogram, K <= 256.  Each lane owns private 16-bit counters laid out
-// [bin][lane] (16 KB per warp): increments need no atomics.  The per-lane
-// read-modify-write chain is broken into pairs (full chunks) or groups of four
+// Stage 2: histogram, K <= 256.  Each lane owns private counters (no atomics): the
+// per-lane read-modify-write chain is broken into pairs (full chunks) or groups of four
 // samples: the counters are loaded together, and the stores (in order) carry the
 // in-group duplicate count, so the last store to a bin holds the right total.  Input
-// is streamed through a 3-stage shared-memory ring filled by cp.async.bulk (TMA bulk
-// copies) issued by a dedicated producer warp; consumers release slots through an
-// mbarrier.  Two CTAs of 5 consumer warps per SM (80 KB of counters + a 30 KB ring
-// each): warps per SM is what the latency-bound loop needs (8 -> 10 warps: -4%; 9:
-// +6%), two rings halve the cross-warp gating of slot release (-1.6% vs one CTA of 10),
-// and the producer keeps kHistPrefetch more chunks on their way into L2 (-3%).
-// Fire-and-forget shared atomics on a conflict-free packed layout measured +39%
-// (ATOMS throughput); a bank-exclusive u16 layout (word (bin/2)*32 + lane) removes the 2-way
-// conflicts of lane pairs but measured +2% (extra address ALU in a latency-bound loop).
-// Counters are flushed (per CTA, then one atomic per bin) before they can overflow.
+// is streamed through a shared-memory ring filled by cp.async.bulk (TMA bulk copies)
+// issued by a dedicated producer warp; consumers release slots through an mbarrier.  Two
+// CTAs per SM: two rings halve the cross-warp gating of slot release, and the producer
+// keeps kHistPrefetch more chunks on their way into L2.  Fire-and-forget shared atomics
+// on a conflict-free packed layout measured +39% (ATOMS throughput).  Counters are
+// flushed (per CTA, then one atomic per bin) before they can overflow.
 // ---------------------------------------------------------------------------
-#ifndef CL_HIST_WARPS
-#define CL_HIST_WARPS 5
+// CL_HIST_U8=1 (default): 8-bit lane counters (8 KB per warp) in a bank-exclusive layout
+// (lane l's counters for bins 4r..4r+3 are the bytes of word r*32 + l, so every lane of a
+// warp always hits its own bank), 8 consumer warps per CTA and a 2-stage ring, flushed
+// every 15 chunks.  Measured at C3 (K=256, ms): u16 5 warps x 3 stages 0.251; u8 layouts
+// 7x3 0.246, 6x4 0.274, 8x2 0.231, 9x2 0.239 (spills), 10 warps x 8 samples 0.256;
+// 8-bit [bin][lane] without the bank-exclusive map 0.262 (4-way conflicts: the shared
+// pipe saturates at 91%).  Warps per SM, not ring depth, is what the loop needs.
+// CL_HIST_U8=0: 16-bit counters [bin][lane] (16 KB per warp, 2-way bank conflicts), 5 warps.
+#ifndef CL_HIST_U8
+#define CL_HIST_U8 1
 #endif
-constexpr int kHistWarps = CL_HIST_WARPS;             // consumer warps per CTA (16 KB counters each)
+#ifndef CL_HIST_WARPS
+#define CL_HIST_WARPS (CL_HIST_U8 ? 8 : 5)
+#endif
+constexpr int kHistWarps = CL_HIST_WARPS;             // consumer warps per CTA
 
 constexpr int kHistThreads = (kHistWarps + 1) * 32;  // + producer warp
 #ifndef CL_HIST_STAGES
-#define CL_HIST_STAGES 3
+#define CL_HIST_STAGES (CL_HIST_U8 ? 2 : 3)
 #endif
 constexpr int kStages = CL_HIST_STAGES;
-constexpr int kChunkFloats = kHistWarps * 512;        // 16 samples per lane per stage
+constexpr int kCntBytes = CL_HIST_U8 ? 1 : 2;              // bytes per lane counter
+#ifndef CL_HIST_SAMPLES
+#define CL_HIST_SAMPLES 16
+#endif
+constexpr int kLaneSamples = CL_HIST_SAMPLES;               // samples per lane per stage
+constexpr int kLaneF4 = kLaneSamples / 4;
+constexpr int kChunkFloats = kHistWarps * 32 * kLaneSamples;
 constexpr int kChunkBytes = kChunkFloats * 4;
 constexpr int kLaneBins = 256;
-constexpr size_t kCounterBytes = size_t(kHistWarps) * kLaneBins * 32 * 2;  // 160 KB
+constexpr int kBinStride = 32 * kCntBytes;                 // bytes per bin row (32 lanes)
+constexpr size_t kCounterBytes = size_t(kHistWarps) * kLaneBins * kBinStride;
 constexpr size_t kHistSmem = kCounterBytes + size_t(kStages) * kChunkBytes + kLaneBins * 4 +
                              2 * kStages * 8 + 64;
 // CTAs that fit one SM's 228 KB (227 KB usable per CTA + 1 KB reserved each)
 constexpr int kHistCtasPerSm = static_cast<int>(233472 / (kHistSmem + 1024 + 1024)) > 4
                                    ? 4
                                    : static_cast<int>(233472 / (kHistSmem + 1024 + 1024));
-constexpr int kFlushChunks = 4000;  // 16 samples/lane/chunk * 4000 < 65536
+// flush before a counter can overflow: chunks * samples per lane (+ up to 6 head/tail
+// samples on block 0, warp 0) stays below 2^(8*kCntBytes)
+constexpr int kFlushChunks = CL_HIST_U8 ? 240 / kLaneSamples : 4000;
+static_assert(kFlushChunks * kLaneSamples + 6 < (1 << (8 * kCntBytes)), "counter overflow");
+using cnt_t = std::conditional_t<CL_HIST_U8 != 0, uint8_t, uint16_t>;
+
+// Byte offset of bin b's counter from the lane's base (counters + warp block + lane's word
+// or half-word): u8 bank-exclusive (b/4)*128 + b%4, u16 [bin][lane] b*64.
+__device__ __forceinline__ uint32_t cofs(uint32_t b) {
+  if (CL_HIST_U8) return (b & ~3u) * 32u + (b & 3u);
+  return b * 64u;
+}
+__device__ __forceinline__ cnt_t& cref(unsigned char* lane_base, int b) {
+  return *reinterpret_cast<cnt_t*>(lane_base + cofs(static_cast<uint32_t>(b)));
+}
 #ifndef CL_HIST_PREFETCH
 #define CL_HIST_PREFETCH 3
 #endif
@@ -330,23 +358,53 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// Sum of the counters packed in one 32-bit word (two u16 or four u8).
+__device__ __forceinline__ uint32_t word_sum(uint32_t w) {
+  if (CL_HIST_U8) return __dp4a(w, 0x01010101u, 0u);
+  return (w & 0xffffu) + (w >> 16);
+}
+
 // Sum this warp's lane-private counters into the CTA histogram and clear them.
-__device__ __forceinline__ void flush_warp(uint16_t* cnt, uint32_t* cta_hist, int lane, int k) {
+__device__ __forceinline__ void flush_warp(cnt_t* cnt, uint32_t* cta_hist, int lane, int k) {
   __syncwarp();
+  if (CL_HIST_U8) {
+    // row r = bins 4r..4r+3 of all 32 lanes (32 words); lane takes rows lane, lane + 32.
+    // Byte lanes are summed pairwise in 16-bit halves (32 * 255 < 65536).
+    const uint4* w4 = reinterpret_cast<const uint4*>(cnt);
+    for (int r = lane; 4 * r < k; r += 32) {
+      uint32_t s02 = 0, s13 = 0;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const uint4 w = w4[r * 8 + ((m + lane) & 7)];  // staggered: 4-way, not 32-way
+        s02 += (w.x & 0x00ff00ffu) + (w.y & 0x00ff00ffu) + (w.z & 0x00ff00ffu) + (w.w & 0x00ff00ffu);
+        s13 += ((w.x >> 8) & 0x00ff00ffu) + ((w.y >> 8) & 0x00ff00ffu) +
+               ((w.z >> 8) & 0x00ff00ffu) + ((w.w >> 8) & 0x00ff00ffu);
+      }
+      const uint32_t c[4] = {s02 & 0xffffu, s13 & 0xffffu, s02 >> 16, s13 >> 16};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (c[e] && 4 * r + e < k) atomicAdd(cta_hist + 4 * r + e, c[e]);
+    }
+    __syncwarp();
+    uint4* c4 = reinterpret_cast<uint4*>(cnt);
+    for (int i = lane; i < ((k + 3) / 4) * 8; i += 32) c4[i] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    return;
+  }
+  constexpr int kRow4 = kBinStride / 16;  // uint4 per bin row (32 lanes' counters)
   for (int b = lane; b < k; b += 32) {
     const uint4* row = reinterpret_cast<const uint4*>(cnt + b * 32);
     uint32_t sum = 0;
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const uint4 w = row[(m + (lane >> 1)) & 3];
-      sum += (w.x & 0xffffu) + (w.x >> 16) + (w.y & 0xffffu) + (w.y >> 16) + (w.z & 0xffffu) +
-             (w.z >> 16) + (w.w & 0xffffu) + (w.w >> 16);
+    for (int m = 0; m < kRow4; ++m) {
+      const uint4 w = row[(m + (lane >> 1)) % kRow4];
+      sum += word_sum(w.x) + word_sum(w.y) + word_sum(w.z) + word_sum(w.w);
     }
     if (sum) atomicAdd(cta_hist + b, sum);
   }
   __syncwarp();
   uint4* c4 = reinterpret_cast<uint4*>(cnt);
-  for (int i = lane; i < k * 32 * 2 / 16; i += 32) c4[i] = make_uint4(0, 0, 0, 0);
+  for (int i = lane; i < k * kBinStride / 16; i += 32) c4[i] = make_uint4(0, 0, 0, 0);
   __syncwarp();
 }
 
@@ -375,7 +433,7 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
                          int range_mode, double fixed_lo, double fixed_hi, int k,
                          const double* __restrict__ d_range, unsigned long long* d_counts) {
   extern __shared__ __align__(128) unsigned char smem[];
-  uint16_t* counters = reinterpret_cast<uint16_t*>(smem);
+  cnt_t* counters = reinterpret_cast<cnt_t*>(smem);
   unsigned char* ring = smem + kCounterBytes;
   uint32_t* cta_hist = reinterpret_cast<uint32_t*>(ring + size_t(kStages) * kChunkBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(cta_hist + kLaneBins);
@@ -431,17 +489,18 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
   }
 
   // ---------------- consumer warps ----------------
-  uint16_t* cnt = counters + warp * kLaneBins * 32 + lane;  // cnt[bin * 32]
+  // this lane's counter base: bin b's counter is at lane_base + cofs(b)
+  unsigned char* lane_base = reinterpret_cast<unsigned char*>(counters + warp * kLaneBins * 32) +
+                             lane * (CL_HIST_U8 ? 4 : 2);
 
   if (blockIdx.x == 0 && warp == 0) {
     for (uint64_t i = lane; i < head; i += 32)
-      if (sampled<MODE>(g0 + i, stride)) cnt[bin_f32(v[i], p, FIXED) * 32] += 1;
+      if (sampled<MODE>(g0 + i, stride)) cref(lane_base, bin_f32(v[i], p, FIXED)) += 1;
     for (uint64_t i = head + body_n + lane; i < n; i += 32)
-      if (sampled<MODE>(g0 + i, stride)) cnt[bin_f32(v[i], p, FIXED) * 32] += 1;
+      if (sampled<MODE>(g0 + i, stride)) cref(lane_base, bin_f32(v[i], p, FIXED)) += 1;
   }
 
-  // byte address of this lane's counter for bin 0; bin b lives at + b*64
-  const uint32_t cbase = smem_u32(counters + warp * kLaneBins * 32 + lane);
+  const uint32_t cbase = smem_u32(lane_base);
   // strided sampling (MODE != 0): residue of this lane's first sample index in the
   // current chunk, advanced incrementally (no per-sample 64-bit modulo)
   const uint64_t lane_off = 4ull * static_cast<uint64_t>(warp * 32 + lane);
@@ -462,9 +521,9 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
     const int valid4 = static_cast<int>(umin64(kChunkFloats, body_n - off) / 4);
     if (MODE == 0 && !FIXED && valid4 == kChunkFloats / 4) {
       // ---- hot path: full chunk, every element sampled ----
-      float val[16];
+      float val[kLaneSamples];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < kLaneF4; ++j) {
         const float4 q = tile[j * (kHistWarps * 32) + warp * 32 + lane];
         val[4 * j] = q.x;
         val[4 * j + 1] = q.y;
@@ -473,17 +532,17 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
-      int bin[16];
+      int bin[kLaneSamples];
       bool any_slow = p.exact_only != 0;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
+      for (int e = 0; e < kLaneSamples; ++e) {
         bool sl;
         bin[e] = bin_fast<false>(val[e], p, &sl);
         any_slow |= sl;
       }
       if (__any_sync(0xffffffffu, any_slow)) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
+        for (int e = 0; e < kLaneSamples; ++e) {
           bool sl;
           bin_fast<false>(val[e], p, &sl);
           if (sl || p.exact_only)
@@ -493,17 +552,27 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
       // pairwise read-modify-write: both counters loaded, then stored in order with
       // the second carrying the pair's duplicate
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
+      for (int g = 0; g < kLaneSamples / 2; ++g) {
         const int b0 = bin[2 * g], b1 = bin[2 * g + 1];
-        const uint32_t a0 = cbase + (static_cast<uint32_t>(b0) << 6);
-        const uint32_t a1 = cbase + (static_cast<uint32_t>(b1) << 6);
+        const uint32_t a0 = cbase + cofs(static_cast<uint32_t>(b0));
+        const uint32_t a1 = cbase + cofs(static_cast<uint32_t>(b1));
         uint32_t v0, v1;
-        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
-        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
+        if (CL_HIST_U8) {
+          asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
+          asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
+        } else {
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
+        }
         v1 += 1u + (b0 == b1 ? 1u : 0u);
         v0 += 1u;
-        asm volatile("st.shared.u16 [%0], %1;" ::"r"(a0), "h"(static_cast<uint16_t>(v0)) : "memory");
-        asm volatile("st.shared.u16 [%0], %1;" ::"r"(a1), "h"(static_cast<uint16_t>(v1)) : "memory");
+        if (CL_HIST_U8) {
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a0), "r"(v0) : "memory");
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a1), "r"(v1) : "memory");
+        } else {
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(a0), "h"(static_cast<uint16_t>(v0)) : "memory");
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(a1), "h"(static_cast<uint16_t>(v1)) : "memory");
+        }
       }
       if (++since_flush == kFlushChunks) {
         flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
@@ -511,11 +580,11 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
       }
       continue;
     }
-    float val[16];
+    float val[kLaneSamples];
     uint32_t inc = 0;  // bit e: sample e is valid and sampled
     uint64_t r_j = r_chunk;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kLaneF4; ++j) {
       const int idx = j * (kHistWarps * 32) + warp * 32 + lane;
       float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
       if (idx < valid4) {
@@ -536,13 +605,13 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
       // at most one sample -- pick it with selects, then one predicated bin + RMW per
       // float4, in order (no dynamic register indexing, no data-dependent loops)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < kLaneF4; ++j) {
         const uint32_t mj = (inc >> (4 * j)) & 0xfu;
         const float v = (mj & 1u) ? val[4 * j] : (mj & 2u) ? val[4 * j + 1]
                                                 : (mj & 4u) ? val[4 * j + 2] : val[4 * j + 3];
         if (mj) {
           const int b = bin_f32(v, p, FIXED);
-          cnt[b * 32] = static_cast<uint16_t>(cnt[b * 32] + 1u);
+          cref(lane_base, b) = static_cast<cnt_t>(cref(lane_base, b) + 1u);
         }
       }
       if (++since_flush == kFlushChunks) {
@@ -552,10 +621,10 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
       continue;
     }
 
-    int bin[16];
+    int bin[kLaneSamples];
     uint32_t slow = 0;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
+    for (int e = 0; e < kLaneSamples; ++e) {
       bool sl;
       bin[e] = bin_fast<FIXED>(val[e], p, &sl);
       slow |= (sl ? 1u : 0u) << e;
@@ -564,25 +633,26 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
     if (p.exact_only) slow = inc;
     if (__any_sync(0xffffffffu, slow != 0)) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e)
+      for (int e = 0; e < kLaneSamples; ++e)
         if (slow & (1u << e)) bin[e] = bin_index_exact(static_cast<double>(val[e]), p.lo, p.width, p.k);
     }
 #pragma unroll
-    for (int e = 0; e < 16; ++e)
+    for (int e = 0; e < kLaneSamples; ++e)
       if (!(inc & (1u << e))) bin[e] = 0;  // +0 on bin 0: harmless in the grouped RMW
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
+    for (int g = 0; g < kLaneF4; ++g) {
       const int b0 = bin[4 * g], b1 = bin[4 * g + 1], b2 = bin[4 * g + 2], b3 = bin[4 * g + 3];
       const uint32_t i0 = (inc >> (4 * g)) & 1u, i1 = (inc >> (4 * g + 1)) & 1u;
       const uint32_t i2 = (inc >> (4 * g + 2)) & 1u, i3 = (inc >> (4 * g + 3)) & 1u;
-      const uint32_t v0 = cnt[b0 * 32], v1 = cnt[b1 * 32], v2 = cnt[b2 * 32], v3 = cnt[b3 * 32];
+      const uint32_t v0 = cref(lane_base, b0), v1 = cref(lane_base, b1);
+      const uint32_t v2 = cref(lane_base, b2), v3 = cref(lane_base, b3);
       const uint32_t n1 = v1 + i1 + (b1 == b0 ? i0 : 0u);
       const uint32_t n2 = v2 + i2 + (b2 == b0 ? i0 : 0u) + (b2 == b1 ? i1 : 0u);
       const uint32_t n3 = v3 + i3 + (b3 == b0 ? i0 : 0u) + (b3 == b1 ? i1 : 0u) + (b3 == b2 ? i2 : 0u);
-      cnt[b0 * 32] = static_cast<uint16_t>(v0 + i0);
-      cnt[b1 * 32] = static_cast<uint16_t>(n1);
-      cnt[b2 * 32] = static_cast<uint16_t>(n2);
-      cnt[b3 * 32] = static_cast<uint16_t>(n3);
+      cref(lane_base, b0) = static_cast<cnt_t>(v0 + i0);
+      cref(lane_base, b1) = static_cast<cnt_t>(n1);
+      cref(lane_base, b2) = static_cast<cnt_t>(n2);
+      cref(lane_base, b3) = static_cast<cnt_t>(n3);
     }
     if (++since_flush == kFlushChunks) {
       flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);

@@ -272,3 +272,26 @@ def test_strided_unsampled_outliers(cuda, port):
             counts, lo, hi, _ = _device_counts(cuda, w, 256, s)
             oc, olo, ohi, _ = port.histogram(w, 256, 1e-8, s)
             assert (counts == oc).all() and lo == olo and hi == ohi
+
+
+@pytest.mark.parametrize("stride", [1, 3, 8])
+def test_counter_flush_no_overflow(cuda, port, stride):
+    """Lane counters are narrow (8-bit, flushed every 15 chunks): inputs large enough for
+    many flushes per CTA, with almost every sample in one bin, must still count exactly
+    (full-chunk hot path at stride 1, the general / sparse paths at strides 3 and 8)."""
+    n = (1 << 26) + 12345  # ~55 chunks per CTA at the default geometry, ragged tail
+    v = np.full(n, 0.25, np.float32)
+    rng = np.random.default_rng(stride)
+    idx = rng.integers(0, n, 4096)
+    v[idx] = rng.uniform(-1.0, 1.0, idx.size).astype(np.float32)
+    counts, lo, hi, _ = _device_counts(cuda, v, 256, stride)
+    oc, olo, ohi, on = port.histogram(v, 256, 1e-8, stride)
+    assert lo == olo and hi == ohi
+    assert (counts == oc).all() and int(counts.sum()) == on
+
+
+def test_counter_flush_degenerate_range(cuda):
+    """Constant input (degenerate range, everything in bin 0) at 64M samples."""
+    n = 1 << 26
+    counts, *_ = _device_counts(cuda, np.full(n, -2.5, np.float32), 256, 1)
+    assert counts[0] == n and counts[1:].sum() == 0

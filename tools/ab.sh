@@ -1,5 +1,14 @@
+# A/B timing: each variant library in $LIBS ("default" = the in-tree build) on $CONFIG,
+# then the GPU parity suite against the in-tree build.
 set -e
 for i in 1 2; do
-for c in 8 0; do CL_SCAN_CFG=$c python tools/profile_stages.py --reps 30 --median 2>&1 | grep cfg; done
+for l in ${LIBS:-default}; do
+  if [ "$l" = default ]; then unset CHUNKLAB_LIB; else export CHUNKLAB_LIB=$l; fi
+  for c in ${CFGS:-default}; do
+    if [ "$c" = default ]; then unset CL_SCAN_CFG; else export CL_SCAN_CFG=$c; fi
+    echo -n "lib=$l "; python tools/profile_stages.py --config ${CONFIG:-C3} --reps 30 --median 2>&1 | grep cfg
+  done
 done
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+done
+unset CHUNKLAB_LIB CL_SCAN_CFG
+[ -n "$NOTEST" ] || timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
