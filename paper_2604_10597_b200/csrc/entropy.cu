@@ -310,6 +310,22 @@ __device__ __forceinline__ uint32_t cofs(uint32_t b) {
   if (CL_HIST_U8) return (b & ~3u) * 32u + (b & 3u);
   return b * 64u;
 }
+// Counter byte offset from the start of the counter block, straight from the bits of the
+// magic-number rounded t = n + 1.5*2^23 (bits 0x4B400000 + n, 0 <= n < 256, so n's bits
+// are the low byte and the exponent bits lie above it): (n & ~3)*32 + (n & 3) plus the
+// lane's word and the warp's block (wl = warp*8192 + lane*4) -- LOP3, LOP3, IMAD.
+__device__ __forceinline__ uint32_t cofs_from_tbits(uint32_t tb, uint32_t wl) {
+  uint32_t o;
+  asm("{\n"
+      ".reg .b32 hi, lo;\n"
+      "and.b32 hi, %1, 0xfc;\n"
+      "lop3.b32 lo, %1, 3, %2, 0xea;\n"  // (tb & 3) | wl: LUT (a & b) | c
+      "mad.lo.u32 %0, hi, 32, lo;\n"
+      "}\n"
+      : "=r"(o)
+      : "r"(tb), "r"(wl));
+  return o;
+}
 __device__ __forceinline__ cnt_t& cref(unsigned char* lane_base, int b) {
   return *reinterpret_cast<cnt_t*>(lane_base + cofs(static_cast<uint32_t>(b)));
 }
@@ -532,44 +548,71 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
-      int bin[kLaneSamples];
-      bool any_slow = p.exact_only != 0;
+      if constexpr (CL_HIST_U8 != 0) {
+        // t bits carry the bin (0x4B400000 + n); near-edge samples get the exact bin's bits
+        uint32_t tb[kLaneSamples];
+        bool any_slow = p.exact_only != 0;
 #pragma unroll
-      for (int e = 0; e < kLaneSamples; ++e) {
-        bool sl;
-        bin[e] = bin_fast<false>(val[e], p, &sl);
-        any_slow |= sl;
-      }
-      if (__any_sync(0xffffffffu, any_slow)) {
+        for (int e = 0; e < kLaneSamples; ++e) {
+          const float x = fmaf(val[e], p.s_f, p.c_f);
+          const float t = x + 12582912.0f;
+          any_slow |= !(fabsf(x - (t - 12582912.0f)) <= p.thr);
+          tb[e] = __float_as_uint(t);
+        }
+        if (__any_sync(0xffffffffu, any_slow)) {
+#pragma unroll
+          for (int e = 0; e < kLaneSamples; ++e) {
+            bool sl;
+            bin_fast<false>(val[e], p, &sl);
+            if (sl || p.exact_only)
+              tb[e] = 0x4B400000u + static_cast<uint32_t>(bin_index_exact(
+                                        static_cast<double>(val[e]), p.lo, p.width, p.k));
+          }
+        }
+        // the counter block starts at dynamic shared offset 0, so an offset is an address
+        // and the loads / stores below are LDS/STS [R + UR(base)] with no add
+        unsigned char* cblk = reinterpret_cast<unsigned char*>(counters);
+        const uint32_t wl = static_cast<uint32_t>(warp) * (kLaneBins * 32) + lane * 4u;
+#pragma unroll
+        for (int g = 0; g < kLaneSamples / 2; ++g) {
+          // plain accesses: the offsets may alias, so the compiler keeps this order
+          const uint32_t o0 = cofs_from_tbits(tb[2 * g], wl);
+          const uint32_t o1 = cofs_from_tbits(tb[2 * g + 1], wl);
+          const uint32_t v0 = cblk[o0];
+          const uint32_t v1 = cblk[o1];
+          cblk[o0] = static_cast<unsigned char>(v0 + 1u);
+          cblk[o1] = static_cast<unsigned char>(v1 + 1u + (o0 == o1 ? 1u : 0u));
+        }
+      } else {
+        int bin[kLaneSamples];
+        bool any_slow = p.exact_only != 0;
 #pragma unroll
         for (int e = 0; e < kLaneSamples; ++e) {
           bool sl;
-          bin_fast<false>(val[e], p, &sl);
-          if (sl || p.exact_only)
-            bin[e] = bin_index_exact(static_cast<double>(val[e]), p.lo, p.width, p.k);
+          bin[e] = bin_fast<false>(val[e], p, &sl);
+          any_slow |= sl;
         }
-      }
-      // pairwise read-modify-write: both counters loaded, then stored in order with
-      // the second carrying the pair's duplicate
+        if (__any_sync(0xffffffffu, any_slow)) {
 #pragma unroll
-      for (int g = 0; g < kLaneSamples / 2; ++g) {
-        const int b0 = bin[2 * g], b1 = bin[2 * g + 1];
-        const uint32_t a0 = cbase + cofs(static_cast<uint32_t>(b0));
-        const uint32_t a1 = cbase + cofs(static_cast<uint32_t>(b1));
-        uint32_t v0, v1;
-        if (CL_HIST_U8) {
-          asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
-          asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
-        } else {
+          for (int e = 0; e < kLaneSamples; ++e) {
+            bool sl;
+            bin_fast<false>(val[e], p, &sl);
+            if (sl || p.exact_only)
+              bin[e] = bin_index_exact(static_cast<double>(val[e]), p.lo, p.width, p.k);
+          }
+        }
+        // pairwise read-modify-write: both counters loaded, then stored in order with
+        // the second carrying the pair's duplicate
+#pragma unroll
+        for (int g = 0; g < kLaneSamples / 2; ++g) {
+          const int b0 = bin[2 * g], b1 = bin[2 * g + 1];
+          const uint32_t a0 = cbase + cofs(static_cast<uint32_t>(b0));
+          const uint32_t a1 = cbase + cofs(static_cast<uint32_t>(b1));
+          uint32_t v0, v1;
           asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
           asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
-        }
-        v1 += 1u + (b0 == b1 ? 1u : 0u);
-        v0 += 1u;
-        if (CL_HIST_U8) {
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a0), "r"(v0) : "memory");
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a1), "r"(v1) : "memory");
-        } else {
+          v1 += 1u + (b0 == b1 ? 1u : 0u);
+          v0 += 1u;
           asm volatile("st.shared.u16 [%0], %1;" ::"r"(a0), "h"(static_cast<uint16_t>(v0)) : "memory");
           asm volatile("st.shared.u16 [%0], %1;" ::"r"(a1), "h"(static_cast<uint16_t>(v1)) : "memory");
         }
