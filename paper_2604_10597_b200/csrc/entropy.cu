@@ -868,10 +868,12 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(DecideArgs a, cl_decis
       terms[threadIdx.x] = t;
       __syncthreads();
       if (threadIdx.x == 0) {
-        // raw -= p*log(p+eps) in bin order (entropy.hpp:154-156)
+        // raw -= p*log(p+eps) in bin order (entropy.hpp:154-156).  Empty bins hold +0.0
+        // and raw - (+0.0) == raw bit for bit, so they are subtracted too: the chain reads
+        // shared memory only (no per-bin global count load and branch)
         const int m = min(kThreads, a.k - base);
-        for (int i = 0; i < m; ++i)
-          if (a.counts[base + i] != 0ull) raw = __dsub_rn(raw, terms[i]);
+#pragma unroll 8
+        for (int i = 0; i < m; ++i) raw = __dsub_rn(raw, terms[i]);
       }
       __syncthreads();
     }
