@@ -786,8 +786,8 @@ __device__ __forceinline__ void pair_box(const unsigned char* st, float* ydst, i
 }
 
 // pair_box for a full box (valid == BOX), software-pipelined by one 4-timestep group:
-// group j+1's serial prologue (LDS of u / delta, bias add, softplus -- one MUFU then a
-// 9-deep FFMA2 chain -- and the partner-lane shuffle) is issued between group j's
+// group j+1's serial prologue (LDS of u / delta / z, bias add, softplus -- one MUFU then
+// a 9-deep FFMA2 chain -- the partner-lane shuffle and the SiLU(z) gate) is issued between group j's
 // exponentials and its recurrence, so its latency hides under group j's MUFU work
 // instead of stalling the MUFU pipe at every group boundary.  Same operations on the
 // same values as pair_box, so the outputs are bit-identical.
@@ -803,7 +803,7 @@ __device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* yd
   const unsigned char* sC = sB + kN * 4;
   const f2_t bias2 = pk(bias, bias);
   // prologue of group j: dt (4 timesteps, softplus'd), x = dt*u, and this lane's u pair
-  auto prep = [&](int j, float (&dt)[4], float (&xs)[4], f2_t& u2) {
+  auto prep = [&](int j, float (&dt)[4], float (&xs)[4], f2_t& u2, f2_t& g2) {
     const int off = Geo<BOX>::swz(r, j);
     const float4 u4 = *reinterpret_cast<const float4*>(st + off);
     const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
@@ -817,10 +817,14 @@ __device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* yd
     upk(x01, xs[0], xs[1]);
     upk(x23, xs[2], xs[3]);
     u2 = hf ? pk(u4.z, u4.w) : pk(u4.x, u4.y);
+    if (HZ) {
+      const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
+      g2 = silu2(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y));
+    }
   };
   float dt[4], xs[4];
-  f2_t u2;
-  prep(0, dt, xs, u2);
+  f2_t u2, g2 = 0ull;
+  prep(0, dt, xs, u2, g2);
 #pragma unroll
   for (int j = 0; j < kG; ++j) {
     f2_t dA[4][kP];
@@ -835,8 +839,8 @@ __device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* yd
       }
     }
     float ndt[4], nxs[4];
-    f2_t nu2 = 0ull;
-    if (j + 1 < kG) prep(j + 1, ndt, nxs, nu2);
+    f2_t nu2 = 0ull, ng2 = 0ull;
+    if (j + 1 < kG) prep(j + 1, ndt, nxs, nu2, ng2);
     float yp[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -862,11 +866,7 @@ __device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* yd
     const f2_t give = hf ? pk(yp[0], yp[1]) : pk(yp[2], yp[3]);
     const f2_t ysum = add2(keep, shfl_xor2(give, 1));
     f2_t yo = fma2(pk(Dc, Dc), u2, ysum);
-    if (HZ) {
-      const float4 z4 =
-          *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + Geo<BOX>::swz(r, j));
-      yo = mul2(yo, silu2(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y)));
-    }
+    if (HZ) yo = mul2(yo, g2);
     if (ydst) {
       float y0, y1;
       upk(yo, y0, y1);
@@ -879,6 +879,7 @@ __device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* yd
         xs[k] = nxs[k];
       }
       u2 = nu2;
+      g2 = ng2;
     }
   }
 }
@@ -1163,21 +1164,27 @@ struct ScanCfg {
   int kind, box, warps, stages;
 };
 constexpr ScanCfg kCfgs[] = {
-    {kWarpSpecPair, 16, 14, 2},  // 14 consumer + 2 producer warps per SM (C3, C4)
+    // 12 consumer + 2 producer warps per SM (C3, C4): three consumers on every SM
+    // sub-partition, so every warp gets the same share of its SMSP's MUFU quarter.
+    // Measured at C3 (scan ms): 12 consumers 1.357; 13: 1.373; 14 (4/4/3/3 per SMSP):
+    // 1.404; 12 x 3 stages 1.371; 8 consumers 1.497; 12 with 1 producer 1.572, with 3
+    // producers 1.371.
+    {kWarpSpecPair, 16, 12, 2},
     {kRowSeq, 32, 4, 3},         // 32-row tiles, self-fed TMA rings
     {kRowSeq, 16, 8, 3},
     {kRowSeq, 16, 7, 3},
     // few 16-row tiles (C1: 96, C2: 128): fewer consumers per CTA so the tiles spread over
-    // all SMs instead of packing 14 to an SM (one producer, deeper ring)
+    // all SMs instead of packing 12 to an SM (one producer, deeper ring)
     {kWarpSpecPair, 16, 1, 4},
     {kWarpSpecPair, 16, 2, 4},
     {kWarpSpecPair, 16, 4, 4},
     {kWarpSpecPair, 16, 7, 3},
-    {kWarpSpecPairNoPipe, 16, 14, 2},  // 8: row 0 without the group software pipeline (A/B)
+    {kWarpSpecPairNoPipe, 16, 12, 2},  // 8: row 0 without the group software pipeline (A/B)
+    {kWarpSpecPair, 16, 14, 2},        // 9: 14 consumers (the previous default)
 };
 constexpr int kDefaultCfg = 0;
 
-// producers per CTA: two keep up with 14 consumers, one with up to 7
+// producers per CTA: two keep up with 12-14 consumers (one feeding 12 costs +16%), one with up to 7
 template <int WARPS>
 constexpr int producers_for() {
   return WARPS >= 8 ? 2 : 1;
@@ -1194,9 +1201,9 @@ int grid_for(int n_tiles, int warps, int num_sms) {
   return max_useful < num_sms ? (max_useful < 1 ? 1 : max_useful) : num_sms;
 }
 
-template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, bool PIPE = true>
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, bool PIPE = true, int NP = 0>
 cudaError_t launch_ws(const CUtensorMap (&m)[6], const TmaArgs& t, int num_sms, cudaStream_t s) {
-  constexpr int kProducers = producers_for<WARPS>();
+  constexpr int kProducers = NP > 0 ? NP : producers_for<WARPS>();
   auto kern = rowpair_ws_kernel<BOX, WARPS, STAGES, SP, HZ, kProducers, PIPE>;
   const size_t smem = size_t(WARPS) * STAGES * GeoP<BOX>::kStageBytes + 1024 +
                       size_t(WARPS) * STAGES * (16 + 8);
@@ -1238,7 +1245,7 @@ cudaError_t dispatch(bool sp, bool hz, const CUtensorMap (&m)[6], const TmaArgs&
 
 // CL_SCAN_CFG=<row> forces a kCfgs row (experiments); otherwise the warp-specialised
 // kernel with the fewest consumers per CTA that still puts every 16-row tile on its own
-// SM (14 consumers once there are >= 7 tiles per SM's worth).
+// SM (12 consumers once there are more than 7 tiles per SM).
 int scan_cfg_index(uint64_t pair_tiles, int num_sms) {
   static const int forced = [] {
     const char* e = getenv("CL_SCAN_CFG");
@@ -1252,7 +1259,7 @@ int scan_cfg_index(uint64_t pair_tiles, int num_sms) {
   if (per_sm <= 2) return 5;
   if (per_sm <= 4) return 6;
   if (per_sm <= 7) return 7;
-  return kDefaultCfg;
+  return kDefaultCfg;  // 12 consumers
 }
 
 }  // namespace
@@ -1332,10 +1339,11 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       case 6: e = dispatch<true, 16, 4, 4>(sp, hz, m, t, n, s); break;
       case 7: e = dispatch<true, 16, 7, 3>(sp, hz, m, t, n, s); break;
       case 8:
-        e = sp && hz ? launch_ws<16, 14, 2, true, true, false>(m, t, n, s)
-                     : dispatch<true, 16, 14, 2>(sp, hz, m, t, n, s);
+        e = sp && hz ? launch_ws<16, 12, 2, true, true, false>(m, t, n, s)
+                     : dispatch<true, 16, 12, 2>(sp, hz, m, t, n, s);
         break;
-      default: e = dispatch<true, 16, 14, 2>(sp, hz, m, t, n, s); break;
+      case 9: e = dispatch<true, 16, 14, 2>(sp, hz, m, t, n, s); break;
+      default: e = dispatch<true, 16, 12, 2>(sp, hz, m, t, n, s); break;
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     ++ctx->launches;
