@@ -573,10 +573,48 @@ def e2e_measure(torch, dist, world, device, x, run_prefill, L, global_batch, ste
         t = torch.tensor([ms], device=device, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    pcie = pcie_bound(torch, host["u"], bufs[0]["u"], h_out, outs[0], h2d, d2h, ms)
     del bufs, outs
     return {"value": global_batch * L / (ms / 1e3), "unit": "tokens/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms,
-            "steps": steps, "pipeline": "H2D(i+1) | prefill(i) | D2H(i-1) on 3 streams"}
+            "steps": steps, "pipeline": "H2D(i+1) | prefill(i) | D2H(i-1) on 3 streams",
+            "pcie": pcie}
+
+
+def pcie_bound(torch, h_src, d_dst, h_dst, d_src, h2d, d2h, ms, reps=3):
+    """The e2e pipeline's roofline: host<->device copy bandwidth measured here (pinned, CUDA
+    events) for H2D alone and for H2D + D2H at once (the link is not fully duplex on these
+    boxes), and the per-step floor it implies -- the readback overlapped with the upload,
+    the rest of the upload alone."""
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    nbytes = h_src.numel() * 4
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps / 1e3
+
+    def both():
+        with torch.cuda.stream(s1):
+            d_dst.copy_(h_src, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_dst.copy_(d_src, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s1)
+        torch.cuda.current_stream().wait_stream(s2)
+
+    h2d_bw = nbytes / timed(lambda: d_dst.copy_(h_src, non_blocking=True))
+    dup_bw = nbytes / timed(both)
+    # D2H fully overlapped with part of the upload at the duplex rate, the rest at H2D rate
+    overlap = min(d2h, h2d)
+    floor_s = overlap / dup_bw + (h2d - overlap) / h2d_bw
+    return {"h2d_gbs": h2d_bw / 1e9, "duplex_gbs_each": dup_bw / 1e9,
+            "floor_ms": floor_s * 1e3, "frac": floor_s * 1e3 / ms}
 
 
 if __name__ == "__main__":
