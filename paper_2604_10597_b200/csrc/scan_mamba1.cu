@@ -688,6 +688,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 // y staging buffer, proxy fence and TMA store saved another ~3%.
 // ---------------------------------------------------------------------------
 constexpr int kRowsP = 16;
+#ifndef CL_PROD_SLEEP_NS
+#define CL_PROD_SLEEP_NS 32
+#endif
 
 template <int BOX>
 struct GeoP {
@@ -978,7 +981,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
           issued = true;
         }
       }
-      if (!__any_sync(0xffffffffu, issued)) __nanosleep(32);
+      if (!__any_sync(0xffffffffu, issued)) __nanosleep(CL_PROD_SLEEP_NS);
     }
     return;
   }
@@ -1167,8 +1170,9 @@ constexpr ScanCfg kCfgs[] = {
     // 12 consumer + 2 producer warps per SM (C3, C4): three consumers on every SM
     // sub-partition, so every warp gets the same share of its SMSP's MUFU quarter.
     // Measured at C3 (scan ms): 12 consumers 1.357; 13: 1.373; 14 (4/4/3/3 per SMSP):
-    // 1.404; 12 x 3 stages 1.371; 8 consumers 1.497; 12 with 1 producer 1.572, with 3
-    // producers 1.371.
+    // 1.404 -- the uneven sub-partitions made warps wait on each other's carries (ncu:
+    // carry-spin samples 2.7% -> 0.3%); 16 (capped at 96 registers, spills): 1.726;
+    // 12 x 3 stages 1.371; 8 consumers 1.497; 12 with 1 producer 1.572, with 3: 1.371.
     {kWarpSpecPair, 16, 12, 2},
     {kRowSeq, 32, 4, 3},         // 32-row tiles, self-fed TMA rings
     {kRowSeq, 16, 8, 3},
