@@ -424,20 +424,6 @@ __device__ __forceinline__ void flush_warp(cnt_t* cnt, uint32_t* cta_hist, int l
   __syncwarp();
 }
 
-// Which of 4 consecutive samples starting at global index gi are taken (gi % stride ==
-// 0), given r = gi % stride: bit e set iff (r + e) % stride == 0.
-__device__ __forceinline__ uint32_t sample_mask4(uint64_t r, uint64_t stride) {
-  const uint64_t e0 = r == 0 ? 0 : stride - r;  // first sampled offset
-  uint32_t m = e0 < 4 ? 1u << e0 : 0u;
-  if (stride < 4) {  // kernel argument: warp-uniform
-#pragma unroll
-    for (uint64_t k = 1; k < 4; ++k) {
-      const uint64_t e = e0 + k * stride;
-      m |= e < 4 ? 1u << e : 0u;
-    }
-  }
-  return m;
-}
 __device__ __forceinline__ uint64_t add_mod(uint64_t r, uint64_t d, uint64_t stride) {
   r += d;  // r, d < stride
   return r >= stride ? r - stride : r;
@@ -519,12 +505,12 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
   const uint32_t cbase = smem_u32(lane_base);
   // strided sampling (MODE != 0): residue of this lane's first sample index in the
   // current chunk, advanced incrementally (no per-sample 64-bit modulo)
-  const uint64_t lane_off = 4ull * static_cast<uint64_t>(warp * 32 + lane);
-  uint64_t r_chunk = 0, step_chunk = 0, step_j = 0;
+  // strided sampling (MODE != 0): residue of the chunk's first element's global index,
+  // advanced incrementally (no per-chunk 64-bit modulo)
+  uint64_t r_chunk = 0, step_chunk = 0;
   if (MODE != 0) {
-    r_chunk = (g0 + head + static_cast<uint64_t>(blockIdx.x) * kChunkFloats + lane_off) % stride;
+    r_chunk = (g0 + head + static_cast<uint64_t>(blockIdx.x) * kChunkFloats) % stride;
     step_chunk = (static_cast<uint64_t>(gridDim.x) * kChunkFloats) % stride;
-    step_j = (4ull * kHistWarps * 32) % stride;
   }
   uint32_t it = 0, since_flush = 0;
   for (uint64_t c = blockIdx.x; c < n_chunks;
@@ -623,37 +609,33 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
       }
       continue;
     }
-    float val[kLaneSamples];
-    uint32_t inc = 0;  // bit e: sample e is valid and sampled
-    uint64_t r_j = r_chunk;
+    if (MODE != 0) {
+      // ---- strided sampling: gather the chunk's samples, sample m to lane m % (32W) ----
+      // Sample m sits at chunk offset first + m*stride, so every lane holds a sample (no
+      // lane idles on a float4 without one, as a float4-per-lane split does at stride 8);
+      // at most kLaneSamples/2 per lane (stride >= 2).
+      const uint64_t valid = static_cast<uint64_t>(valid4) * 4u;
+      const uint64_t first = r_chunk == 0 ? 0 : stride - r_chunk;
+      const float* ringf = reinterpret_cast<const float*>(tile);
+      constexpr int kMaxPer = kLaneSamples / 2;
+      const uint32_t m0 = static_cast<uint32_t>(warp * 32 + lane);
+      float sv[kMaxPer];
+      uint32_t have = 0;
 #pragma unroll
-    for (int j = 0; j < kLaneF4; ++j) {
-      const int idx = j * (kHistWarps * 32) + warp * 32 + lane;
-      float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (idx < valid4) {
-        q = tile[idx];
-        inc |= (MODE == 0 ? 0xfu : sample_mask4(r_j, stride)) << (4 * j);
+      for (int t = 0; t < kMaxPer; ++t) {
+        const uint64_t o = first + static_cast<uint64_t>(m0 + t * kHistWarps * 32) * stride;
+        sv[t] = 0.f;
+        if (o < valid) {
+          sv[t] = ringf[o];
+          have |= 1u << t;
+        }
       }
-      if (MODE != 0) r_j = add_mod(r_j, step_j, stride);
-      val[4 * j] = q.x;
-      val[4 * j + 1] = q.y;
-      val[4 * j + 2] = q.z;
-      val[4 * j + 3] = q.w;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + s);
-
-    if (MODE != 0 && stride >= 4) {
-      // sparse sampling (e.g. the sampled-histogram policy's stride 8): each float4 holds
-      // at most one sample -- pick it with selects, then one predicated bin + RMW per
-      // float4, in order (no dynamic register indexing, no data-dependent loops)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
 #pragma unroll
-      for (int j = 0; j < kLaneF4; ++j) {
-        const uint32_t mj = (inc >> (4 * j)) & 0xfu;
-        const float v = (mj & 1u) ? val[4 * j] : (mj & 2u) ? val[4 * j + 1]
-                                                : (mj & 4u) ? val[4 * j + 2] : val[4 * j + 3];
-        if (mj) {
-          const int b = bin_f32(v, p, FIXED);
+      for (int t = 0; t < kMaxPer; ++t) {
+        if (have & (1u << t)) {
+          const int b = bin_f32(sv[t], p, FIXED);
           cref(lane_base, b) = static_cast<cnt_t>(cref(lane_base, b) + 1u);
         }
       }
@@ -663,6 +645,25 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
       }
       continue;
     }
+
+    // ---- every element sampled: partial chunk, or the fixed-range mode ----
+    float val[kLaneSamples];
+    uint32_t inc = 0;  // bit e: sample e is valid
+#pragma unroll
+    for (int j = 0; j < kLaneF4; ++j) {
+      const int idx = j * (kHistWarps * 32) + warp * 32 + lane;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (idx < valid4) {
+        q = tile[idx];
+        inc |= 0xfu << (4 * j);
+      }
+      val[4 * j] = q.x;
+      val[4 * j + 1] = q.y;
+      val[4 * j + 2] = q.z;
+      val[4 * j + 3] = q.w;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
 
     int bin[kLaneSamples];
     uint32_t slow = 0;
