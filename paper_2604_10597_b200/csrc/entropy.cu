@@ -943,20 +943,22 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(DecideArgs a, cl_decis
 // per-position raw entropies averaged in position order.
 //
 // Four stream-ordered stages (the multi-GPU protocol inserts its two collectives
-// between them, exactly as for the global histogram):
-//   1. token_minmax: blocks own a tile of kTokTile positions x a share of the channels;
+// between them, exactly as for the global histogram).  fp32 inputs with K <= 256 and
+// 16-byte aligned rows take the lane-per-position kernels further down
+// (token_minmax_lane_kernel, token_hist_lane_kernel); the tiled kernels here serve fp64,
+// K > 256 and unaligned inputs:
+//   1. token_minmax: blocks own a tile of 32 positions (8 x float4) x a share of the channels;
 //      a thread loads 16 contiguous bytes of one channel row per step (a warp covers 4
 //      channel rows x 128 B), keeps per-position min/max + the finite flag, and the
 //      block folds them into trange [2][L] = {-lo, hi} with fp64 atomic max.
 //   2. token_hist: same tiling, per-position bin parameters from trange, an
-//      [kTokTile][K] u32 shared-memory histogram flushed into counts [L][K] (global
+//      [32][K] u32 shared-memory histogram flushed into counts [L][K] (global
 //      atomics straight into counts when the tile does not fit shared memory).
 //   3. token_entropy: a warp per position, estimate_entropy in fp64, bin order.
 //   4. token_finalize: the ordered mean over positions.
 // Channel indices are global (channel_offset + c) so a row-sharded tensor samples the
 // same slice entries as the whole one.
 // ---------------------------------------------------------------------------
-constexpr int kTokTile = 32;  // positions per block tile (8 threads x float4)
 constexpr int kTokMaxSmemHist = 64 * 1024;
 
 template <typename T>
@@ -993,7 +995,7 @@ __device__ __forceinline__ void tok_channel_share(uint64_t channels, uint64_t* c
 }
 
 // thread -> (position group g of 8, channel lane cl of 32); a group is kV positions for
-// vector loads (8 x kV = kTokTile for fp32) or 1 position for scalar loads.
+// vector loads (8 x kV = 32 for fp32) or 1 position for scalar loads.
 template <typename T, int VEC>
 __global__ void __launch_bounds__(kThreads) token_minmax_kernel(const T* __restrict__ v,
                                                                 TokArgs a, double* trange,
@@ -1129,6 +1131,255 @@ __global__ void __launch_bounds__(kThreads) token_hist_kernel(const T* __restric
   for (int i = threadIdx.x; i < kTile * k; i += kThreads) {
     const uint64_t t = tb + i / k;
     if (t < a.length && thist[i]) atomicAdd(counts + t * k + (i % k), thist[i]);
+  }
+}
+
+// ---- fp32 fast path (K <= 256, 16-byte aligned rows): lane-per-position kernels ----
+// The tiled kernels above give every (position, bin) counter to many threads, so each
+// sample is a shared-memory atomic (ATOMS throughput bound).  Here a lane owns positions:
+//   min/max  a lane holds 4 consecutive positions (one float4 per channel row), a warp
+//            streams 512 contiguous bytes of one row per load, the block's 8 warps split
+//            the channel share and fold their ranges in shared memory;
+//   hist     a lane owns ONE position and lane-private 16-bit counters [bin][lane] (16 KB
+//            per warp, no atomics; in-order pairwise read-modify-write as in the global
+//            histogram), a warp reads 128 contiguous bytes of one channel row per load;
+//            the block's 4 warps are summed at the end and added to counts [L][K].
+// Work items are (position tile, channel split) pairs walked grid-stride by resident
+// blocks.  Channels are sampled by global index (channel_offset + c) % stride == 0 (the
+// minmax pass still reads every channel: the finite check covers all values).
+constexpr int kTokMmWarps = 8;              // min/max: warps per block, 128 positions
+constexpr int kTokHWarps = 4;               // hist: warps per block, 32 positions
+#ifndef CL_TOK_MM_ROWS
+#define CL_TOK_MM_ROWS 8
+#endif
+#ifndef CL_TOK_H_UNROLL
+#define CL_TOK_H_UNROLL 24
+#endif
+// Measured at C3 (u 8x4096x8192 as 32768 channels x 8192 positions): min/max 0.31-0.33 ms
+// for 4, 8 or 16 rows per batch; histogram 0.98 / 0.72 / 0.53 / 0.47 / 0.77 ms for 4 / 8 /
+// 16 / 24 / 32 rows (32: 182 registers, 2 blocks per SM).  Loads in flight, not
+// instructions, bound the histogram: a lane reads 4 bytes of a row, a warp 128 bytes.
+constexpr int kTokMmRows = CL_TOK_MM_ROWS;  // min/max: channel rows per batch
+constexpr int kTokHUnroll = CL_TOK_H_UNROLL;  // hist: channel rows per batch (2 in flight)
+constexpr int kTokHMaxPerFlush = 65000;     // u16 counters: flush before overflow
+
+__device__ __forceinline__ void tok_item_split(uint64_t item, uint64_t tiles, uint64_t splits,
+                                               uint64_t channels, uint64_t* tile,
+                                               uint64_t* c0, uint64_t* c1) {
+  *tile = item % tiles;
+  const uint64_t sp = item / tiles;
+  const uint64_t per = (channels + splits - 1) / splits;
+  *c0 = sp * per;
+  *c1 = umin64(channels, *c0 + per);
+}
+
+__global__ void __launch_bounds__(kTokMmWarps * 32) token_minmax_lane_kernel(
+    const float* __restrict__ v, TokArgs a, uint64_t tiles, uint64_t splits, double* trange,
+    double* flag) {
+  __shared__ float s_lo[kTokMmWarps][128], s_hi[kTokMmWarps][128];
+  __shared__ int s_bad;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) s_bad = 0;
+  bool bad = false;
+  for (uint64_t item = blockIdx.x; item < tiles * splits; item += gridDim.x) {
+    uint64_t tile, c0, c1;
+    tok_item_split(item, tiles, splits, a.channels, &tile, &c0, &c1);
+    const uint64_t t0 = tile * 128 + lane * 4;
+    float lo[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+    float hi[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    if (t0 < a.length) {
+      const uint64_t per = (c1 - c0 + kTokMmWarps - 1) / kTokMmWarps;
+      const uint64_t w0 = umin64(c1, c0 + warp * per), w1 = umin64(c1, w0 + per);
+      uint64_t cm = (a.offset + w0) % a.stride;  // (offset + c) % stride, incremental
+      uint64_t c = w0;
+      const float* rp = v + w0 * a.length + t0;
+      for (; c + kTokMmRows <= w1; c += kTokMmRows) {
+        float4 q[kTokMmRows];
+#pragma unroll
+        for (int i = 0; i < kTokMmRows; ++i) {
+          q[i] = __ldcs(reinterpret_cast<const float4*>(rp));
+          rp += a.length;
+        }
+#pragma unroll
+        for (int i = 0; i < kTokMmRows; ++i) {
+          const float x[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+          const bool smp = cm == 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            bad |= !(fabsf(x[e]) <= FLT_MAX);
+            if (smp) {
+              lo[e] = x[e] < lo[e] ? x[e] : lo[e];  // std::min keeps lo unless x < lo
+              hi[e] = hi[e] < x[e] ? x[e] : hi[e];
+            }
+          }
+          if (++cm == a.stride) cm = 0;
+        }
+      }
+      for (; c < w1; ++c) {
+        const float4 q = __ldcs(reinterpret_cast<const float4*>(v + c * a.length + t0));
+        const float x[4] = {q.x, q.y, q.z, q.w};
+        const bool smp = cm == 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          bad |= !(fabsf(x[e]) <= FLT_MAX);
+          if (smp) {
+            lo[e] = x[e] < lo[e] ? x[e] : lo[e];
+            hi[e] = hi[e] < x[e] ? x[e] : hi[e];
+          }
+        }
+        if (++cm == a.stride) cm = 0;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      s_lo[warp][lane * 4 + e] = lo[e];
+      s_hi[warp][lane * 4 + e] = hi[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < 128) {
+      const uint64_t t = tile * 128 + threadIdx.x;
+      float l = s_lo[0][threadIdx.x], h = s_hi[0][threadIdx.x];
+      for (int w = 1; w < kTokMmWarps; ++w) {
+        l = s_lo[w][threadIdx.x] < l ? s_lo[w][threadIdx.x] : l;
+        h = h < s_hi[w][threadIdx.x] ? s_hi[w][threadIdx.x] : h;
+      }
+      if (t < a.length && h >= l) {
+        atomic_max_f64(trange + t, -static_cast<double>(l));
+        atomic_max_f64(trange + a.length + t, static_cast<double>(h));
+      }
+    }
+    __syncthreads();
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0 && s_bad) atomic_max_f64(flag, 1.0);
+}
+
+// Adds the block's 4 warps' counters for its 32 positions into counts [L][K] and clears
+// them: warp w sums bins w, w+4, ... over the warps for position (tile*32 + lane).
+__device__ __forceinline__ void tok_flush(uint16_t* cnt, uint64_t t, bool t_ok, int k,
+                                          unsigned int* counts) {
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int b = warp; b < k; b += kTokHWarps) {
+    uint32_t sum = 0;
+#pragma unroll
+    for (int w = 0; w < kTokHWarps; ++w) sum += cnt[(w * 256 + b) * 32 + lane];
+    if (sum && t_ok) atomicAdd(counts + t * k + b, sum);
+  }
+  __syncthreads();
+  uint4* c4 = reinterpret_cast<uint4*>(cnt);
+  for (int i = threadIdx.x; i < kTokHWarps * 256 * 32 * 2 / 16; i += blockDim.x)
+    c4[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+}
+
+template <bool FIXED>
+__global__ void __launch_bounds__(kTokHWarps * 32) token_hist_lane_kernel(
+    const float* __restrict__ v, TokArgs a, uint64_t tiles, uint64_t splits,
+    const double* trange, double fixed_lo, double fixed_hi, unsigned int* counts) {
+  extern __shared__ __align__(16) uint16_t tcnt[];  // [warp][256 bins][32 lanes]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int k = a.k;
+  {
+    uint4* c4 = reinterpret_cast<uint4*>(tcnt);
+    for (int i = threadIdx.x; i < kTokHWarps * 256 * 32 * 2 / 16; i += blockDim.x)
+      c4[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  const uint32_t cbase = static_cast<uint32_t>(__cvta_generic_to_shared(tcnt)) +
+                         static_cast<uint32_t>(warp) * (256 * 32 * 2) + lane * 2u;
+  for (uint64_t item = blockIdx.x; item < tiles * splits; item += gridDim.x) {
+    uint64_t tile, c0, c1;
+    tok_item_split(item, tiles, splits, a.channels, &tile, &c0, &c1);
+    const uint64_t t = tile * 32 + lane;
+    const bool t_ok = t < a.length;
+    const BinParams P = FIXED ? make_bin_params_lohi(fixed_lo, fixed_hi, k)
+                        : t_ok ? make_bin_params_lohi(-trange[t], trange[a.length + t], k)
+                               : make_bin_params_lohi(0.0, 0.0, k);
+    // this warp's sampled channels: c = cf + i*stride, cf the first sampled one >= w0
+    const uint64_t per = (c1 - c0 + kTokHWarps - 1) / kTokHWarps;
+    const uint64_t w0 = umin64(c1, c0 + warp * per), w1 = umin64(c1, w0 + per);
+    const uint64_t r = (a.offset + w0) % a.stride;
+    const uint64_t cf = w0 + (r == 0 ? 0 : a.stride - r);
+    const uint64_t n = cf < w1 ? (w1 - cf + a.stride - 1) / a.stride : 0;
+    // block-uniform trip count (an upper bound on every warp's n), so the flush's
+    // __syncthreads below is reached by all warps together
+    const uint64_t n_blk = per / a.stride + 1;
+    const float* col = v + (t_ok ? t : 0);
+    const uint64_t rstep = a.stride * a.length;  // elements between sampled rows
+    const uint32_t inc = t_ok ? 1u : 0u;
+    uint32_t since = 0;
+    // loads run one batch ahead of the binning: 2 x kTokHUnroll rows in flight per lane;
+    // full batches (the common case) carry no per-sample predicates
+    float xn[kTokHUnroll];
+    {
+      const float* q = col + cf * a.length;
+#pragma unroll
+      for (int u = 0; u < kTokHUnroll; ++u) {
+        xn[u] = static_cast<uint64_t>(u) < n ? __ldcs(q) : 0.f;
+        q += rstep;
+      }
+    }
+    for (uint64_t i = 0; i < n_blk; i += kTokHUnroll) {
+      float x[kTokHUnroll];
+#pragma unroll
+      for (int u = 0; u < kTokHUnroll; ++u) x[u] = xn[u];
+      const float* q = col + (cf + (i + kTokHUnroll) * a.stride) * a.length;
+      if (i + 2 * kTokHUnroll <= n) {
+#pragma unroll
+        for (int u = 0; u < kTokHUnroll; ++u) {
+          xn[u] = __ldcs(q);
+          q += rstep;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kTokHUnroll; ++u) {
+          xn[u] = i + kTokHUnroll + u < n ? __ldcs(q) : 0.f;
+          q += rstep;
+        }
+      }
+      int bin[kTokHUnroll];
+      bool any_slow = P.exact_only != 0;
+#pragma unroll
+      for (int u = 0; u < kTokHUnroll; ++u) {
+        bool sl;
+        bin[u] = bin_fast<FIXED>(x[u], P, &sl);
+        any_slow |= sl;
+      }
+      if (__any_sync(0xffffffffu, any_slow)) {
+#pragma unroll
+        for (int u = 0; u < kTokHUnroll; ++u) {
+          bool sl;
+          bin_fast<FIXED>(x[u], P, &sl);
+          if (sl || P.exact_only)
+            bin[u] = bin_index_exact(static_cast<double>(x[u]), P.lo, P.width, k);
+        }
+      }
+      const bool full = i + kTokHUnroll <= n;
+#pragma unroll
+      for (int g = 0; g < kTokHUnroll / 2; ++g) {
+        const uint32_t i0 = (full || i + 2 * g < n) ? inc : 0u;
+        const uint32_t i1 = (full || i + 2 * g + 1 < n) ? inc : 0u;
+        const int b0 = bin[2 * g], b1 = bin[2 * g + 1];
+        const uint32_t a0 = cbase + static_cast<uint32_t>(b0) * 64u;
+        const uint32_t a1 = cbase + static_cast<uint32_t>(b1) * 64u;
+        uint32_t v0, v1;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
+        v0 += i0;
+        v1 += i1 + (b0 == b1 ? i0 : 0u);
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(a0), "h"(static_cast<uint16_t>(v0)) : "memory");
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(a1), "h"(static_cast<uint16_t>(v1)) : "memory");
+      }
+      since += kTokHUnroll;
+      // flush before a 16-bit counter can overflow (block-uniform condition)
+      if (since >= kTokHMaxPerFlush && i + kTokHUnroll < n_blk) {
+        tok_flush(tcnt, t, t_ok, k, counts);
+        since = 0;
+      }
+    }
+    tok_flush(tcnt, t, t_ok, k, counts);
   }
 }
 
@@ -1441,10 +1692,40 @@ cudaError_t launch_token_range_init(double* d_trange, double* d_flag, uint64_t l
   return cudaMemsetAsync(d_flag, 0, sizeof(double), s);
 }
 
+// (position tiles, channel splits) for the lane kernels: enough items for ~4 per resident
+// block, each split >= 256 channels
+void tok_lane_items(uint64_t channels, uint64_t length, uint64_t tile, int resident,
+                    uint64_t* tiles, uint64_t* splits) {
+  *tiles = (length + tile - 1) / tile;
+  uint64_t sp = (static_cast<uint64_t>(resident) * 4 + *tiles - 1) / *tiles;
+  const uint64_t max_sp = (channels + 255) / 256;
+  if (sp > max_sp) sp = max_sp;
+  *splits = sp < 1 ? 1 : sp;
+}
+
+bool tok_lane_ok(const float* v, uint64_t length, int k) {
+  return k <= 256 && length % 4 == 0 && (reinterpret_cast<uintptr_t>(v) & 15u) == 0;
+}
+template <typename T>
+bool tok_lane_ok(const T*, uint64_t, int) {
+  return false;
+}
+
 template <typename T>
 cudaError_t launch_token_minmax(const T* v, uint64_t channels, uint64_t length, uint64_t offset,
                                 uint64_t stride, double* d_trange, double* d_flag, int num_sms,
                                 cudaStream_t s) {
+  if (tok_lane_ok(v, length, 0)) {
+    const TokArgs a{channels, length, offset, stride, 0, 1};
+    uint64_t tiles, splits;
+    const int resident = num_sms * 2;  // 2 blocks of 8 warps per SM
+    tok_lane_items(channels, length, 128, resident, &tiles, &splits);
+    const uint64_t items = tiles * splits;
+    const unsigned grid = static_cast<unsigned>(items < static_cast<uint64_t>(resident) ? items : resident);
+    token_minmax_lane_kernel<<<grid, kTokMmWarps * 32, 0, s>>>(
+        reinterpret_cast<const float*>(v), a, tiles, splits, d_trange, d_flag);
+    return cudaGetLastError();
+  }
   const bool vec = tok_vec_ok(v, length);
   const TokArgs a{channels, length, offset, stride, 0, vec ? 1 : 0};
   const dim3 grid = tok_grid<T>(channels, length, vec, num_sms);
@@ -1480,6 +1761,23 @@ template <typename T>
 cudaError_t launch_token_hist(const T* v, uint64_t channels, uint64_t length, uint64_t offset,
                               const cl_hist_spec& spec, const double* d_trange,
                               unsigned int* d_counts, int num_sms, cudaStream_t s) {
+  if (tok_lane_ok(v, length, spec.bin_count)) {
+    const TokArgs a{channels, length, offset, spec.sample_stride, spec.bin_count, 1};
+    uint64_t tiles, splits;
+    const int resident = num_sms * 3;  // 3 blocks of 4 warps (64 KB of counters) per SM
+    tok_lane_items(channels, length, 32, resident, &tiles, &splits);
+    const uint64_t items = tiles * splits;
+    const unsigned grid = static_cast<unsigned>(items < static_cast<uint64_t>(resident) ? items : resident);
+    const size_t smem = size_t(kTokHWarps) * 256 * 32 * 2;
+    const bool fixed = spec.range_mode == CL_RANGE_FIXED;
+    auto kern = fixed ? token_hist_lane_kernel<true> : token_hist_lane_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kTokHWarps * 32, smem, s>>>(reinterpret_cast<const float*>(v), a, tiles, splits,
+                                            d_trange, spec.fixed_lo, spec.fixed_hi, d_counts);
+    return cudaGetLastError();
+  }
   const bool vec = tok_vec_ok(v, length);
   const TokArgs a{channels, length, offset, spec.sample_stride, spec.bin_count, vec ? 1 : 0};
   const dim3 grid = tok_grid<T>(channels, length, vec, num_sms);
