@@ -78,7 +78,14 @@ def test_golden_device_f32_prefill(cuda, golden, port):
 
 @pytest.mark.parametrize("ch,L,k,stride,fixed", [(33, 1, 256, 1, None), (65, 19, 64, 2, None),
                                                   (1000, 9, 4096, 7, None), (7, 130, 16, 1, (0., .5)),
-                                                  (2048, 8, 256, 1, None)])
+                                                  (2048, 8, 256, 1, None),
+                                                  # fp32 lane-per-position kernels (L % 4 == 0,
+                                                  # K <= 256): ragged position tiles, strides,
+                                                  # fixed range, many channel splits
+                                                  (4096, 100, 256, 3, None),
+                                                  (3000, 36, 64, 1, (-1.0, 1.0)),
+                                                  (20000, 44, 256, 8, None),
+                                                  (513, 1028, 128, 1, None)])
 def test_random_shapes_vs_port(cuda, port, ch, L, k, stride, fixed):
     v = np.random.default_rng(ch * L).standard_normal((ch, L))
     raw, norm, n = port.token_entropy(v, k, 1e-8, stride, fixed)
