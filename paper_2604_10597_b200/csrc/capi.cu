@@ -199,6 +199,7 @@ int cl_ctx_destroy(cl_ctx* ctx) {
   cudaFree(ctx->d_scratch_decision);
   cudaFree(ctx->d_work);
   cudaFree(ctx->d_carry);
+  cudaFree(ctx->d_tcarry);
   cudaFree(ctx->d_bct);
   cudaFree(ctx->d_token_raw);
   cudaFree(ctx->d_token_range);

@@ -21,6 +21,12 @@ struct cl_ctx {
   size_t work_bytes = 0;
   float* d_carry = nullptr;  // scan segment carry (grown on demand)
   size_t carry_bytes = 0;
+  // tagged segment carry of the warp-specialised scan: 64-bit words {tag, h}; tags are
+  // epoch + segment with the epoch advanced past every launch's tags, so stale words from
+  // earlier launches never match (zeroed on allocation and on epoch wrap)
+  unsigned long long* d_tcarry = nullptr;
+  size_t tcarry_bytes = 0;
+  unsigned int carry_epoch = 0;
   float* d_bct = nullptr;  // B^T / C^T (b, L, N) for the TMA scan (grown on demand)
   size_t bct_bytes = 0;
   // token_entropy scratch (grown on demand): per-position raw entropies [L], ranges

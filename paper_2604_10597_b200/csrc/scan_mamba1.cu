@@ -309,6 +309,15 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned int* p) {
 __device__ __forceinline__ void st_release(unsigned int* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// two 64-bit words per access (each word single-copy atomic: a tag and its value)
+__device__ __forceinline__ void ld_relaxed_u64x2(const unsigned long long* p,
+                                                 unsigned long long& a, unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_u64x2(unsigned long long* p, unsigned long long a,
+                                                 unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
 
 // ---- packed fp32x2 (FFMA2) helpers: a 64-bit register pair holds two fp32 lanes ----
 typedef unsigned long long f2_t;
@@ -383,6 +392,8 @@ struct TmaArgs {
   float* h_last;
   float* carry;            // [n_tiles][32][16]
   unsigned int* flags;     // [n_tiles] completed segments
+  unsigned long long* tcarry;  // [n_tiles][16][16] {tag << 32 | h bits} (rowpair_ws_kernel)
+  unsigned int epoch;          // tag of segment s's carry-in = epoch + s
   unsigned int* ticket;    // work counter
   uint64_t batch, dim, L;
   int tiles_per_batch;
@@ -1022,19 +1033,38 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
       const float* src = nullptr;
       if (cur.seg == 0) {
         src = a.h0 ? a.h0 + size_t(row) * kN + 8 * hf : nullptr;
-      } else {
-        // chained carry from segment seg-1 of this tile
-        if (lane == 0)
-          while (ld_acquire(a.flags + cur.tile) < static_cast<unsigned>(cur.seg)) __nanosleep(64);
-        __syncwarp();
-        src = a.carry + (size_t(cur.tile) * kRowsP + r) * kN + 8 * hf;
       }
+      if (cur.seg == 0) {
 #pragma unroll
-      for (int s = 0; s < kN / 2; s += 4) {
-        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (src) q = __ldcg(reinterpret_cast<const float4*>(src + s));
-        h2[s / 2] = pk(q.x, q.y);
-        h2[s / 2 + 1] = pk(q.z, q.w);
+        for (int s = 0; s < kN / 2; s += 4) {
+          float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (src) q = __ldcg(reinterpret_cast<const float4*>(src + s));
+          h2[s / 2] = pk(q.x, q.y);
+          h2[s / 2 + 1] = pk(q.z, q.w);
+        }
+      } else {
+        // chained carry from segment seg-1 of this tile: every word carries its own tag,
+        // so a lane polls its 8 words with relaxed loads -- no flag, no acquire / release
+        // (the writer's release would also wait for all of its y stores to land)
+        const unsigned long long* w64 =
+            a.tcarry + (size_t(cur.tile) * kRowsP + r) * kN + 8 * hf;
+        const unsigned want = a.epoch + static_cast<unsigned>(cur.seg);
+        unsigned long long w[kN / 2];
+        for (;;) {
+          bool ok = true;
+#pragma unroll
+          for (int i = 0; i < kN / 2; i += 2) {
+            ld_relaxed_u64x2(w64 + i, w[i], w[i + 1]);
+            ok &= static_cast<unsigned>(w[i] >> 32) == want;
+            ok &= static_cast<unsigned>(w[i + 1] >> 32) == want;
+          }
+          if (__all_sync(0xffffffffu, ok)) break;
+          __nanosleep(64);
+        }
+#pragma unroll
+        for (int i = 0; i < kP; ++i)
+          h2[i] = pk(__uint_as_float(static_cast<unsigned>(w[2 * i])),
+                     __uint_as_float(static_cast<unsigned>(w[2 * i + 1])));
       }
     }
 
@@ -1052,21 +1082,19 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
       float hs[kN / 2];
 #pragma unroll
       for (int i = 0; i < kP; ++i) upk(h2[i], hs[2 * i], hs[2 * i + 1]);
-      float* dst = nullptr;
       if (cur.seg == n_seg - 1) {
-        if (a.h_last && row_valid) dst = a.h_last + size_t(row) * kN + 8 * hf;
+        if (a.h_last && row_valid) {
+          float* dst = a.h_last + size_t(row) * kN + 8 * hf;
+          __stcg(reinterpret_cast<float4*>(dst), make_float4(hs[0], hs[1], hs[2], hs[3]));
+          __stcg(reinterpret_cast<float4*>(dst + 4), make_float4(hs[4], hs[5], hs[6], hs[7]));
+        }
       } else {
-        dst = a.carry + (size_t(cur.tile) * kRowsP + r) * kN + 8 * hf;
-      }
-      if (dst) {
-        __stcg(reinterpret_cast<float4*>(dst), make_float4(hs[0], hs[1], hs[2], hs[3]));
-        __stcg(reinterpret_cast<float4*>(dst + 4), make_float4(hs[4], hs[5], hs[6], hs[7]));
-      }
-      if (cur.seg != n_seg - 1) {
-        // bar.warp.sync orders every lane's carry store before lane 0's gpu-scope
-        // release (cumulative); the reader pairs it with ld.acquire + bar.warp.sync
-        __syncwarp();
-        if (lane == 0) st_release(a.flags + cur.tile, static_cast<unsigned>(cur.seg + 1));
+        unsigned long long* w64 = a.tcarry + (size_t(cur.tile) * kRowsP + r) * kN + 8 * hf;
+        const unsigned long long tag =
+            static_cast<unsigned long long>(a.epoch + static_cast<unsigned>(cur.seg + 1)) << 32;
+#pragma unroll
+        for (int i = 0; i < kN / 2; i += 2)
+          st_relaxed_u64x2(w64 + i, tag | __float_as_uint(hs[i]), tag | __float_as_uint(hs[i + 1]));
       }
     }
   }
@@ -1290,6 +1318,23 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     if (!rc) rc = grow(ctx, &ctx->d_carry, &ctx->carry_bytes, carry_bytes, "cudaMalloc(carry)");
     if (!rc) rc = grow(ctx, &ctx->d_bct, &ctx->bct_bytes, bc_bytes, "cudaMalloc(B/C transpose)");
     if (rc) return rc;
+    unsigned int epoch = 0;
+    if (ws) {
+      // tagged carry words: zeroed when (re)allocated or when the epoch would wrap; each
+      // launch takes tags epoch + 1 .. epoch + (segments <= boxes), above every older tag
+      const size_t tcarry_bytes = size_t(n_tiles) * kRowsP * kN * sizeof(unsigned long long);
+      const bool fresh = ctx->tcarry_bytes < tcarry_bytes;
+      rc = grow(ctx, &ctx->d_tcarry, &ctx->tcarry_bytes, tcarry_bytes, "cudaMalloc(tagged carry)");
+      if (rc) return rc;
+      const unsigned span = static_cast<unsigned>((L + cfg.box - 1) / cfg.box) + 2u;
+      if (fresh || ctx->carry_epoch == 0 || ctx->carry_epoch > 0xFFFFFFFFu - span) {
+        cudaError_t e = cudaMemsetAsync(ctx->d_tcarry, 0, ctx->tcarry_bytes, s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(tagged carry)");
+        ctx->carry_epoch = 1;
+      }
+      epoch = ctx->carry_epoch;
+      ctx->carry_epoch += span;
+    }
     // B^T / C^T: interleaved per timestep ([B | C], 128 B rows, one TMA box) for the
     // warp-specialised kernel, two separate (b, L, 16) arrays for the row kernel
     float* d_Bt = ctx->d_bct;
@@ -1323,6 +1368,8 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     t.h0 = a.h0;
     t.h_last = a.h_last;
     t.carry = ctx->d_carry;
+    t.tcarry = ctx->d_tcarry;
+    t.epoch = epoch;
     t.ticket = ctx->d_work;
     t.flags = ctx->d_work + 32;
     t.batch = Bt;
