@@ -283,6 +283,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0,
                                              int c1, int c2) {
   asm volatile(
@@ -394,6 +402,8 @@ struct TmaArgs {
   unsigned int* flags;     // [n_tiles] completed segments
   unsigned long long* tcarry;  // [n_tiles][16][16] {tag << 32 | h bits} (rowpair_ws_kernel)
   unsigned int epoch;          // tag of segment s's carry-in = epoch + s
+  int stage_params;            // A / bias / D 16-byte aligned: the producer stages a full
+                               // tile's rows of them into shared memory with the item's first box
   unsigned int* ticket;    // work counter
   uint64_t batch, dim, L;
   int tiles_per_batch;
@@ -708,7 +718,10 @@ struct GeoP {
   static constexpr int kTileBytes = kRowsP * BOX * 4;  // u / delta / z: [16 rows][BOX]
   static constexpr int kBCBytes = BOX * 2 * kN * 4;    // [BOX][B 0..15 | C 0..15]
   static constexpr int kStageBytes = 3 * kTileBytes + kBCBytes;
+  // per-item parameters staged with an item's first box: A rows [16][16], bias [16], D [16]
+  static constexpr int kParamBytes = kRowsP * kN * 4 + 2 * kRowsP * 4;
 };
+constexpr int kStagedFlag = 1 << 30;  // meta.y bit: this item's parameters are in shared memory
 
 __device__ __forceinline__ f2_t shfl_xor2(f2_t v, int m) {
   float lo, hi;
@@ -921,7 +934,8 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   constexpr int kWB = STAGES * G::kStageBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(WARPS) * kWB);  // [WARPS][STAGES]
+  unsigned char* params = smem + size_t(WARPS) * kWB;  // [WARPS][STAGES][kParamBytes]
+  uint64_t* full = reinterpret_cast<uint64_t*>(params + size_t(WARPS) * STAGES * G::kParamBytes);
   uint64_t* empty = full + WARPS * STAGES;                                  // [WARPS][STAGES]
   int2* meta = reinterpret_cast<int2*>(empty + WARPS * STAGES);              // [WARPS][STAGES]
 
@@ -972,10 +986,20 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
             mbar_arrive(bar);
             live = false;
           } else {
-            meta[w * STAGES + slot] = make_int2(p_item, p_box);
             unsigned char* st = wbase + slot * G::kStageBytes;
             const int t = p_it.t0 + p_box * BOX;
-            mbar_expect_tx(bar, HZ ? G::kStageBytes : G::kStageBytes - G::kTileBytes);
+            const bool stage = p_box == 0 && a.stage_params &&
+                               p_r0 + kRowsP <= static_cast<int>(a.dim);
+            meta[w * STAGES + slot] = make_int2(p_item, p_box | (stage ? kStagedFlag : 0));
+            uint32_t tx = HZ ? G::kStageBytes : G::kStageBytes - G::kTileBytes;
+            if (stage) tx += kRowsP * kN * 4 + (a.bias ? kRowsP * 4 : 0) + (a.D ? kRowsP * 4 : 0);
+            mbar_expect_tx(bar, tx);
+            if (stage) {
+              unsigned char* pp = params + (size_t(w) * STAGES + slot) * G::kParamBytes;
+              bulk_g2s(pp, a.A + size_t(p_r0) * kN, kRowsP * kN * 4, bar);
+              if (a.bias) bulk_g2s(pp + kRowsP * kN * 4, a.bias + p_r0, kRowsP * 4, bar);
+              if (a.D) bulk_g2s(pp + kRowsP * kN * 4 + kRowsP * 4, a.D + p_r0, kRowsP * 4, bar);
+            }
             tma_load_3d(st, &map_u, t, p_r0, p_b, bar);
             tma_load_3d(st + G::kTileBytes, &map_dt, t, p_r0, p_b, bar);
             if (HZ) tma_load_3d(st + 2 * G::kTileBytes, &map_z, t, p_r0, p_b, bar);
@@ -1014,7 +1038,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     mbar_wait(wfull + slot, (iter / STAGES) & 1);
     const int2 m = wmeta[slot];
     if (m.x < 0) break;
-    const int box = m.y;
+    const int box = m.y & ~kStagedFlag;
     if (box == 0) {
       cur = decode(m.x);
       const int b = cur.tile / a.tiles_per_batch;
@@ -1022,14 +1046,27 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
       row_valid = c < static_cast<int>(a.dim);
       const int cc = row_valid ? c : 0;
       row = b * static_cast<int>(a.dim) + cc;
+      if (m.y & kStagedFlag) {
+        // staged by the producer with this box (shared memory: no global round trip)
+        const unsigned char* pp = params + (size_t(warp) * STAGES + slot) * G::kParamBytes;
 #pragma unroll
-      for (int s = 0; s < kN / 2; s += 4) {
-        const float4 q = *reinterpret_cast<const float4*>(a.A + size_t(cc) * kN + 8 * hf + s);
-        A2p[s / 2] = pk(q.x * kLog2e, q.y * kLog2e);
-        A2p[s / 2 + 1] = pk(q.z * kLog2e, q.w * kLog2e);
+        for (int s = 0; s < kN / 2; s += 4) {
+          const float4 q = *reinterpret_cast<const float4*>(pp + (r * kN + 8 * hf + s) * 4);
+          A2p[s / 2] = pk(q.x * kLog2e, q.y * kLog2e);
+          A2p[s / 2 + 1] = pk(q.z * kLog2e, q.w * kLog2e);
+        }
+        bias = a.bias ? reinterpret_cast<const float*>(pp + kRowsP * kN * 4)[r] : 0.f;
+        Dc = a.D ? reinterpret_cast<const float*>(pp + kRowsP * kN * 4 + kRowsP * 4)[r] : 0.f;
+      } else {
+#pragma unroll
+        for (int s = 0; s < kN / 2; s += 4) {
+          const float4 q = *reinterpret_cast<const float4*>(a.A + size_t(cc) * kN + 8 * hf + s);
+          A2p[s / 2] = pk(q.x * kLog2e, q.y * kLog2e);
+          A2p[s / 2 + 1] = pk(q.z * kLog2e, q.w * kLog2e);
+        }
+        bias = a.bias ? a.bias[cc] : 0.f;
+        Dc = a.D ? a.D[cc] : 0.f;
       }
-      bias = a.bias ? a.bias[cc] : 0.f;
-      Dc = a.D ? a.D[cc] : 0.f;
       const float* src = nullptr;
       if (cur.seg == 0) {
         src = a.h0 ? a.h0 + size_t(row) * kN + 8 * hf : nullptr;
@@ -1237,8 +1274,8 @@ template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, bool PIPE = true, in
 cudaError_t launch_ws(const CUtensorMap (&m)[6], const TmaArgs& t, int num_sms, cudaStream_t s) {
   constexpr int kProducers = NP > 0 ? NP : producers_for<WARPS>();
   auto kern = rowpair_ws_kernel<BOX, WARPS, STAGES, SP, HZ, kProducers, PIPE>;
-  const size_t smem = size_t(WARPS) * STAGES * GeoP<BOX>::kStageBytes + 1024 +
-                      size_t(WARPS) * STAGES * (16 + 8);
+  const size_t smem = size_t(WARPS) * STAGES * (GeoP<BOX>::kStageBytes + GeoP<BOX>::kParamBytes) +
+                      1024 + size_t(WARPS) * STAGES * (16 + 8);
   cudaError_t e = set_smem(kern, smem);
   if (e != cudaSuccess) return e;
   kern<<<grid_for(t.n_tiles, WARPS, num_sms), (WARPS + kProducers) * 32, smem, s>>>(
@@ -1370,6 +1407,8 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     t.carry = ctx->d_carry;
     t.tcarry = ctx->d_tcarry;
     t.epoch = epoch;
+    t.stage_params = aligned16(a.A) && (!a.delta_bias || aligned16(a.delta_bias)) &&
+                     (!a.D || aligned16(a.D));
     t.ticket = ctx->d_work;
     t.flags = ctx->d_work + 32;
     t.batch = Bt;

@@ -128,3 +128,25 @@ def test_large_rows_subset(cuda, port):
         assert_close_normwise(y.reshape(-1, L)[r:r + 1], yr, TOL, f"y row {r}")
         assert_close_normwise(h.reshape(-1, N)[r:r + 1], hr, TOL, f"h row {r}")
     assert np.isfinite(y).all()
+
+
+def test_parameter_staging_paths_bitwise(cuda):
+    """Per-item A / bias / D reach the scan either staged by the producer's bulk copies
+    (16-byte aligned, full 16-row tiles) or by direct loads (misaligned bias or D, the
+    partial last tile).  Both must give the same bits."""
+    x = mamba_inputs(31, 2, 72, 16, 256)  # 72 = 4 full 16-row tiles + a partial one
+    d = to_dev(x, cuda)
+    ref, href = selective_scan_fn(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"],
+                                  d["delta_bias"], True, True, chunk_size=64)
+
+    def shifted(t):  # same values at a 4-byte (not 16-byte) aligned address
+        buf = torch.empty(t.numel() + 1, device=cuda, dtype=t.dtype)
+        buf[1:].copy_(t)
+        return buf[1:]
+
+    for bias, D in ((shifted(d["delta_bias"]), d["D"]), (d["delta_bias"], shifted(d["D"]))):
+        assert bias.data_ptr() % 16 or D.data_ptr() % 16
+        y, h = selective_scan_fn(d["u"], d["delta"], d["A"], d["B"], d["C"], D, d["z"], bias,
+                                 True, True, chunk_size=64)
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref) and torch.equal(h, href)
