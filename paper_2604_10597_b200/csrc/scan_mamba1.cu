@@ -914,7 +914,7 @@ __device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* yd
 // Per consumer warp and stage: full[s] (producer arrive.expect_tx + TMA bytes) and
 // empty[s] (consumer lane 0 arrive after its last shared-memory read of the stage).
 // The meta words (item, box) travel through shared memory under full[s]'s release.
-template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int NPROD, bool PIPE>
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int NPROD, int PIPE>
 __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     rowpair_ws_kernel(const __grid_constant__ CUtensorMap map_u,
                       const __grid_constant__ CUtensorMap map_dt,
@@ -1107,7 +1107,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
 
     const int tbox = cur.t0 + box * BOX;
     float* ydst = row_valid ? a.out + size_t(row) * a.L + tbox : nullptr;
-    if (PIPE && tbox + BOX <= L)
+    if (PIPE == 1 && tbox + BOX <= L)
       pair_box_pipe<BOX, SP, HZ>(wbase + slot * G::kStageBytes, ydst, r, hf, bias, Dc, A2p, h2);
     else
       pair_box<BOX, SP, HZ>(wbase + slot * G::kStageBytes, ydst, r, hf, min(BOX, L - tbox), bias,
@@ -1270,7 +1270,7 @@ int grid_for(int n_tiles, int warps, int num_sms) {
   return max_useful < num_sms ? (max_useful < 1 ? 1 : max_useful) : num_sms;
 }
 
-template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, bool PIPE = true, int NP = 0>
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int PIPE = 1, int NP = 0>
 cudaError_t launch_ws(const CUtensorMap (&m)[6], const TmaArgs& t, int num_sms, cudaStream_t s) {
   constexpr int kProducers = NP > 0 ? NP : producers_for<WARPS>();
   auto kern = rowpair_ws_kernel<BOX, WARPS, STAGES, SP, HZ, kProducers, PIPE>;
@@ -1429,7 +1429,7 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       case 6: e = dispatch<true, 16, 4, 4>(sp, hz, m, t, n, s); break;
       case 7: e = dispatch<true, 16, 7, 3>(sp, hz, m, t, n, s); break;
       case 8:
-        e = sp && hz ? launch_ws<16, 12, 2, true, true, false>(m, t, n, s)
+        e = sp && hz ? launch_ws<16, 12, 2, true, true, 0>(m, t, n, s)
                      : dispatch<true, 16, 12, 2>(sp, hz, m, t, n, s);
         break;
       case 9: e = dispatch<true, 16, 14, 2>(sp, hz, m, t, n, s); break;
