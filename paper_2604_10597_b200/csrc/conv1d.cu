@@ -125,6 +125,77 @@ __global__ void __launch_bounds__(kConvThreads) conv1d_vec_kernel(ConvArgs a) {
   if (a.range) range::commit<kConvThreads>(acc, a.range);
 }
 
+// Warp-coalesced path (L a multiple of 128, 16-byte aligned x and u): a warp owns runs
+// of kWQ consecutive 32-quad blocks of one row (2 KB of x per block group); lane l takes
+// quad l of each block, so every load and store instruction covers 512 contiguous bytes.
+// The causal halo of a quad (the previous quad's last W-1 inputs) comes from lane l-1 by
+// shuffle, and from the previous block's lane 31 (or one load / the zero padding at the
+// row start) for lane 0.
+constexpr int kWQ = 4;  // 32-quad blocks per warp run (4 x 16 B in flight per lane)
+
+template <int W, int MODE>
+__global__ void __launch_bounds__(kConvThreads) conv1d_warp_kernel(ConvArgs a) {
+  range::Acc acc;
+  const int lane = threadIdx.x % 32;
+  const uint64_t qpr = a.L / 4;                  // quads per row (a multiple of 32)
+  const uint64_t runs_per_row = qpr / (32 * kWQ);  // whole runs per row
+  const uint64_t tail_blocks = (qpr / 32) % kWQ;   // 32-quad blocks after the last run
+  const uint64_t units_per_row = runs_per_row + (tail_blocks ? 1 : 0);
+  const uint64_t units = a.rows * units_per_row;
+  const float4* x4 = reinterpret_cast<const float4*>(a.x);
+  float4* u4 = reinterpret_cast<float4*>(a.u);
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+  for (uint64_t unit = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+       unit < units; unit += warps) {
+    const uint64_t row = unit / units_per_row;
+    const uint64_t ur = unit - row * units_per_row;
+    const int nb = ur < runs_per_row ? kWQ : static_cast<int>(tail_blocks);
+    const uint64_t qb = row * qpr + ur * 32 * kWQ;  // first quad of the run
+    const uint64_t d = row % a.dim;
+    float4 in[kWQ];
+#pragma unroll
+    for (int m = 0; m < kWQ; ++m)
+      in[m] = m < nb ? __ldcs(x4 + qb + m * 32 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+    // halo of the run's first quad: the quad before it in the row (zero at the row start)
+    float4 prev31 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ur > 0) prev31 = __ldg(x4 + qb - 1);
+    float wk[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) wk[k] = __ldg(a.w + d * W + k);
+    const float bias = a.bias ? __ldg(a.bias + d) : 0.f;
+#pragma unroll
+    for (int m = 0; m < kWQ; ++m) {
+      if (m >= nb) break;
+      // previous quad: lane-1's, or for lane 0 the last quad of the previous block
+      float4 pv;
+      pv.y = __shfl_up_sync(0xffffffffu, in[m].y, 1);
+      pv.z = __shfl_up_sync(0xffffffffu, in[m].z, 1);
+      pv.w = __shfl_up_sync(0xffffffffu, in[m].w, 1);
+      if (lane == 0) pv = prev31;
+      prev31.y = __shfl_sync(0xffffffffu, in[m].y, 31);
+      prev31.z = __shfl_sync(0xffffffffu, in[m].z, 31);
+      prev31.w = __shfl_sync(0xffffffffu, in[m].w, 31);
+      const float xs[8] = {0.f, pv.y, pv.z, pv.w, in[m].x, in[m].y, in[m].z, in[m].w};
+      float o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float s = bias;
+#pragma unroll
+        for (int k = 0; k < W; ++k) s = fmaf(wk[k], xs[4 + i - (W - 1) + k], s);
+        o[i] = act(s, a.silu != 0);
+      }
+      const uint64_t q = qb + m * 32 + lane;
+      __stcs(u4 + q, make_float4(o[0], o[1], o[2], o[3]));
+      if (a.range) {
+        const uint64_t gi = a.g0 + q * 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc.visit(o[i], sampled<MODE>(gi + i, a.stride));
+      }
+    }
+  }
+  if (a.range) range::commit<kConvThreads>(acc, a.range);
+}
+
 // Scalar path: any L, any alignment, W <= 4.
 template <int MODE>
 __global__ void __launch_bounds__(kConvThreads) conv1d_scalar_kernel(ConvArgs a) {
@@ -165,6 +236,13 @@ cudaError_t launch_mode(const ConvArgs& a, bool vec, int num_sms, cudaStream_t s
   const dim3 grid(static_cast<unsigned>(blocks));
   if (!vec) {
     conv1d_scalar_kernel<MODE><<<grid, kConvThreads, 0, s>>>(a);
+  } else if (a.L % 128 == 0) {
+    switch (a.width) {
+      case 1: conv1d_warp_kernel<1, MODE><<<grid, kConvThreads, 0, s>>>(a); break;
+      case 2: conv1d_warp_kernel<2, MODE><<<grid, kConvThreads, 0, s>>>(a); break;
+      case 3: conv1d_warp_kernel<3, MODE><<<grid, kConvThreads, 0, s>>>(a); break;
+      default: conv1d_warp_kernel<4, MODE><<<grid, kConvThreads, 0, s>>>(a); break;
+    }
   } else {
     switch (a.width) {
       case 1: launch_vec<1, MODE>(a, grid, s); break;

@@ -39,7 +39,8 @@ def minmax_range(u, cuda, g0=0, stride=1):
 
 
 @pytest.mark.parametrize("width", [1, 2, 3, 4])
-@pytest.mark.parametrize("L", [64, 37])  # vector path / scalar path (L % 4 != 0)
+@pytest.mark.parametrize("L", [64, 37, 384, 1152])  # float4 runs / scalar (L % 4 != 0) /
+# warp-coalesced (L % 128 == 0: 3 blocks per row, 2 runs + a 1-block tail)
 def test_conv_matches_fp64(cuda, width, L):
     x, w, b = conv_inputs(width, 2, 24, L, width)
     for silu in (True, False):
