@@ -1156,10 +1156,16 @@ constexpr int kTokHWarps = 4;               // hist: warps per block, 32 positio
 #define CL_TOK_H_UNROLL 24
 #endif
 // Measured at C3 (u 8x4096x8192 as 32768 channels x 8192 positions): min/max 0.31-0.33 ms
-// for 4, 8 or 16 rows per batch; histogram 0.98 / 0.72 / 0.53 / 0.47 / 0.77 ms for 4 / 8 /
+// for 4, 8 or 16 rows per batch with one 128-position slice per block, 0.25 with 2-4
+// slices side by side (the block reads 1-2 KB of a row at a time: DRAM locality), 0.26
+// with 8; histogram 0.98 / 0.72 / 0.53 / 0.47 / 0.77 ms for 4 / 8 /
 // 16 / 24 / 32 rows (32: 182 registers, 2 blocks per SM).  Loads in flight, not
 // instructions, bound the histogram: a lane reads 4 bytes of a row, a warp 128 bytes.
+#ifndef CL_TOK_MM_COLS
+#define CL_TOK_MM_COLS 4
+#endif
 constexpr int kTokMmRows = CL_TOK_MM_ROWS;  // min/max: channel rows per batch
+constexpr int kTokMmCols = CL_TOK_MM_COLS;  // min/max: 128-position slices per block tile
 constexpr int kTokHUnroll = CL_TOK_H_UNROLL;  // hist: channel rows per batch (2 in flight)
 constexpr int kTokHMaxPerFlush = 65000;     // u16 counters: flush before overflow
 
@@ -1184,12 +1190,16 @@ __global__ void __launch_bounds__(kTokMmWarps * 32) token_minmax_lane_kernel(
   for (uint64_t item = blockIdx.x; item < tiles * splits; item += gridDim.x) {
     uint64_t tile, c0, c1;
     tok_item_split(item, tiles, splits, a.channels, &tile, &c0, &c1);
-    const uint64_t t0 = tile * 128 + lane * 4;
+    // kTokMmCols 128-position column slices per tile; the kTokMmWarps / kTokMmCols warps
+    // of a slice split the item's channels
+    constexpr int kSliceWarps = kTokMmWarps / kTokMmCols;
+    const int col = warp / kSliceWarps, wsl = warp % kSliceWarps;
+    const uint64_t t0 = (tile * kTokMmCols + col) * 128 + lane * 4;
     float lo[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
     float hi[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
     if (t0 < a.length) {
-      const uint64_t per = (c1 - c0 + kTokMmWarps - 1) / kTokMmWarps;
-      const uint64_t w0 = umin64(c1, c0 + warp * per), w1 = umin64(c1, w0 + per);
+      const uint64_t per = (c1 - c0 + kSliceWarps - 1) / kSliceWarps;
+      const uint64_t w0 = umin64(c1, c0 + wsl * per), w1 = umin64(c1, w0 + per);
       uint64_t cm = (a.offset + w0) % a.stride;  // (offset + c) % stride, incremental
       uint64_t c = w0;
       const float* rp = v + w0 * a.length + t0;
@@ -1236,12 +1246,13 @@ __global__ void __launch_bounds__(kTokMmWarps * 32) token_minmax_lane_kernel(
       s_hi[warp][lane * 4 + e] = hi[e];
     }
     __syncthreads();
-    if (threadIdx.x < 128) {
-      const uint64_t t = tile * 128 + threadIdx.x;
-      float l = s_lo[0][threadIdx.x], h = s_hi[0][threadIdx.x];
-      for (int w = 1; w < kTokMmWarps; ++w) {
-        l = s_lo[w][threadIdx.x] < l ? s_lo[w][threadIdx.x] : l;
-        h = h < s_hi[w][threadIdx.x] ? s_hi[w][threadIdx.x] : h;
+    for (int i = threadIdx.x; i < 128 * kTokMmCols; i += blockDim.x) {
+      const int cs = i / 128, p = i % 128;
+      const uint64_t t = (tile * kTokMmCols + cs) * 128 + p;
+      float l = s_lo[cs * kSliceWarps][p], h = s_hi[cs * kSliceWarps][p];
+      for (int w = 1; w < kSliceWarps; ++w) {
+        l = s_lo[cs * kSliceWarps + w][p] < l ? s_lo[cs * kSliceWarps + w][p] : l;
+        h = h < s_hi[cs * kSliceWarps + w][p] ? s_hi[cs * kSliceWarps + w][p] : h;
       }
       if (t < a.length && h >= l) {
         atomic_max_f64(trange + t, -static_cast<double>(l));
@@ -1719,7 +1730,7 @@ cudaError_t launch_token_minmax(const T* v, uint64_t channels, uint64_t length, 
     const TokArgs a{channels, length, offset, stride, 0, 1};
     uint64_t tiles, splits;
     const int resident = num_sms * 2;  // 2 blocks of 8 warps per SM
-    tok_lane_items(channels, length, 128, resident, &tiles, &splits);
+    tok_lane_items(channels, length, 128 * kTokMmCols, resident, &tiles, &splits);
     const uint64_t items = tiles * splits;
     const unsigned grid = static_cast<unsigned>(items < static_cast<uint64_t>(resident) ? items : resident);
     token_minmax_lane_kernel<<<grid, kTokMmWarps * 32, 0, s>>>(
