@@ -252,10 +252,18 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local_rank)
-    device = torch.device("cuda", local_rank)
+    # CL_BENCH_DIST_BACKEND=gloo is a functional check of the N>1 code path on a
+    # one-GPU box (ranks share cuda:0, collectives staged through the host by gloo);
+    # its timings are not scaling numbers.  The product path is NCCL, one GPU per rank.
+    backend = os.environ.get("CL_BENCH_DIST_BACKEND", "nccl")
+    dev_index = local_rank if backend == "nccl" else local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    device = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
 
     import paper_2604_10597_b200 as cl
     from paper_2604_10597_b200.mamba1 import Prefill
@@ -328,7 +336,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(dev_index) as clocks:
         time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
         clocks.mark("t_start")
         start.record()
@@ -381,7 +389,9 @@ def main():
                      "frac": scan_gbs / peak, "traffic": traffic, "kernel": "rowpair_ws_kernel",
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": ab["scan"]},
-        "stage_ms": {k: statistics.mean(v) for k, v in stage_ms.items()},
+        "stage_ms": ({k: statistics.mean(v) for k, v in stage_ms.items()} if world == 1 else
+                     {"entropy_allreduce_decide": statistics.mean(stage_ms["minmax"]),
+                      "scan": statistics.mean(stage_ms["scan"])}),
         "entropy_gbs": ab["entropy"] / (ent_ms / 1e3) / 1e9,
         "chunk": rec.decision.chunk, "raw_nats": rec.entropy.raw_nats,
         "gpu_launches": launches,

@@ -424,6 +424,15 @@ __device__ __forceinline__ void flush_warp(cnt_t* cnt, uint32_t* cta_hist, int l
   __syncwarp();
 }
 
+#ifndef CL_HIST_X2
+#define CL_HIST_X2 1
+#endif
+__device__ __forceinline__ uint64_t pack_f2(float a, float b) {
+  return (static_cast<uint64_t>(__float_as_uint(b)) << 32) | __float_as_uint(a);
+}
+__device__ __forceinline__ float lo_f(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+__device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+
 __device__ __forceinline__ uint64_t add_mod(uint64_t r, uint64_t d, uint64_t stride) {
   r += d;  // r, d < stride
   return r >= stride ? r - stride : r;
@@ -538,6 +547,25 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
         // t bits carry the bin (0x4B400000 + n); near-edge samples get the exact bin's bits
         uint32_t tb[kLaneSamples];
         bool any_slow = p.exact_only != 0;
+#if CL_HIST_X2
+        // the same per-sample fp32 operations on sample pairs (FFMA2 / FADD2: every f32x2
+        // lane rounds exactly like the scalar op), half the FMA-pipe instructions
+        const uint64_t s2 = pack_f2(p.s_f, p.s_f), c2 = pack_f2(p.c_f, p.c_f);
+        const uint64_t mp = pack_f2(12582912.0f, 12582912.0f);
+        const uint64_t mn = pack_f2(-12582912.0f, -12582912.0f);
+#pragma unroll
+        for (int e = 0; e < kLaneSamples; e += 2) {
+          uint64_t x2, t2, r2, d2;
+          asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(x2) : "l"(pack_f2(val[e], val[e + 1])), "l"(s2), "l"(c2));
+          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t2) : "l"(x2), "l"(mp));
+          asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r2) : "l"(t2), "l"(mn));
+          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d2) : "l"(x2), "l"(r2));
+          any_slow |= !(fabsf(lo_f(d2)) <= p.thr);
+          any_slow |= !(fabsf(hi_f(d2)) <= p.thr);
+          tb[e] = static_cast<uint32_t>(t2);
+          tb[e + 1] = static_cast<uint32_t>(t2 >> 32);
+        }
+#else
 #pragma unroll
         for (int e = 0; e < kLaneSamples; ++e) {
           const float x = fmaf(val[e], p.s_f, p.c_f);
@@ -545,6 +573,7 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
           any_slow |= !(fabsf(x - (t - 12582912.0f)) <= p.thr);
           tb[e] = __float_as_uint(t);
         }
+#endif
         if (__any_sync(0xffffffffu, any_slow)) {
 #pragma unroll
           for (int e = 0; e < kLaneSamples; ++e) {
