@@ -195,8 +195,10 @@ typedef struct {
   int delta_softplus;
 } cl_mamba1_args;
 
-/* Scan variants (all bit-identical): CL_SCAN_AUTO picks by shape. */
-enum { CL_SCAN_AUTO = 0, CL_SCAN_ROWSEQ_TMA = 1, CL_SCAN_GENERIC = 2 };
+/* Scan variants (all bit-identical): CL_SCAN_AUTO picks by shape.  CL_SCAN_CONFIG_BASE + i
+ * forces row i of the TMA kernel table (scan_mamba1.cu kCfgs: lane-pair / quad / row
+ * kernels and their warp counts) -- for A/B measurements and the bitwise cross-checks. */
+enum { CL_SCAN_AUTO = 0, CL_SCAN_ROWSEQ_TMA = 1, CL_SCAN_GENERIC = 2, CL_SCAN_CONFIG_BASE = 16 };
 int cl_selective_scan_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_decision* d_decision,
                           int fixed_chunk /* used when d_decision == NULL */, int variant,
                           void* stream);

@@ -18,7 +18,7 @@ CL_RANGE_DYNAMIC, CL_RANGE_FIXED = 0, 1
 (CL_POL_STATIC, CL_POL_MIDPOINT, CL_POL_FULL_HIST, CL_POL_SAMPLED_HIST, CL_POL_LEARNED_TABLE,
  CL_POL_GUARDED, CL_POL_RULE, CL_POL_TOKEN_HIST) = range(8)
 CL_SRC_GUARDED, CL_SRC_GUARDED_FALLBACK = 16, 32
-CL_SCAN_AUTO, CL_SCAN_ROWSEQ_TMA, CL_SCAN_GENERIC = 0, 1, 2
+CL_SCAN_AUTO, CL_SCAN_ROWSEQ_TMA, CL_SCAN_GENERIC, CL_SCAN_CONFIG_BASE = 0, 1, 2, 16
 
 SOURCE_NAMES = {0: "static", 1: "no_entropy_midpoint", 2: "full_histogram",
                 3: "sampled_histogram", 4: "learned_table", 6: "rule", 7: "token_histogram"}

@@ -92,8 +92,15 @@ def selective_scan_fn(u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_
                              dtype=torch.float32)
     a = _mamba_args(u, delta, A, B, C, D, z, delta_bias, h0, out, h_last, delta_softplus)
     ctx.call("cl_selective_scan_f32", C_byref(a), _ptr(decision), int(chunk_size),
-             _VARIANTS[variant], _stream_ptr(u.device))
+             _variant_code(variant), _stream_ptr(u.device))
     return (out, h_last) if return_last_state else out
+
+
+def _variant_code(variant: str) -> int:
+    """"auto" / "rowseq_tma" / "generic", or "cfg:<i>" for row i of the TMA kernel table."""
+    if variant.startswith("cfg:"):
+        return _lib.CL_SCAN_CONFIG_BASE + int(variant[4:])
+    return _VARIANTS[variant]
 
 
 def selective_state_update(state, x, dt, A, B, C, D=None, z=None, dt_bias=None,

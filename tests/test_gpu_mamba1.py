@@ -150,3 +150,64 @@ def test_parameter_staging_paths_bitwise(cuda):
                                  True, True, chunk_size=64)
         torch.cuda.synchronize()
         assert torch.equal(y, ref) and torch.equal(h, href)
+
+
+# TMA kernel table rows (scan_mamba1.cu kCfgs): 0/4-7/9 lane pair, 8 lane pair without the
+# group pipeline, 10-13 quad layout (a warp pair per tile), 1-3 row kernels
+PAIR_CFGS = [0, 4, 5, 6, 7, 8, 9]
+QUAD_CFGS = [10, 11, 12, 13]
+ROW_CFGS = [1, 2, 3]
+
+
+@pytest.mark.parametrize("shape,chunk", [
+    ((1, 48, 16, 256), 64),     # 3 tiles, 4 segments: carry hand-offs
+    ((2, 40, 16, 100), 32),     # partial tile, L % 16 != 0 (short last box)
+    ((1, 128, 16, 1024), 512),
+    ((3, 16, 16, 4), 512),      # one box, four timesteps
+])
+@pytest.mark.parametrize("flags", [(True, True, True), (False, False, False), (True, False, True)])
+def test_all_kernel_configs_bitwise(cuda, port, shape, chunk, flags):
+    """Every TMA kernel configuration -- lane pair, quad, row kernels -- gives the same
+    bits for y and h_last (the shared canonical arithmetic), and matches the oracle."""
+    softplus, use_z, use_D = flags
+    batch, dim, N, L = shape
+    x = mamba_inputs(hash((shape, chunk)) % 997, batch, dim, N, L)
+    if not softplus:  # raw delta must stay positive or exp(delta*A) > 1 blows the state up
+        x["delta"] = np.abs(x["delta"]) * 0.1
+        x["delta_bias"] = np.abs(x["delta_bias"]) * 0.01
+    d = to_dev(x, cuda)
+    h0 = torch.randn(batch, dim, N, device=cuda, generator=torch.Generator(cuda).manual_seed(3))
+
+    def go(variant):
+        out, h = selective_scan_fn(d["u"], d["delta"], d["A"], d["B"], d["C"],
+                                   d["D"] if use_D else None, d["z"] if use_z else None,
+                                   d["delta_bias"], softplus, True, chunk_size=chunk,
+                                   variant=variant, h0=h0)
+        torch.cuda.synchronize()
+        return out, h
+
+    ref_y, ref_h = go("cfg:0")
+    for c in PAIR_CFGS + QUAD_CFGS + ROW_CFGS:
+        y, h = go(f"cfg:{c}")
+        assert torch.equal(y, ref_y), c
+        assert torch.equal(h, ref_h), c
+    gy, gh = go("generic")
+    assert torch.equal(gy, ref_y) and torch.equal(gh, ref_h)
+
+
+@pytest.mark.parametrize("cfg", QUAD_CFGS)
+def test_quad_matches_oracle(cuda, port, cfg):
+    x = mamba_inputs(cfg, 1, 80, 16, 520)
+    d = to_dev(x, cuda)
+    y, h = selective_scan_fn(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"],
+                             d["delta_bias"], True, True, chunk_size=128, variant=f"cfg:{cfg}")
+    torch.cuda.synchronize()
+    yr, hr = oracle(port, x)
+    assert_close_normwise(y.cpu().numpy().reshape(-1, 520), yr, TOL, "y")
+    assert_close_normwise(h.cpu().numpy().reshape(-1, 16), hr, TOL, "h_last")
+
+
+def test_config_variant_errors(cuda):
+    x = to_dev(mamba_inputs(1, 1, 16, 16, 32), cuda)
+    with pytest.raises(Exception, match="no such kernel configuration"):
+        selective_scan_fn(x["u"], x["delta"], x["A"], x["B"], x["C"], variant="cfg:99")
