@@ -911,124 +911,10 @@ __device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* yd
   }
 }
 
-// Few-tile shapes (C1, C2, the B = 1 serving mix): one lane-pair warp per 16-row tile
-// leaves three of an SM's four sub-partitions idle, and a lone warp reaches about half
-// of its sub-partition's MUFU rate.  The quad layout gives each row FOUR lanes and a tile
-// two warps (rows 8w..8w+7), so every tile runs on two sub-partitions with half the
-// exponentials per lane.  Lane q = 2hf + sb of a row owns states 8hf+2sb+{0,1,4,5}: the
-// sb = 0 lane carries the canonical chain ya = (s0,s1) then (s4,s5) of its half, sb = 1
-// carries yb = (s2,s3) then (s6,s7), with the same FFMA2 operations on the same values
-// as the lane pair, so y, h_last and the carry are bit-identical to pair_box.  Per
-// 4-timestep group: lane q computes softplus for timestep q (3 shuffles gather all four),
-// a xor-1 exchange forms L_hf = (ya.lo + yb.lo) + (ya.hi + yb.hi) for two timesteps, a
-// xor-2 exchange forms y = L_0 + L_1 for timestep q, and lane q stores y[4j + q].
-template <int BOX, bool SP, bool HZ>
-__device__ __forceinline__ void quad_box(const unsigned char* st, float* ydst, int r, int q,
-                                         int valid, float bias, float Dc,
-                                         const f2_t (&A2p)[kN / 4], f2_t (&h2)[kN / 4]) {
-  using G = GeoP<BOX>;
-  constexpr int kBCRow = 2 * kN * 4;
-  constexpr int kG = BOX / 4;
-  const int hf = q >> 1, sb = q & 1;
-  const int ng = (valid + 3) >> 2;
-  const unsigned char* sB = st + 3 * G::kTileBytes + 32 * hf + 8 * sb;
-  const unsigned char* sC = sB + kN * 4;
-  // A lone warp per sub-partition has nothing to hide latency behind, so the box is
-  // software-pipelined by hand: group j+1's prologue (loads, softplus, dt gather, SiLU)
-  // and group j-1's y exchange are issued under group j's exponentials.
-  auto prep = [&](int j, float (&dt)[4], float (&xs)[4], float& uq, float& gq) {
-    const int off = Geo<BOX>::swz(r, j);
-    const float4 u4 = *reinterpret_cast<const float4*>(st + off);
-    const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
-    const float dq = q == 0 ? d4.x : (q == 1 ? d4.y : (q == 2 ? d4.z : d4.w));
-    float sp = __fadd_rn(dq, bias);
-    if (SP) sp = softplus_canon(sp);
-    const float o1 = __shfl_xor_sync(0xffffffffu, sp, 1);
-    const f2_t mine = sb ? pk(o1, sp) : pk(sp, o1);
-    const f2_t other = shfl_xor2(mine, 2);
-    const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
-    const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
-    upk(dt01, dt[0], dt[1]);
-    upk(dt23, dt[2], dt[3]);
-    upk(x01, xs[0], xs[1]);
-    upk(x23, xs[2], xs[3]);
-    uq = q == 0 ? u4.x : (q == 1 ? u4.y : (q == 2 ? u4.z : u4.w));
-    if (HZ) {
-      const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
-      gq = silu_canon(q == 0 ? z4.x : (q == 1 ? z4.y : (q == 2 ? z4.z : z4.w)));
-    }
-  };
-  // y for timestep 4j + q from the four lanes' chains P[0..3] of group j
-  auto finish = [&](int j, const f2_t (&P)[4], float uq, float gq) {
-    const f2_t r0 = shfl_xor2(sb ? P[0] : P[1], 1);
-    const f2_t r1 = shfl_xor2(sb ? P[2] : P[3], 1);
-    float a0, a1;
-    upk(add2(sb ? P[1] : P[0], r0), a0, a1);
-    const float La = a0 + a1;  // L_hf at timestep sb
-    upk(add2(sb ? P[3] : P[2], r1), a0, a1);
-    const float Lb = a0 + a1;  // L_hf at timestep 2 + sb
-    const float recv = __shfl_xor_sync(0xffffffffu, hf ? La : Lb, 2);
-    const float ysum = __fadd_rn(hf ? Lb : La, recv);
-    float y = fmaf(Dc, uq, ysum);
-    if (HZ) y = __fmul_rn(y, gq);
-    if (ydst) __stcs(ydst + 4 * j + q, y);
-  };
-  float dt[4], xs[4], uq = 0.f, gq = 0.f;
-  f2_t Pp[4];
-  float uqp = 0.f, gqp = 0.f;
-  prep(0, dt, xs, uq, gq);
-#pragma unroll
-  for (int j = 0; j < kG; ++j) {
-    if (j >= ng) break;
-    f2_t dA[4][2];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const f2_t dd = pk(dt[k], dt[k]);
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        float al, ah;
-        upk(mul2(A2p[i], dd), al, ah);
-        dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
-      }
-    }
-    if (j > 0) finish(j - 1, Pp, uqp, gqp);
-    float ndt[4], nxs[4], nuq = 0.f, ngq = 0.f;
-    if (j + 1 < ng) prep(j + 1, ndt, nxs, nuq, ngq);
-    f2_t P[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int t = 4 * j + k;
-      const f2_t b0 = *reinterpret_cast<const f2_t*>(sB + t * kBCRow);
-      const f2_t b1 = *reinterpret_cast<const f2_t*>(sB + t * kBCRow + 16);
-      const f2_t c0 = *reinterpret_cast<const f2_t*>(sC + t * kBCRow);
-      const f2_t c1 = *reinterpret_cast<const f2_t*>(sC + t * kBCRow + 16);
-      const f2_t xx = pk(xs[k], xs[k]);
-      h2[0] = fma2(dA[k][0], h2[0], mul2(b0, xx));
-      h2[1] = fma2(dA[k][1], h2[1], mul2(b1, xx));
-      P[k] = fma2(c1, h2[1], fma2(c0, h2[0], 0ull));  // canonical chain (ya or yb)
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) Pp[k] = P[k];
-    uqp = uq;
-    gqp = gq;
-    if (j + 1 < ng) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        dt[k] = ndt[k];
-        xs[k] = nxs[k];
-      }
-      uq = nuq;
-      gq = ngq;
-    }
-  }
-  finish(ng - 1, Pp, uqp, gqp);
-}
-
 // Per consumer warp and stage: full[s] (producer arrive.expect_tx + TMA bytes) and
 // empty[s] (consumer lane 0 arrive after its last shared-memory read of the stage).
 // The meta words (item, box) travel through shared memory under full[s]'s release.
-// QUAD: each ring (item stream) is consumed by a warp pair in the quad layout (quad_box).
-template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int NPROD, int PIPE, bool QUAD = false>
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int NPROD, int PIPE>
 __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     rowpair_ws_kernel(const __grid_constant__ CUtensorMap map_u,
                       const __grid_constant__ CUtensorMap map_dt,
@@ -1047,17 +933,15 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  static_assert(!QUAD || WARPS % 2 == 0, "quad rings take warp pairs");
-  constexpr int RINGS = QUAD ? WARPS / 2 : WARPS;  // item streams (TMA rings) per CTA
   constexpr int kWB = STAGES * G::kStageBytes;
-  unsigned char* params = smem + size_t(RINGS) * kWB;  // [RINGS][STAGES][kParamBytes]
-  uint64_t* full = reinterpret_cast<uint64_t*>(params + size_t(RINGS) * STAGES * G::kParamBytes);
-  uint64_t* empty = full + RINGS * STAGES;                                  // [RINGS][STAGES]
-  int2* meta = reinterpret_cast<int2*>(empty + RINGS * STAGES);              // [RINGS][STAGES]
+  unsigned char* params = smem + size_t(WARPS) * kWB;  // [WARPS][STAGES][kParamBytes]
+  uint64_t* full = reinterpret_cast<uint64_t*>(params + size_t(WARPS) * STAGES * G::kParamBytes);
+  uint64_t* empty = full + WARPS * STAGES;                                  // [WARPS][STAGES]
+  int2* meta = reinterpret_cast<int2*>(empty + WARPS * STAGES);              // [WARPS][STAGES]
 
-  if (threadIdx.x < RINGS * STAGES) {
+  if (threadIdx.x < WARPS * STAGES) {
     mbar_init(full + threadIdx.x, 1);
-    mbar_init(empty + threadIdx.x, QUAD ? 2 : 1);
+    mbar_init(empty + threadIdx.x, 1);
   }
   if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
@@ -1074,9 +958,9 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
 
   if (warp >= WARPS) {
     // ---------------- producers ----------------
-    constexpr int kPer = (RINGS + NPROD - 1) / NPROD;
+    constexpr int kPer = (WARPS + NPROD - 1) / NPROD;
     const int w = (warp - WARPS) * kPer + lane;
-    bool live = lane < kPer && w < RINGS;
+    bool live = lane < kPer && w < WARPS;
     if (lane == 0 && warp == WARPS) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_u)));
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_dt)));
@@ -1088,7 +972,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     Item p_it = decode(p_item);
     int p_b = p_it.tile / a.tiles_per_batch, p_r0 = (p_it.tile % a.tiles_per_batch) * kRowsP;
     int p_box = 0, n_issued = 0;
-    unsigned char* wbase = smem + size_t(w < RINGS ? w : 0) * kWB;
+    unsigned char* wbase = smem + size_t(w < WARPS ? w : 0) * kWB;
     while (__any_sync(0xffffffffu, live)) {
       bool issued = false;
       if (live) {
@@ -1138,17 +1022,11 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
   }
 
   // ---------------- consumers ----------------
-  // lane pair: row r = lane / 2, states 8hf..8hf+7; quad: row r = 8 * (warp & 1) + lane / 4,
-  // states so + {0, 1, 4, 5} with so = 8hf + 2sb (q = lane % 4 = 2hf + sb)
-  const int ring = QUAD ? warp >> 1 : warp;
-  const int r = QUAD ? 8 * (warp & 1) + (lane >> 2) : lane >> 1;
-  const int q = lane & 3;
-  const int hf = QUAD ? q >> 1 : lane & 1;
-  const int so = QUAD ? 8 * hf + 2 * (q & 1) : 8 * hf;
-  const unsigned char* wbase = smem + size_t(ring) * kWB;
-  uint64_t* wfull = full + ring * STAGES;
-  uint64_t* wempty = empty + ring * STAGES;
-  const int2* wmeta = meta + ring * STAGES;
+  const int r = lane >> 1, hf = lane & 1;
+  const unsigned char* wbase = smem + size_t(warp) * kWB;
+  uint64_t* wfull = full + warp * STAGES;
+  uint64_t* wempty = empty + warp * STAGES;
+  const int2* wmeta = meta + warp * STAGES;
   constexpr int kP = kN / 4;
   f2_t h2[kP], A2p[kP];
   float bias = 0.f, Dc = 0.f;
@@ -1168,28 +1046,9 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
       row_valid = c < static_cast<int>(a.dim);
       const int cc = row_valid ? c : 0;
       row = b * static_cast<int>(a.dim) + cc;
-      if (QUAD) {
-        const float* Ar = (m.y & kStagedFlag)
-                              ? reinterpret_cast<const float*>(
-                                    params + (size_t(ring) * STAGES + slot) * G::kParamBytes) +
-                                    r * kN
-                              : a.A + size_t(cc) * kN;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const float2 v = *reinterpret_cast<const float2*>(Ar + so + 4 * i);
-          A2p[i] = pk(v.x * kLog2e, v.y * kLog2e);
-        }
-        if (m.y & kStagedFlag) {
-          const unsigned char* pp = params + (size_t(ring) * STAGES + slot) * G::kParamBytes;
-          bias = a.bias ? reinterpret_cast<const float*>(pp + kRowsP * kN * 4)[r] : 0.f;
-          Dc = a.D ? reinterpret_cast<const float*>(pp + kRowsP * kN * 4 + kRowsP * 4)[r] : 0.f;
-        } else {
-          bias = a.bias ? a.bias[cc] : 0.f;
-          Dc = a.D ? a.D[cc] : 0.f;
-        }
-      } else if (m.y & kStagedFlag) {
+      if (m.y & kStagedFlag) {
         // staged by the producer with this box (shared memory: no global round trip)
-        const unsigned char* pp = params + (size_t(ring) * STAGES + slot) * G::kParamBytes;
+        const unsigned char* pp = params + (size_t(warp) * STAGES + slot) * G::kParamBytes;
 #pragma unroll
         for (int s = 0; s < kN / 2; s += 4) {
           const float4 q = *reinterpret_cast<const float4*>(pp + (r * kN + 8 * hf + s) * 4);
@@ -1210,33 +1069,9 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
       }
       const float* src = nullptr;
       if (cur.seg == 0) {
-        src = a.h0 ? a.h0 + size_t(row) * kN + so : nullptr;
+        src = a.h0 ? a.h0 + size_t(row) * kN + 8 * hf : nullptr;
       }
-      if (QUAD && cur.seg == 0) {
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          float2 v = make_float2(0.f, 0.f);
-          if (src) v = __ldcg(reinterpret_cast<const float2*>(src + 4 * i));
-          h2[i] = pk(v.x, v.y);
-        }
-      } else if (QUAD) {
-        const unsigned long long* w64 = a.tcarry + (size_t(cur.tile) * kRowsP + r) * kN + so;
-        const unsigned want = a.epoch + static_cast<unsigned>(cur.seg);
-        unsigned long long w[4];
-        for (;;) {
-          ld_relaxed_u64x2(w64, w[0], w[1]);
-          ld_relaxed_u64x2(w64 + 4, w[2], w[3]);
-          bool ok = true;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) ok &= static_cast<unsigned>(w[i] >> 32) == want;
-          if (__all_sync(0xffffffffu, ok)) break;
-          __nanosleep(64);
-        }
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-          h2[i] = pk(__uint_as_float(static_cast<unsigned>(w[2 * i])),
-                     __uint_as_float(static_cast<unsigned>(w[2 * i + 1])));
-      } else if (cur.seg == 0) {
+      if (cur.seg == 0) {
 #pragma unroll
         for (int s = 0; s < kN / 2; s += 4) {
           float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1272,10 +1107,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
 
     const int tbox = cur.t0 + box * BOX;
     float* ydst = row_valid ? a.out + size_t(row) * a.L + tbox : nullptr;
-    if (QUAD)
-      quad_box<BOX, SP, HZ>(wbase + slot * G::kStageBytes, ydst, r, q, min(BOX, L - tbox), bias,
-                            Dc, A2p, h2);
-    else if (PIPE == 1 && tbox + BOX <= L)
+    if (PIPE == 1 && tbox + BOX <= L)
       pair_box_pipe<BOX, SP, HZ>(wbase + slot * G::kStageBytes, ydst, r, hf, bias, Dc, A2p, h2);
     else
       pair_box<BOX, SP, HZ>(wbase + slot * G::kStageBytes, ydst, r, hf, min(BOX, L - tbox), bias,
@@ -1283,24 +1115,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(wempty + slot);  // stage consumed: producer may refill
 
-    if (QUAD && box == cur.nbox - 1) {
-      float hs[4];
-      upk(h2[0], hs[0], hs[1]);
-      upk(h2[1], hs[2], hs[3]);
-      if (cur.seg == n_seg - 1) {
-        if (a.h_last && row_valid) {
-          float* dst = a.h_last + size_t(row) * kN + so;
-          __stcg(reinterpret_cast<float2*>(dst), make_float2(hs[0], hs[1]));
-          __stcg(reinterpret_cast<float2*>(dst + 4), make_float2(hs[2], hs[3]));
-        }
-      } else {
-        unsigned long long* w64 = a.tcarry + (size_t(cur.tile) * kRowsP + r) * kN + so;
-        const unsigned long long tag =
-            static_cast<unsigned long long>(a.epoch + static_cast<unsigned>(cur.seg + 1)) << 32;
-        st_relaxed_u64x2(w64, tag | __float_as_uint(hs[0]), tag | __float_as_uint(hs[1]));
-        st_relaxed_u64x2(w64 + 4, tag | __float_as_uint(hs[2]), tag | __float_as_uint(hs[3]));
-      }
-    } else if (box == cur.nbox - 1) {
+    if (box == cur.nbox - 1) {
       float hs[kN / 2];
 #pragma unroll
       for (int i = 0; i < kP; ++i) upk(h2[i], hs[2 * i], hs[2 * i + 1]);
@@ -1412,7 +1227,7 @@ int grow(cl_ctx* ctx, T** ptr, size_t* have, size_t need, const char* what) {
 }
 
 // ---- kernel table (CL_SCAN_CFG=<index> selects a row, for experiments) ----
-enum ScanKind { kWarpSpecPair = 0, kRowSeq = 1, kWarpSpecPairNoPipe = 2, kWarpSpecQuad = 3 };
+enum ScanKind { kWarpSpecPair = 0, kRowSeq = 1, kWarpSpecPairNoPipe = 2 };
 struct ScanCfg {
   int kind, box, warps, stages;
 };
@@ -1435,11 +1250,11 @@ constexpr ScanCfg kCfgs[] = {
     {kWarpSpecPair, 16, 7, 3},
     {kWarpSpecPairNoPipe, 16, 12, 2},  // 8: row 0 without the group software pipeline (A/B)
     {kWarpSpecPair, 16, 14, 2},        // 9: 14 consumers (the previous default)
-    // few tiles, quad layout: a warp pair per tile (warps = 2 x tiles per CTA)
-    {kWarpSpecQuad, 16, 2, 4},   // 10
-    {kWarpSpecQuad, 16, 4, 4},   // 11
-    {kWarpSpecQuad, 16, 8, 4},   // 12
-    {kWarpSpecQuad, 16, 14, 3},  // 13
+    // A quad layout for few tiles (a warp pair per 16-row tile, four lanes per row, each
+    // lane's chain a canonical ya / yb, bitwise equal to the lane pair) was measured
+    // slower: C1 0.26 vs 0.17 ms, C2 0.49 vs 0.30 -- the per-lane elementwise work
+    // (softplus, SiLU, exchanges) does not shrink with the lane's state count, so the
+    // instruction count went up 1.8x on latency-bound lone warps (commit history).
 };
 constexpr int kDefaultCfg = 0;
 
@@ -1460,17 +1275,15 @@ int grid_for(int n_tiles, int warps, int num_sms) {
   return max_useful < num_sms ? (max_useful < 1 ? 1 : max_useful) : num_sms;
 }
 
-template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int PIPE = 1, int NP = 0,
-          bool QUAD = false>
+template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int PIPE = 1, int NP = 0>
 cudaError_t launch_ws(const CUtensorMap (&m)[6], const TmaArgs& t, int num_sms, cudaStream_t s) {
-  constexpr int kRings = QUAD ? WARPS / 2 : WARPS;
-  constexpr int kProducers = NP > 0 ? NP : producers_for<kRings>();
-  auto kern = rowpair_ws_kernel<BOX, WARPS, STAGES, SP, HZ, kProducers, PIPE, QUAD>;
-  const size_t smem = size_t(kRings) * STAGES * (GeoP<BOX>::kStageBytes + GeoP<BOX>::kParamBytes) +
-                      1024 + size_t(kRings) * STAGES * (16 + 8);
+  constexpr int kProducers = NP > 0 ? NP : producers_for<WARPS>();
+  auto kern = rowpair_ws_kernel<BOX, WARPS, STAGES, SP, HZ, kProducers, PIPE>;
+  const size_t smem = size_t(WARPS) * STAGES * (GeoP<BOX>::kStageBytes + GeoP<BOX>::kParamBytes) +
+                      1024 + size_t(WARPS) * STAGES * (16 + 8);
   cudaError_t e = set_smem(kern, smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid_for(t.n_tiles, kRings, num_sms), (WARPS + kProducers) * 32, smem, s>>>(
+  kern<<<grid_for(t.n_tiles, WARPS, num_sms), (WARPS + kProducers) * 32, smem, s>>>(
       m[0], m[1], m[2], m[4], t);
   return cudaGetLastError();
 }
@@ -1485,15 +1298,6 @@ cudaError_t launch_rowseq(const CUtensorMap (&m)[6], const TmaArgs& t, int num_s
   kern<<<grid_for(t.n_tiles, WARPS, num_sms), WARPS * 32, smem, s>>>(m[0], m[1], m[2], m[3],
                                                                       m[4], m[5], t);
   return cudaGetLastError();
-}
-
-template <int BOX, int WARPS, int STAGES>
-cudaError_t dispatch_quad(bool sp, bool hz, const CUtensorMap (&m)[6], const TmaArgs& t, int n,
-                          cudaStream_t s) {
-  if (sp && hz) return launch_ws<BOX, WARPS, STAGES, true, true, 1, 0, true>(m, t, n, s);
-  if (sp) return launch_ws<BOX, WARPS, STAGES, true, false, 1, 0, true>(m, t, n, s);
-  if (hz) return launch_ws<BOX, WARPS, STAGES, false, true, 1, 0, true>(m, t, n, s);
-  return launch_ws<BOX, WARPS, STAGES, false, false, 1, 0, true>(m, t, n, s);
 }
 
 // softplus / z-gate are compile-time switches: four instantiations per geometry
@@ -1640,10 +1444,6 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
                      : dispatch<true, 16, 12, 2>(sp, hz, m, t, n, s);
         break;
       case 9: e = dispatch<true, 16, 14, 2>(sp, hz, m, t, n, s); break;
-      case 10: e = dispatch_quad<16, 2, 4>(sp, hz, m, t, n, s); break;
-      case 11: e = dispatch_quad<16, 4, 4>(sp, hz, m, t, n, s); break;
-      case 12: e = dispatch_quad<16, 8, 4>(sp, hz, m, t, n, s); break;
-      case 13: e = dispatch_quad<16, 14, 3>(sp, hz, m, t, n, s); break;
       default: e = dispatch<true, 16, 12, 2>(sp, hz, m, t, n, s); break;
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
