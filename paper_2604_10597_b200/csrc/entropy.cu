@@ -1190,6 +1190,8 @@ constexpr int kTokHWarps = 4;               // hist: warps per block, 32 positio
 // with 8; histogram 0.98 / 0.72 / 0.53 / 0.47 / 0.77 ms for 4 / 8 /
 // 16 / 24 / 32 rows (32: 182 registers, 2 blocks per SM).  Loads in flight, not
 // instructions, bound the histogram: a lane reads 4 bytes of a row, a warp 128 bytes.
+// Giving the block's warps 2 or 4 adjacent 32-position slices (256 / 512 contiguous bytes
+// of a row per block step, as in the min/max kernel) measured slower: 0.51 / 0.56 ms.
 #ifndef CL_TOK_MM_COLS
 #define CL_TOK_MM_COLS 4
 #endif
