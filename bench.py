@@ -166,6 +166,25 @@ def cpu_reference_step(lib_kind, x_host, dim, L, N, threads, ref, port):
     return dt, chunk, raw
 
 
+def cpu_single_thread(ref, x, dim, L, rows=256):
+    """The reference exactly as shipped (one thread): entropy + rule over one batch's u,
+    the scan over `rows` of its channels, scan time scaled to all channels (rows are
+    independent and equal work)."""
+    u = x["u"]
+    t0 = time.perf_counter()
+    masses, lo, hi, n = ref.histogram_masses(u.reshape(-1), 256, 1e-8, 1)
+    raw, _ = ref.entropy(masses)
+    ref.select_chunk(raw, 32, 512, np.log(256.0))
+    t1 = time.perf_counter()
+    ref.mamba1_f32(u, x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"], x["delta_bias"],
+                   True, rows=(0, rows), threads=1)
+    t2 = time.perf_counter()
+    total = (t1 - t0) + (t2 - t1) * dim / rows
+    return {"value": L / total, "unit": "tokens/s", "cores": 1,
+            "sample": f"entropy + rule over 1 batch ({dim} x {L}) {t1 - t0:.2f} s; fp64 "
+                      f"Mamba-1 scan of {rows} of {dim} rows {t2 - t1:.2f} s, scaled x{dim / rows:g}"}
+
+
 def _port_mamba_threaded(port, x, dim, L, N, threads):
     from concurrent.futures import ThreadPoolExecutor
     per = (dim + threads - 1) // threads
@@ -448,6 +467,8 @@ def main():
                 "value": L / dt, "unit": "tokens/s", "cores": threads, "kind": kind,
                 "sample": f"1 batch of {args.config} ({dim} x {L}): entropy + rule + fp64 "
                           f"Mamba-1 scan, {threads} threads, {dt:.2f} s"}
+            if kind == "reference":
+                result["cpu_baseline"]["single_thread"] = cpu_single_thread(ref, xh, dim, L)
         except Exception as e:  # the baseline must never take the bench down
             result["cpu_baseline"] = {"value": None, "error": str(e)}
 
