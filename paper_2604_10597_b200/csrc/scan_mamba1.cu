@@ -1255,6 +1255,11 @@ constexpr ScanCfg kCfgs[] = {
     // slower: C1 0.26 vs 0.17 ms, C2 0.49 vs 0.30 -- the per-lane elementwise work
     // (softplus, SiLU, exchanges) does not shrink with the lane's state count, so the
     // instruction count went up 1.8x on latency-bound lone warps (commit history).
+    {kWarpSpecPair, 32, 1, 4},  // 10: few tiles, 32-timestep boxes (half the per-box overhead)
+    {kWarpSpecPair, 32, 2, 4},  // 11
+    {kWarpSpecPair, 32, 4, 3},  // 12
+    {kWarpSpecPair, 32, 8, 2},  // 13
+    {kWarpSpecPair, 32, 6, 3},  // 14
 };
 constexpr int kDefaultCfg = 0;
 
@@ -1332,10 +1337,15 @@ int scan_cfg_index(uint64_t pair_tiles, int num_sms, int variant) {
   }();
   if (forced >= 0) return forced;
   const uint64_t per_sm = (pair_tiles + num_sms - 1) / num_sms;
-  if (per_sm <= 1) return 4;
-  if (per_sm <= 2) return 5;
-  if (per_sm <= 4) return 6;
-  if (per_sm <= 7) return 7;
+  // Below ~11 tiles per SM, 32-timestep boxes (half the per-box pipeline fill and barrier
+  // round trips) with the fewest consumers per CTA that still cover the tiles in about one
+  // wave.  Measured (scan ms, tools/cfg_ab.py): C1 (96 tiles) 0.167 -> 0.152 (row 11);
+  // C2 (128) 0.301 -> 0.269 (11); 512 tiles 0.327 -> 0.309 (12); 768: 0.453 -> 0.388 (12);
+  // 1280: 0.634 -> 0.521 (13); 1792 and C3's 2048 stay with row 0 (0.649 vs 0.708, 1.376
+  // vs 1.530 for row 13).
+  if (per_sm <= 2) return 11;
+  if (per_sm <= 6) return 12;
+  if (per_sm <= 10) return 13;
   return kDefaultCfg;  // 12 consumers
 }
 
@@ -1444,6 +1454,11 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
                      : dispatch<true, 16, 12, 2>(sp, hz, m, t, n, s);
         break;
       case 9: e = dispatch<true, 16, 14, 2>(sp, hz, m, t, n, s); break;
+      case 10: e = dispatch<true, 32, 1, 4>(sp, hz, m, t, n, s); break;
+      case 11: e = dispatch<true, 32, 2, 4>(sp, hz, m, t, n, s); break;
+      case 12: e = dispatch<true, 32, 4, 3>(sp, hz, m, t, n, s); break;
+      case 13: e = dispatch<true, 32, 8, 2>(sp, hz, m, t, n, s); break;
+      case 14: e = dispatch<true, 32, 6, 3>(sp, hz, m, t, n, s); break;
       default: e = dispatch<true, 16, 12, 2>(sp, hz, m, t, n, s); break;
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");

@@ -154,7 +154,7 @@ def test_parameter_staging_paths_bitwise(cuda):
 
 # TMA kernel table rows (scan_mamba1.cu kCfgs): 0/4-7/9 lane pair, 8 lane pair without the
 # group pipeline, 1-3 row kernels
-PAIR_CFGS = [0, 4, 5, 6, 7, 8, 9]
+PAIR_CFGS = [0, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14]  # 10-14: 32-timestep boxes
 ROW_CFGS = [1, 2, 3]
 
 
