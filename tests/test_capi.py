@@ -57,3 +57,22 @@ def test_kernels_are_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
+
+
+def test_enum_constants_match_the_header():
+    """The Python constants mirror the header's enums (a drift would silently select the
+    wrong kernel or policy)."""
+    src = open(HEADER).read()
+    for name in ("CL_SCAN_AUTO", "CL_SCAN_ROWSEQ_TMA", "CL_SCAN_GENERIC", "CL_SCAN_CONFIG_BASE"):
+        m = re.search(rf"\b{name}\s*=\s*(\d+)", src)
+        assert m, name
+        assert getattr(_lib, name) == int(m.group(1)), name
+
+
+def test_scan_variant_codes():
+    from paper_2604_10597_b200.mamba1 import _variant_code
+    assert _variant_code("auto") == _lib.CL_SCAN_AUTO
+    assert _variant_code("generic") == _lib.CL_SCAN_GENERIC
+    assert _variant_code("cfg:11") == _lib.CL_SCAN_CONFIG_BASE + 11
+    with pytest.raises(KeyError):
+        _variant_code("nope")
