@@ -1238,6 +1238,9 @@ constexpr ScanCfg kCfgs[] = {
     // 1.404 -- the uneven sub-partitions made warps wait on each other's carries (ncu:
     // carry-spin samples 2.7% -> 0.3%); 16 (capped at 96 registers, spills): 1.726;
     // 12 x 3 stages 1.371; 8 consumers 1.497; 12 with 1 producer 1.572, with 3: 1.371.
+    // 16 consumers + a producer warpgroup that hands its registers over with setmaxnreg
+    // (consumers 112, producers 24; no hot-loop spills): 1.654 -- more warps per SMSP do
+    // not buy MUFU issue once each has fewer registers for the group pipeline.
     {kWarpSpecPair, 16, 12, 2},
     {kRowSeq, 32, 4, 3},         // 32-row tiles, self-fed TMA rings
     {kRowSeq, 16, 8, 3},
