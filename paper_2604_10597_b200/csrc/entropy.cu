@@ -1297,7 +1297,8 @@ constexpr int kTokHWarps = 4;               // hist: warps per block, 32 positio
 // 16 / 24 / 32 rows (32: 182 registers, 2 blocks per SM).  Loads in flight, not
 // instructions, bound the histogram: a lane reads 4 bytes of a row, a warp 128 bytes.
 // Giving the block's warps 2 or 4 adjacent 32-position slices (256 / 512 contiguous bytes
-// of a row per block step, as in the min/max kernel) measured slower: 0.51 / 0.56 ms.
+// of a row per block step, as in the min/max kernel) measured slower: 0.51 / 0.56 ms; so
+// did bulk L2 prefetches of each warp's row segments 1-4 batches ahead: 0.59-0.61 ms.
 #ifndef CL_TOK_MM_COLS
 #define CL_TOK_MM_COLS 4
 #endif
