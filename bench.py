@@ -37,6 +37,9 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# single-GPU step: histogram + decision as one launch (cl_histogram_decide_f32);
+# CL_BENCH_SEPARATE_DECIDE=1 times the separate decide kernel instead (A/B)
+FUSED_DECIDE = os.environ.get("CL_BENCH_SEPARATE_DECIDE", "0") != "1"
 sys.path.insert(0, ROOT)
 
 METRIC = "selective-scan tokens/s & HBM GB/s (% roofline) at 1/2/4/8 B200 vs CPU ref"
@@ -332,10 +335,17 @@ def main():
             pf.stage_minmax(uf, g0)
             if ev:
                 ev[1].record()
-            pf.stage_histogram(uf, g0)
-            if ev:
-                ev[2].record()
-            pf.stage_decide(n_total, L)
+            if FUSED_DECIDE:
+                # histogram + decision in one launch (its last CTA decides): stage
+                # "histogram" includes the decision, "decide" is the empty interval
+                pf.stage_histogram_decide(uf, L)
+                if ev:
+                    ev[2].record()
+            else:
+                pf.stage_histogram(uf, g0)
+                if ev:
+                    ev[2].record()
+                pf.stage_decide(n_total, L)
             if ev:
                 ev[3].record()
         pf.stage_scan(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"],

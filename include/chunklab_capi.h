@@ -174,6 +174,20 @@ int cl_decide(cl_ctx* ctx, const uint64_t* d_counts, const double* d_range,
               const cl_hist_spec* spec, uint64_t n_samples_total, const cl_rule_spec* rule,
               uint64_t seq_len, cl_decision* d_decision, void* stream);
 
+/* Stages 2+3 in one launch for a single-GPU call (no collective between them):
+ * cl_histogram_f32 over all n values (global_offset 0) followed by cl_decide with
+ * n_samples_total = ceil(n / stride), same results bit for bit.  Where the
+ * register-fed histogram applies (K <= 256, Dynamic range, stride 1, n >= 4096) its
+ * last CTA writes the decision; otherwise the two kernels run back to back.
+ * d_range must come from cl_range_init + cl_minmax_f32 of this call: its spare word
+ * d_range[3] is the CTAs' arrival ticket (left at 0).  d_counts zeroed as for
+ * cl_histogram_f32.  Replaces the compute_histogram -> estimate_entropy ->
+ * select_chunk sequence of entropy.hpp:101-174 / chunk.hpp:68-89. */
+int cl_histogram_decide_f32(cl_ctx* ctx, const float* d_values, uint64_t n,
+                            const cl_hist_spec* spec, const double* d_range, uint64_t* d_counts,
+                            const cl_rule_spec* rule, uint64_t seq_len, cl_decision* d_decision,
+                            void* stream);
+
 /* Stage 4: fused Mamba-1 selective scan (fp32), chunk read from d_decision.
  * Layouts (mamba_ssm selective_scan_fn): u, delta, z, out: (batch, dim, L)
  * row-major; A: (dim, N); B, C: (batch, N, L); D, delta_bias: (dim) or NULL;

@@ -105,6 +105,8 @@ SIGNATURES = {
     "cl_histogram_f64": (C.c_int, [_P, _P, _u64, _u64, C.POINTER(cl_hist_spec), _P, _P, _P]),
     "cl_decide": (C.c_int, [_P, _P, _P, C.POINTER(cl_hist_spec), _u64, C.POINTER(cl_rule_spec),
                             _u64, _P, _P]),
+    "cl_histogram_decide_f32": (C.c_int, [_P, _P, _u64, C.POINTER(cl_hist_spec), _P, _P,
+                                          C.POINTER(cl_rule_spec), _u64, _P, _P]),
     "cl_token_entropy_f32": (C.c_int, [_P, _P, _u64, _u64, C.POINTER(cl_hist_spec), _P, _P]),
     "cl_token_range_init": (C.c_int, [_P, _P, _u64, _P]),
     "cl_token_minmax_f32": (C.c_int, [_P, _P, _u64, _u64, _u64, _u64, _P, _P]),

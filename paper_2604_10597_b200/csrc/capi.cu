@@ -144,6 +144,10 @@ uint64_t samples_of(uint64_t n, uint64_t stride) { return n == 0 ? 0 : (n + stri
 
 using namespace cl;
 
+#ifndef CL_HIST_FUSE
+#define CL_HIST_FUSE 1
+#endif
+
 extern "C" {
 
 int cl_abi_version(void) { return CL_ABI_VERSION; }
@@ -303,6 +307,33 @@ int cl_histogram_f64(cl_ctx* ctx, const double* d_values, uint64_t n, uint64_t g
                                        ctx->num_sms, static_cast<cudaStream_t>(stream), &l);
   ctx->launches += l;
   return check_launch(ctx, e, "histogram_f64");
+}
+
+int cl_histogram_decide_f32(cl_ctx* ctx, const float* d_values, uint64_t n,
+                            const cl_hist_spec* spec, const double* d_range, uint64_t* d_counts,
+                            const cl_rule_spec* rule, uint64_t seq_len, cl_decision* d_decision,
+                            void* stream) {
+  int rc = validate_spec(ctx, spec);
+  if (rc) return rc;
+  rc = validate_rule(ctx, rule);
+  if (rc) return rc;
+  if (!d_values || !d_range || !d_counts || !d_decision)
+    return fail(ctx, CL_E_INVALID, "null argument");
+  if (n == 0) return fail(ctx, CL_E_INVALID, "no samples");
+  bool fused = false;
+  {
+    DeviceGuard g(ctx->device);
+    const HistFuse fz{samples_of(n, spec->sample_stride), rule, seq_len, d_decision};
+    int l = 0;
+    cudaError_t e = launch_histogram_f32(d_values, n, 0, *spec, d_range, d_counts, ctx->num_sms,
+                                         static_cast<cudaStream_t>(stream), &l,
+                                         CL_HIST_FUSE ? &fz : nullptr, &fused);
+    ctx->launches += l;
+    if ((rc = check_launch(ctx, e, "histogram_f32"))) return rc;
+  }
+  if (fused) return CL_OK;
+  return cl_decide(ctx, d_counts, d_range, spec, samples_of(n, spec->sample_stride), rule,
+                   seq_len, d_decision, stream);
 }
 
 int cl_decide(cl_ctx* ctx, const uint64_t* d_counts, const double* d_range,
@@ -527,9 +558,8 @@ int cl_prefill_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_hist_spec* 
   if ((rc = cl_range_init(ctx, d_range, stream))) return rc;
   if ((rc = cl_minmax_f32(ctx, args->u, n, 0, spec->sample_stride, d_range, stream))) return rc;
   if ((rc = cl_counts_zero(ctx, d_counts, spec->bin_count, stream))) return rc;
-  if ((rc = cl_histogram_f32(ctx, args->u, n, 0, spec, d_range, d_counts, stream))) return rc;
-  if ((rc = cl_decide(ctx, d_counts, d_range, spec, samples_of(n, spec->sample_stride), rule,
-                      args->seq_len, d_decision, stream)))
+  if ((rc = cl_histogram_decide_f32(ctx, args->u, n, spec, d_range, d_counts, rule,
+                                     args->seq_len, d_decision, stream)))
     return rc;
   return cl_selective_scan_f32(ctx, args, d_decision, 0, CL_SCAN_AUTO, stream);
 }

@@ -57,10 +57,19 @@ cudaError_t launch_minmax_f32(const float* v, uint64_t n, uint64_t g0, uint64_t 
                               double* d_range, int num_sms, cudaStream_t s, int* launches);
 cudaError_t launch_minmax_f64(const double* v, uint64_t n, uint64_t g0, uint64_t stride,
                               double* d_range, int num_sms, cudaStream_t s, int* launches);
+// Histogram + decision in one launch (single-GPU prefill): the decision's inputs
+// beyond the histogram's own.  The caller's range[3] must be 0 (range_init).
+struct HistFuse {
+  uint64_t n_samples;
+  const cl_rule_spec* rule;
+  uint64_t seq_len;
+  cl_decision* d_out;
+};
 cudaError_t launch_histogram_f32(const float* v, uint64_t n, uint64_t g0,
                                  const cl_hist_spec& spec, const double* d_range,
                                  uint64_t* d_counts, int num_sms, cudaStream_t s,
-                                 int* launches);
+                                 int* launches, const HistFuse* fuse = nullptr,
+                                 bool* fused = nullptr);
 cudaError_t launch_histogram_f64(const double* v, uint64_t n, uint64_t g0,
                                  const cl_hist_spec& spec, const double* d_range,
                                  uint64_t* d_counts, int num_sms, cudaStream_t s,

@@ -762,127 +762,8 @@ __global__ void __launch_bounds__(kHistThreads, kHistCtasPerSm)
 #ifndef CL_HIST_REG_PF
 #define CL_HIST_REG_PF 3
 #endif
-constexpr int kRegWarps = 16;
-constexpr int kRegChunk = 32 * kLaneSamples;  // floats per warp-chunk
-constexpr size_t kRegSmem = size_t(kRegWarps) * kLaneBins * kBinStride + kLaneBins * 4 + 64;
-
-__global__ void __launch_bounds__(kRegWarps * 32, 1)
-    hist_f32_reg_kernel(const float* __restrict__ v, uint64_t n, int range_mode, double fixed_lo,
-                        double fixed_hi, int k, const double* __restrict__ d_range,
-                        unsigned long long* d_counts) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  cnt_t* counters = reinterpret_cast<cnt_t*>(smem);
-  uint32_t* cta_hist = reinterpret_cast<uint32_t*>(smem + size_t(kRegWarps) * kLaneBins * kBinStride);
-  __shared__ BinParams sp;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (threadIdx.x == 0) sp = make_bin_params(d_range, range_mode, fixed_lo, fixed_hi, k);
-  {
-    uint4* c4 = reinterpret_cast<uint4*>(smem);
-    for (int i = threadIdx.x; i < static_cast<int>(size_t(kRegWarps) * kLaneBins * kBinStride / 16);
-         i += blockDim.x)
-      c4[i] = make_uint4(0, 0, 0, 0);
-    for (int i = threadIdx.x; i < kLaneBins; i += blockDim.x) cta_hist[i] = 0;
-  }
-  __syncthreads();
-  const BinParams p = sp;
-  unsigned char* lane_base = reinterpret_cast<unsigned char*>(counters + warp * kLaneBins * 32) + lane * 4;
-
-  const uint64_t head = umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
-  const float* body = v + head;
-  const uint64_t nwc = (n - head) / kRegChunk;  // full warp-chunks
-  const uint64_t tail0 = head + nwc * kRegChunk;
-  if (blockIdx.x == 0 && warp == 0) {
-    for (uint64_t i = lane; i < head; i += 32) cref(lane_base, bin_f32(v[i], p, false)) += 1;
-    for (uint64_t i = tail0 + lane; i < n; i += 32) cref(lane_base, bin_f32(v[i], p, false)) += 1;
-    // up to 3 + 16 samples per lane: flush now so the chunk loop's budget is untouched
-    flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
-  }
-  const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * kRegWarps;
-  uint64_t c = static_cast<uint64_t>(blockIdx.x) * kRegWarps + warp;
-  if (lane == 0) {
-#pragma unroll 1
-    for (int d = 0; d < CL_HIST_REG_PF; ++d) {
-      const uint64_t pc = c + d * wstride;
-      if (pc < nwc) bulk_prefetch_l2(body + pc * kRegChunk, kRegChunk * 4);
-    }
-  }
-  float4 nx[kLaneF4];
-  if (c < nwc) {
-    const float4* src = reinterpret_cast<const float4*>(body + c * kRegChunk);
-#pragma unroll
-    for (int j = 0; j < kLaneF4; ++j) nx[j] = __ldcs(src + j * 32 + lane);
-  }
-  uint32_t since_flush = 0;
-  for (; c < nwc; c += wstride) {
-    float val[kLaneSamples];
-#pragma unroll
-    for (int j = 0; j < kLaneF4; ++j) {
-      val[4 * j] = nx[j].x;
-      val[4 * j + 1] = nx[j].y;
-      val[4 * j + 2] = nx[j].z;
-      val[4 * j + 3] = nx[j].w;
-    }
-    const uint64_t cn = c + wstride;
-    if (cn < nwc) {
-      const float4* src = reinterpret_cast<const float4*>(body + cn * kRegChunk);
-#pragma unroll
-      for (int j = 0; j < kLaneF4; ++j) nx[j] = __ldcs(src + j * 32 + lane);
-    }
-    if (lane == 0) {
-      const uint64_t pc = c + CL_HIST_REG_PF * wstride;
-      if (pc < nwc) bulk_prefetch_l2(body + pc * kRegChunk, kRegChunk * 4);
-    }
-    lane_count_u8(val, p, reinterpret_cast<unsigned char*>(counters), warp, lane);
-    if (++since_flush == kFlushChunks) {
-      flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
-      since_flush = 0;
-    }
-  }
-  flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
-  __syncthreads();
-  for (int b = threadIdx.x; b < k; b += blockDim.x)
-    if (cta_hist[b]) atomicAdd(d_counts + b, static_cast<unsigned long long>(cta_hist[b]));
-}
-
-
-// K > 256 (or f64 input): shared-memory atomics on a CTA histogram.
-template <typename T, int MODE>
-__global__ void __launch_bounds__(kThreads)
-    hist_atomic_kernel(const T* __restrict__ v, uint64_t n, uint64_t g0, uint64_t stride,
-                       int range_mode, double fixed_lo, double fixed_hi, int k,
-                       const double* __restrict__ d_range, unsigned long long* d_counts,
-                       int use_smem) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);
-  __shared__ BinParams sp;
-  if (threadIdx.x == 0) sp = make_bin_params(d_range, range_mode, fixed_lo, fixed_hi, k);
-  if (use_smem)
-    for (int i = threadIdx.x; i < k; i += blockDim.x) hist[i] = 0;
-  __syncthreads();
-  const BinParams p = sp;
-  const uint64_t nthr = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += nthr) {
-    if (!sampled<MODE>(g0 + i, stride)) continue;
-    int b;
-    if constexpr (sizeof(T) == 4)
-      b = bin_f32(v[i], p, range_mode == CL_RANGE_FIXED);
-    else
-      b = bin_index_exact(v[i], p.lo, p.width, k);
-    if (use_smem)
-      atomicAdd(hist + b, 1u);
-    else
-      atomicAdd(d_counts + b, 1ull);
-  }
-  if (use_smem) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < k; i += blockDim.x)
-      if (hist[i]) atomicAdd(d_counts + i, static_cast<unsigned long long>(hist[i]));
-  }
-}
-
 // ---------------------------------------------------------------------------
-// Stage 3: entropy + rule + policy (one CTA).
+// Stage 3: entropy + rule + policy (one CTA, or the histogram's last CTA).
 // ---------------------------------------------------------------------------
 struct DecideArgs {
   const unsigned long long* counts;  // may be null (host-features mode)
@@ -983,7 +864,11 @@ __device__ int decide_simple(const DecideArgs& a, int kind, int static_chunk, do
   return 0;
 }
 
-__global__ void __launch_bounds__(kThreads) decide_kernel(DecideArgs a, cl_decision* d_out) {
+// The decision of one CTA (blockDim.x >= kThreads; the first kThreads threads form the
+// bin terms).  COHERENT: counts were accumulated by other CTAs of the same grid (the
+// histogram's last CTA), so they are read from L2.
+template <bool COHERENT>
+__device__ void decide_block(const DecideArgs& a, cl_decision* d_out) {
   __shared__ double terms[kThreads];
   cl_decision out = {};
   out.margin = 1.0;
@@ -997,11 +882,12 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(DecideArgs a, cl_decis
     for (int base = 0; base < a.k; base += kThreads) {
       const int b = base + threadIdx.x;
       double t = 0.0;
-      if (b < a.k) {
-        const double pm = __dmul_rn(static_cast<double>(a.counts[b]), inv_n);
+      if (threadIdx.x < kThreads && b < a.k) {
+        const unsigned long long cb = COHERENT ? __ldcg(a.counts + b) : a.counts[b];
+        const double pm = __dmul_rn(static_cast<double>(cb), inv_n);
         if (pm > 0.0) t = __dmul_rn(pm, log(__dadd_rn(pm, a.epsilon)));
       }
-      terms[threadIdx.x] = t;
+      if (threadIdx.x < kThreads) terms[threadIdx.x] = t;
       __syncthreads();
       if (threadIdx.x == 0) {
         // raw -= p*log(p+eps) in bin order (entropy.hpp:154-156).  Empty bins hold +0.0
@@ -1069,6 +955,146 @@ __global__ void __launch_bounds__(kThreads) decide_kernel(DecideArgs a, cl_decis
   }
   out.status = status;
   *d_out = out;
+}
+
+__global__ void __launch_bounds__(kThreads) decide_kernel(DecideArgs a, cl_decision* d_out) {
+  decide_block<false>(a, d_out);
+}
+
+constexpr int kRegWarps = 16;
+constexpr int kRegChunk = 32 * kLaneSamples;  // floats per warp-chunk
+constexpr size_t kRegSmem = size_t(kRegWarps) * kLaneBins * kBinStride + kLaneBins * 4 + 64;
+
+// FUSE: the CTA that finishes last (an arrival ticket in the range's spare word
+// range[3], zeroed by range_init and reset here) also runs the decision, so the
+// single-GPU prefill has no separate decide launch.
+template <bool FUSE>
+__global__ void __launch_bounds__(kRegWarps * 32, 1)
+    hist_f32_reg_kernel(const float* __restrict__ v, uint64_t n, int range_mode, double fixed_lo,
+                        double fixed_hi, int k, const double* __restrict__ d_range,
+                        unsigned long long* d_counts, DecideArgs da, cl_decision* d_out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  cnt_t* counters = reinterpret_cast<cnt_t*>(smem);
+  uint32_t* cta_hist = reinterpret_cast<uint32_t*>(smem + size_t(kRegWarps) * kLaneBins * kBinStride);
+  __shared__ BinParams sp;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) sp = make_bin_params(d_range, range_mode, fixed_lo, fixed_hi, k);
+  {
+    uint4* c4 = reinterpret_cast<uint4*>(smem);
+    for (int i = threadIdx.x; i < static_cast<int>(size_t(kRegWarps) * kLaneBins * kBinStride / 16);
+         i += blockDim.x)
+      c4[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < kLaneBins; i += blockDim.x) cta_hist[i] = 0;
+  }
+  __syncthreads();
+  const BinParams p = sp;
+  unsigned char* lane_base = reinterpret_cast<unsigned char*>(counters + warp * kLaneBins * 32) + lane * 4;
+
+  const uint64_t head = umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
+  const float* body = v + head;
+  const uint64_t nwc = (n - head) / kRegChunk;  // full warp-chunks
+  const uint64_t tail0 = head + nwc * kRegChunk;
+  if (blockIdx.x == 0 && warp == 0) {
+    for (uint64_t i = lane; i < head; i += 32) cref(lane_base, bin_f32(v[i], p, false)) += 1;
+    for (uint64_t i = tail0 + lane; i < n; i += 32) cref(lane_base, bin_f32(v[i], p, false)) += 1;
+    // up to 3 + 16 samples per lane: flush now so the chunk loop's budget is untouched
+    flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+  }
+  const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * kRegWarps;
+  uint64_t c = static_cast<uint64_t>(blockIdx.x) * kRegWarps + warp;
+  if (lane == 0) {
+#pragma unroll 1
+    for (int d = 0; d < CL_HIST_REG_PF; ++d) {
+      const uint64_t pc = c + d * wstride;
+      if (pc < nwc) bulk_prefetch_l2(body + pc * kRegChunk, kRegChunk * 4);
+    }
+  }
+  float4 nx[kLaneF4];
+  if (c < nwc) {
+    const float4* src = reinterpret_cast<const float4*>(body + c * kRegChunk);
+#pragma unroll
+    for (int j = 0; j < kLaneF4; ++j) nx[j] = __ldcs(src + j * 32 + lane);
+  }
+  uint32_t since_flush = 0;
+  for (; c < nwc; c += wstride) {
+    float val[kLaneSamples];
+#pragma unroll
+    for (int j = 0; j < kLaneF4; ++j) {
+      val[4 * j] = nx[j].x;
+      val[4 * j + 1] = nx[j].y;
+      val[4 * j + 2] = nx[j].z;
+      val[4 * j + 3] = nx[j].w;
+    }
+    const uint64_t cn = c + wstride;
+    if (cn < nwc) {
+      const float4* src = reinterpret_cast<const float4*>(body + cn * kRegChunk);
+#pragma unroll
+      for (int j = 0; j < kLaneF4; ++j) nx[j] = __ldcs(src + j * 32 + lane);
+    }
+    if (lane == 0) {
+      const uint64_t pc = c + CL_HIST_REG_PF * wstride;
+      if (pc < nwc) bulk_prefetch_l2(body + pc * kRegChunk, kRegChunk * 4);
+    }
+    lane_count_u8(val, p, reinterpret_cast<unsigned char*>(counters), warp, lane);
+    if (++since_flush == kFlushChunks) {
+      flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+      since_flush = 0;
+    }
+  }
+  flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+  __syncthreads();
+  for (int b = threadIdx.x; b < k; b += blockDim.x)
+    if (cta_hist[b]) atomicAdd(d_counts + b, static_cast<unsigned long long>(cta_hist[b]));
+  if constexpr (FUSE) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    auto* ticket = reinterpret_cast<unsigned long long*>(const_cast<double*>(d_range) + 3);
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1ull) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      decide_block<true>(da, d_out);
+      if (threadIdx.x == 0) *ticket = 0ull;
+    }
+  }
+}
+
+
+// K > 256 (or f64 input): shared-memory atomics on a CTA histogram.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kThreads)
+    hist_atomic_kernel(const T* __restrict__ v, uint64_t n, uint64_t g0, uint64_t stride,
+                       int range_mode, double fixed_lo, double fixed_hi, int k,
+                       const double* __restrict__ d_range, unsigned long long* d_counts,
+                       int use_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw);
+  __shared__ BinParams sp;
+  if (threadIdx.x == 0) sp = make_bin_params(d_range, range_mode, fixed_lo, fixed_hi, k);
+  if (use_smem)
+    for (int i = threadIdx.x; i < k; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const BinParams p = sp;
+  const uint64_t nthr = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += nthr) {
+    if (!sampled<MODE>(g0 + i, stride)) continue;
+    int b;
+    if constexpr (sizeof(T) == 4)
+      b = bin_f32(v[i], p, range_mode == CL_RANGE_FIXED);
+    else
+      b = bin_index_exact(v[i], p.lo, p.width, k);
+    if (use_smem)
+      atomicAdd(hist + b, 1u);
+    else
+      atomicAdd(d_counts + b, 1ull);
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += blockDim.x)
+      if (hist[i]) atomicAdd(d_counts + i, static_cast<unsigned long long>(hist[i]));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1676,10 +1702,33 @@ cudaError_t launch_minmax_f64(const double* v, uint64_t n, uint64_t g0, uint64_t
   return cudaGetLastError();
 }
 
+DecideArgs make_decide_args(const uint64_t* d_counts, const double* d_range,
+                            const cl_hist_spec& spec, uint64_t n_samples,
+                            const cl_rule_spec& rule, uint64_t seq_len,
+                            const cl_features* features) {
+  DecideArgs a{};
+  a.counts = reinterpret_cast<const unsigned long long*>(d_counts);
+  a.range = d_range;
+  a.k = spec.bin_count;
+  a.epsilon = spec.epsilon;
+  a.range_mode = spec.range_mode;
+  a.fixed_lo = spec.fixed_lo;
+  a.fixed_hi = spec.fixed_hi;
+  a.n_samples = n_samples;
+  a.rule = rule;
+  a.seq_len = seq_len;
+  a.features_mode = features ? 1 : 0;
+  if (features) a.f = *features;
+  return a;
+}
+
+// The histogram; with fuse != null and the register-fed kernel applicable, that
+// kernel's last CTA also writes the decision (*fused = true; no launch_decide needed).
 cudaError_t launch_histogram_f32(const float* v, uint64_t n, uint64_t g0,
                                  const cl_hist_spec& spec, const double* d_range,
                                  uint64_t* d_counts, int num_sms, cudaStream_t s,
-                                 int* launches) {
+                                 int* launches, const HistFuse* fuse, bool* fused) {
+  if (fused) *fused = false;
   if (n == 0) return cudaSuccess;
   const uint64_t stride = spec.sample_stride;
   const int k = spec.bin_count;
@@ -1698,13 +1747,23 @@ cudaError_t launch_histogram_f32(const float* v, uint64_t n, uint64_t g0,
                                                  counts);
     };
     if (CL_HIST_REG && !fixed && mode == 0 && CL_HIST_U8) {
-      cudaFuncSetAttribute(hist_f32_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(kRegSmem));
+      const bool fz = fuse != nullptr && g0 == 0;
       const uint64_t wchunks = n / kRegChunk + 1;
       const uint64_t gmax = (wchunks + kRegWarps - 1) / kRegWarps;
       const int rgrid = static_cast<int>(gmax < static_cast<uint64_t>(num_sms) ? gmax : num_sms);
-      hist_f32_reg_kernel<<<rgrid, kRegWarps * 32, kRegSmem, s>>>(
-          v, n, spec.range_mode, spec.fixed_lo, spec.fixed_hi, k, d_range, counts);
+      DecideArgs da{};
+      cl_decision* d_out = nullptr;
+      if (fz) {
+        da = make_decide_args(d_counts, d_range, spec, fuse->n_samples, *fuse->rule,
+                              fuse->seq_len, nullptr);
+        d_out = fuse->d_out;
+      }
+      auto kern = fz ? hist_f32_reg_kernel<true> : hist_f32_reg_kernel<false>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(kRegSmem));
+      kern<<<rgrid, kRegWarps * 32, kRegSmem, s>>>(v, n, spec.range_mode, spec.fixed_lo,
+                                                   spec.fixed_hi, k, d_range, counts, da, d_out);
+      if (fused) *fused = fz;
     } else if (fixed) {
       if (mode == 0) launch(hist_f32_lane_kernel<0, true>);
       else if (mode == 1) launch(hist_f32_lane_kernel<1, true>);
@@ -1783,19 +1842,8 @@ cudaError_t launch_decide(const uint64_t* d_counts, const double* d_range,
                           const cl_hist_spec& spec, uint64_t n_samples, const cl_rule_spec& rule,
                           uint64_t seq_len, const cl_features* features, cl_decision* d_out,
                           cudaStream_t s) {
-  DecideArgs a{};
-  a.counts = reinterpret_cast<const unsigned long long*>(d_counts);
-  a.range = d_range;
-  a.k = spec.bin_count;
-  a.epsilon = spec.epsilon;
-  a.range_mode = spec.range_mode;
-  a.fixed_lo = spec.fixed_lo;
-  a.fixed_hi = spec.fixed_hi;
-  a.n_samples = n_samples;
-  a.rule = rule;
-  a.seq_len = seq_len;
-  a.features_mode = features ? 1 : 0;
-  if (features) a.f = *features;
+  const DecideArgs a =
+      make_decide_args(d_counts, d_range, spec, n_samples, rule, seq_len, features);
   decide_kernel<<<1, kThreads, 0, s>>>(a, d_out);
   return cudaGetLastError();
 }

@@ -258,6 +258,16 @@ class Prefill:
                       C.byref(self.rule), int(seq_len), self.decision_buf.data_ptr(),
                       _stream_ptr(self.device))
 
+    def stage_histogram_decide(self, u_flat: torch.Tensor, seq_len: int, zero: bool = True):
+        """Single-GPU stages 2+3 in one launch (the histogram's last CTA decides);
+        needs this call's stage_minmax (range_init) before it."""
+        s = _stream_ptr(self.device)
+        if zero:
+            self.ctx.call("cl_counts_zero", self.counts.data_ptr(), int(self.spec.bin_count), s)
+        self.ctx.call("cl_histogram_decide_f32", u_flat.data_ptr(), u_flat.numel(),
+                      C.byref(self.cspec), self.range.data_ptr(), self.counts.data_ptr(),
+                      C.byref(self.rule), int(seq_len), self.decision_buf.data_ptr(), s)
+
     def stage_decide(self, n_samples_total: int, seq_len: int):
         self.ctx.call("cl_decide", self.counts.data_ptr(), self.range.data_ptr(),
                       C.byref(self.cspec), int(n_samples_total), C.byref(self.rule),
@@ -283,8 +293,7 @@ class Prefill:
         else:
             uf = u.reshape(-1)
             self.stage_minmax(uf)
-            self.stage_histogram(uf)
-            self.stage_decide(self.n_samples(uf.numel()), u.shape[-1])
+            self.stage_histogram_decide(uf, u.shape[-1])
         res = self.stage_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, out,
                               return_last_state, h0)
         if return_last_state:

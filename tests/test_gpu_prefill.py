@@ -140,3 +140,42 @@ def test_no_host_sync_in_prefill(cuda):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("case", ["default", "repeat", "stride8", "fixed", "k512", "small",
+                                  "nonfinite", "guarded", "ragged"])
+def test_histogram_decide_fused_equals_separate(cuda, case):
+    """cl_histogram_decide_f32 (the histogram's last CTA decides, where the register-fed
+    kernel applies) writes the same counts and the same cl_decision bytes as
+    cl_histogram_f32 + cl_decide, on the fused path and on every fallback."""
+    n = {"small": 3000, "ragged": 1_000_003}.get(case, 1 << 20)
+    g = torch.Generator().manual_seed(11)
+    u = torch.randn(n, generator=g).to(cuda)
+    if case == "nonfinite":
+        u[12345] = float("nan")
+    spec = cl.HistogramSpec()
+    policy = None
+    bounds = cl.ChunkBounds(32, 512)
+    if case == "stride8":
+        spec = cl.HistogramSpec(sample_stride=8)
+    elif case == "fixed":
+        spec = cl.HistogramSpec(range_mode=cl.RangeMode.Fixed, fixed_lo=-2.0, fixed_hi=2.0)
+    elif case == "k512":
+        spec = cl.HistogramSpec(bin_count=512)
+    elif case == "guarded":
+        inner = cl.SchedulerPolicy(cl.FullHistogramPolicy(), [128, 256, 512, 1024, 2048])
+        policy = cl.SchedulerPolicy(cl.GuardedPolicy(inner, 512, 2), [128, 256, 512, 1024, 2048])
+        bounds = cl.ChunkBounds(128, 2048)
+    a = Prefill(spec, policy, bounds, cl.CalibrationRef.log_k(spec.bin_count), device=cuda)
+    b = Prefill(spec, policy, bounds, cl.CalibrationRef.log_k(spec.bin_count), device=cuda)
+    reps = 3 if case == "repeat" else 1
+    for _ in range(reps):  # the arrival ticket must be back at 0 after every call
+        a.stage_minmax(u)
+        a.stage_histogram_decide(u, 4096)
+        b.stage_minmax(u)
+        b.stage_histogram(u)
+        b.stage_decide(b.n_samples(n), 4096)
+        torch.cuda.synchronize()
+        assert torch.equal(a.counts, b.counts)
+        assert torch.equal(a.decision_buf, b.decision_buf)
+        assert torch.equal(a.range, b.range)
