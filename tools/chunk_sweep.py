@@ -28,11 +28,22 @@ from paper_2604_10597_b200.mamba1 import Prefill, selective_scan_fn  # noqa: E40
 BUCKETS = [64, 128, 256, 512, 1024, 2048]
 
 
+_L2BUF = []
+
+
+def flush_l2():
+    """Write 256 MB (twice the 126 MB L2) so no rep reads the previous rep's lines."""
+    if not _L2BUF:
+        _L2BUF.append(torch.empty(256 << 20, dtype=torch.uint8, device="cuda"))
+    _L2BUF[0].zero_()
+
+
 def timed(fn, reps):
     fn()
     torch.cuda.synchronize()
     out = []
     for _ in range(reps):
+        flush_l2()  # outside the events
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
