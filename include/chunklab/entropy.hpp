@@ -22,8 +22,7 @@ struct ActivationTensor {
   std::size_t size() const { return values.size(); }
 };
 
-// Shape checks here; the all-values finite check (entropy.hpp:42) runs on the GPU
-// inside compute_histogram's min/max pass.
+// Shape checks of validate_tensor (entropy.hpp:34-41), host-side.
 inline void validate_tensor_shape(const ActivationTensor& t) {
   if (t.shape.empty()) throw invalid_input("empty shape");
   std::size_t n = 1;
@@ -32,6 +31,22 @@ inline void validate_tensor_shape(const ActivationTensor& t) {
     n *= e;
   }
   if (n != t.values.size()) throw invalid_input("shape/value count mismatch");
+}
+
+namespace detail {
+// validate_tensor's value check (entropy.hpp:42) over every value, on the device
+inline void require_all_finite(std::span<const double> values) {
+  int ok = 1;
+  b200::check(cl_all_finite_host(b200::Runtime::get().ctx(), values.data(), values.size(), &ok));
+  if (!ok) throw invalid_input("non-finite input");
+}
+}  // namespace detail
+
+// validate_tensor (entropy.hpp:34-43): shape checks in the reference's order, then the
+// finite check over every value (a min/max pass on the GPU, cl_all_finite_host).
+inline void validate_tensor(const ActivationTensor& t) {
+  validate_tensor_shape(t);
+  detail::require_all_finite(t.values);
 }
 
 enum class RangeMode { Dynamic, Fixed };
@@ -93,20 +108,9 @@ inline Histogram compute_histogram(std::span<const double> values, const Histogr
   return h;
 }
 
-namespace detail {
-// validate_tensor's value check (entropy.hpp:42) over every value, on the device
-inline void require_all_finite(const ActivationTensor& t) {
-  int ok = 1;
-  b200::check(cl_all_finite_host(b200::Runtime::get().ctx(), t.values.data(), t.values.size(),
-                                 &ok));
-  if (!ok) throw invalid_input("non-finite input");
-}
-}  // namespace detail
-
 inline Histogram compute_histogram(const ActivationTensor& tensor, const HistogramSpec& spec) {
   if (tensor.values.empty()) throw invalid_input("no samples");
-  validate_tensor_shape(tensor);
-  detail::require_all_finite(tensor);
+  validate_tensor(tensor);
   return compute_histogram(std::span<const double>(tensor.values), spec);
 }
 
@@ -130,8 +134,7 @@ inline EntropyEstimate estimate_tensor_entropy(const ActivationTensor& tensor,
 // entropy.hpp:180-210: mean over positions of the per-position histogram entropy, one
 // device call (cl_token_entropy_host: a block per 8 positions, both passes on the GPU).
 inline EntropyEstimate token_entropy(const ActivationTensor& tensor, const HistogramSpec& spec) {
-  validate_tensor_shape(tensor);
-  detail::require_all_finite(tensor);
+  validate_tensor(tensor);
   validate_spec(spec);
   if (tensor.shape.size() < 2)
     throw invalid_input("token entropy needs a (channels, length) tensor");

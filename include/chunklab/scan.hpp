@@ -37,7 +37,7 @@ struct ScanOutput {
   std::vector<double> y;
 };
 
-// scan.hpp:54-69, shape part (finiteness is checked on the device by the scan call)
+// scan.hpp:54-68, the shape part (the scan call checks finiteness on the device)
 inline void validate_scan_shapes(const ScanParams& p) {
   if (p.channels == 0 || p.state_dim == 0 || p.seq_len == 0) throw invalid_input("shape mismatch");
   const std::size_t cs = p.channels * p.state_dim;
@@ -46,6 +46,24 @@ inline void validate_scan_shapes(const ScanParams& p) {
                   (p.c.size() == p.state_dim || p.c.size() == p.seq_len * p.state_dim) &&
                   p.d.size() == p.channels && p.x.size() == p.channels * p.seq_len;
   if (!ok) throw invalid_input("shape mismatch");
+}
+
+namespace detail {
+inline bool all_finite_on_device(const std::vector<double>& v) {
+  int ok = 1;
+  b200::check(cl_all_finite_host(b200::Runtime::get().ctx(), v.data(), v.size(), &ok));
+  return ok != 0;
+}
+}  // namespace detail
+
+// validate_scan_params (scan.hpp:54-69): the shape checks, then "non-finite input" if
+// any of a, b, c, d, x holds a NaN or infinity (checked by a min/max pass on the GPU).
+inline void validate_scan_params(const ScanParams& p) {
+  validate_scan_shapes(p);
+  if (!detail::all_finite_on_device(p.a) || !detail::all_finite_on_device(p.b) ||
+      !detail::all_finite_on_device(p.c) || !detail::all_finite_on_device(p.d) ||
+      !detail::all_finite_on_device(p.x))
+    throw invalid_input("non-finite input");
 }
 
 namespace detail {

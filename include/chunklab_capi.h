@@ -10,10 +10,17 @@
  *
  * Conventions
  *   - Every function returns int status: CL_OK (0) or a CL_E_* code; the
- *     message is available from cl_last_error(ctx) and, for CL_E_INVALID,
- *     is byte-identical to the reference's chunklab::invalid_input what().
+ *     message is available from cl_last_error() on the calling thread
+ *     (errno-style) and, for CL_E_INVALID, is byte-identical to the reference's
+ *     chunklab::invalid_input what().
  *   - "d_" pointers are device pointers, "h_" pointers are host pointers.
  *     Buffers are caller-owned; scratch belongs to the context.
+ *   - Threads and streams (the reference's functions are pure and reentrant,
+ *     SPEC.md:86): a context may be shared by any number of host threads.  Its
+ *     device scratch (scan work tickets and carries, the B/C transpose, the
+ *     fused histogram's arrival ticket, token-entropy buffers) is kept per
+ *     stream, so launch sequences on different streams never share scratch;
+ *     the host path (*_host) is serialised on the context.
  *   - Device-path functions (cl_minmax_f32 ... cl_selective_scan_f32) are
  *     asynchronous on the given cudaStream_t (passed as void*) and never
  *     synchronise with the host.  Errors only the device can see
@@ -61,6 +68,7 @@ typedef struct cl_ctx cl_ctx;
 /* ------------------------------------------------------------------------ */
 int cl_ctx_create(int device, cl_ctx** out);
 int cl_ctx_destroy(cl_ctx* ctx);
+/* Message of the calling thread's last failed call (ctx may be NULL). */
 const char* cl_last_error(const cl_ctx* ctx);
 int cl_abi_version(void);
 /* Number of kernel launches this context has issued (bench evidence). */
@@ -179,9 +187,8 @@ int cl_decide(cl_ctx* ctx, const uint64_t* d_counts, const double* d_range,
  * n_samples_total = ceil(n / stride), same results bit for bit.  Where the
  * register-fed histogram applies (K <= 256, Dynamic range, stride 1, n >= 4096) its
  * last CTA writes the decision; otherwise the two kernels run back to back.
- * d_range must come from cl_range_init + cl_minmax_f32 of this call: its spare word
- * d_range[3] is the CTAs' arrival ticket (left at 0).  d_counts zeroed as for
- * cl_histogram_f32.  Replaces the compute_histogram -> estimate_entropy ->
+ * d_range from cl_range_init + cl_minmax_f32 of this call; d_counts zeroed as for
+ * cl_histogram_f32.  The CTAs' arrival ticket lives in the stream's workspace.  Replaces the compute_histogram -> estimate_entropy ->
  * select_chunk sequence of entropy.hpp:101-174 / chunk.hpp:68-89. */
 int cl_histogram_decide_f32(cl_ctx* ctx, const float* d_values, uint64_t n,
                             const cl_hist_spec* spec, const double* d_range, uint64_t* d_counts,

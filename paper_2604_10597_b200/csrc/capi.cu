@@ -12,18 +12,56 @@
 
 namespace cl {
 
-int fail(cl_ctx* ctx, int code, const std::string& msg) {
-  if (ctx) ctx->last_error = msg;
+namespace {
+// cl_last_error is per calling thread (errno-style): contexts are shared between host
+// threads (the drop-in's process-wide context), so a per-context string would race.
+thread_local std::string g_error;
+}  // namespace
+
+int fail(cl_ctx*, int code, const std::string& msg) {
+  g_error = msg;
   return code;
 }
+
+const std::string& thread_error() { return g_error; }
+
+cl_workspace* workspace(cl_ctx* ctx, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lk(ctx->ws_mu);
+  auto it = ctx->ws.find(stream);
+  if (it != ctx->ws.end()) return it->second;
+  auto* w = new cl_workspace();
+  cudaError_t e = cudaMalloc(&w->d_hist_ticket, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(w->d_hist_ticket, 0, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    cudaFree(w->d_hist_ticket);
+    delete w;
+    cuda_fail(ctx, e, "cudaMalloc(stream workspace)");
+    return nullptr;
+  }
+  ctx->ws.emplace(stream, w);
+  return w;
+}
+
+namespace {
+void free_workspace(cl_workspace* w) {
+  cudaFree(w->d_work);
+  cudaFree(w->d_carry);
+  cudaFree(w->d_tcarry);
+  cudaFree(w->d_bct);
+  cudaFree(w->d_agg);
+  cudaFree(w->d_hist_ticket);
+  cudaFree(w->d_token_raw);
+  cudaFree(w->d_token_range);
+  cudaFree(w->d_token_counts);
+  delete w;
+}
+}  // namespace
 
 int cuda_fail(cl_ctx* ctx, cudaError_t e, const char* where) {
   return fail(ctx, CL_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
 namespace {
-
-thread_local std::string g_no_ctx_error;
 
 struct DeviceGuard {
   int prev = -1;
@@ -124,12 +162,25 @@ const char* device_error_message(int code) {
   }
 }
 
+// Host-path device staging: the context's upload buffer, grown on demand and reused, so a
+// host call does no cudaMalloc / cudaFree once warm.  Callers hold ctx->host_mu.
 template <typename T>
 struct DevBuf {
+  cl_ctx* ctx;
   T* p = nullptr;
-  cudaError_t alloc(size_t n) { return cudaMalloc(&p, n * sizeof(T) + 16); }
-  ~DevBuf() {
-    if (p) cudaFree(p);
+  explicit DevBuf(cl_ctx* c) : ctx(c) {}
+  cudaError_t alloc(size_t n) {
+    const size_t need = n * sizeof(T) + 16;
+    if (ctx->stage_bytes < need) {
+      cudaFree(ctx->d_stage);
+      ctx->d_stage = nullptr;
+      ctx->stage_bytes = 0;
+      cudaError_t e = cudaMalloc(&ctx->d_stage, need);
+      if (e != cudaSuccess) return e;
+      ctx->stage_bytes = need;
+    }
+    p = static_cast<T*>(ctx->d_stage);
+    return cudaSuccess;
   }
 };
 
@@ -158,11 +209,11 @@ int cl_ctx_create(int device, cl_ctx** out) {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
   if (e != cudaSuccess || n == 0) {
-    g_no_ctx_error = "no CUDA device available: the chunklab B200 path has no CPU fallback";
+    g_error = "no CUDA device available: the chunklab B200 path has no CPU fallback";
     return CL_E_CUDA;
   }
   if (device < 0 || device >= n) {
-    g_no_ctx_error = "invalid device ordinal";
+    g_error = "invalid device ordinal";
     return CL_E_INVALID;
   }
   auto* ctx = new cl_ctx();
@@ -171,12 +222,12 @@ int cl_ctx_create(int device, cl_ctx** out) {
   cudaDeviceProp prop;
   e = cudaGetDeviceProperties(&prop, device);
   if (e != cudaSuccess) {
-    g_no_ctx_error = cudaGetErrorString(e);
+    g_error = cudaGetErrorString(e);
     delete ctx;
     return CL_E_CUDA;
   }
   if (prop.major < 10) {
-    g_no_ctx_error = "libchunklab_b200 is built for sm_100a (Blackwell); found sm_" +
+    g_error = "libchunklab_b200 is built for sm_100a (Blackwell); found sm_" +
                      std::to_string(prop.major) + std::to_string(prop.minor);
     delete ctx;
     return CL_E_CUDA;
@@ -186,7 +237,7 @@ int cl_ctx_create(int device, cl_ctx** out) {
       (e = cudaMalloc(&ctx->d_scratch_counts, kMaxBinsScratch * sizeof(uint64_t))) != cudaSuccess ||
       (e = cudaMalloc(&ctx->d_scratch_decision, sizeof(cl_decision))) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking)) != cudaSuccess) {
-    g_no_ctx_error = cudaGetErrorString(e);
+    g_error = cudaGetErrorString(e);
     cl_ctx_destroy(ctx);
     return CL_E_CUDA;
   }
@@ -197,28 +248,23 @@ int cl_ctx_create(int device, cl_ctx** out) {
 int cl_ctx_destroy(cl_ctx* ctx) {
   if (!ctx) return CL_OK;
   DeviceGuard g(ctx->device);
+  // cudaFree synchronises the device, so no workspace is freed under a running kernel
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
   cudaFree(ctx->d_scratch_range);
   cudaFree(ctx->d_scratch_counts);
   cudaFree(ctx->d_scratch_decision);
-  cudaFree(ctx->d_work);
-  cudaFree(ctx->d_carry);
-  cudaFree(ctx->d_tcarry);
-  cudaFree(ctx->d_bct);
-  cudaFree(ctx->d_token_raw);
-  cudaFree(ctx->d_token_range);
-  cudaFree(ctx->d_token_counts);
   cudaFree(ctx->d_token_out);
+  cudaFree(ctx->d_stage);
+  for (auto& kv : ctx->ws) free_workspace(kv.second);
+  ctx->ws.clear();
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return CL_OK;
 }
 
-const char* cl_last_error(const cl_ctx* ctx) {
-  return ctx ? ctx->last_error.c_str() : g_no_ctx_error.c_str();
-}
+const char* cl_last_error(const cl_ctx*) { return g_error.c_str(); }
 
-uint64_t cl_launch_count(const cl_ctx* ctx) { return ctx ? ctx->launches : 0; }
+uint64_t cl_launch_count(const cl_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
 int cl_validate_hist_spec(cl_ctx* ctx, const cl_hist_spec* spec) { return validate_spec(ctx, spec); }
 int cl_validate_rule(cl_ctx* ctx, const cl_rule_spec* rule) { return validate_rule(ctx, rule); }
@@ -323,7 +369,10 @@ int cl_histogram_decide_f32(cl_ctx* ctx, const float* d_values, uint64_t n,
   bool fused = false;
   {
     DeviceGuard g(ctx->device);
-    const HistFuse fz{samples_of(n, spec->sample_stride), rule, seq_len, d_decision};
+    cl_workspace* w = workspace(ctx, static_cast<cudaStream_t>(stream));
+    if (!w) return CL_E_CUDA;
+    const HistFuse fz{samples_of(n, spec->sample_stride), rule, seq_len, d_decision,
+                      w->d_hist_ticket};
     int l = 0;
     cudaError_t e = launch_histogram_f32(d_values, n, 0, *spec, d_range, d_counts, ctx->num_sms,
                                          static_cast<cudaStream_t>(stream), &l,
@@ -376,36 +425,37 @@ int grow_bytes(cl_ctx* ctx, P** ptr, size_t* have, size_t need) {
   return CL_OK;
 }
 
-int grow_token(cl_ctx* ctx, uint64_t length, int k) {
-  int rc = grow_bytes(ctx, &ctx->d_token_raw, &ctx->token_raw_bytes, length * sizeof(double));
+int grow_token(cl_ctx* ctx, cl_workspace* w, uint64_t length, int k) {
+  int rc = grow_bytes(ctx, &w->d_token_raw, &w->token_raw_bytes, length * sizeof(double));
   if (!rc)
-    rc = grow_bytes(ctx, &ctx->d_token_range, &ctx->token_range_bytes,
+    rc = grow_bytes(ctx, &w->d_token_range, &w->token_range_bytes,
                     (2 * length + 1) * sizeof(double));
   if (!rc)
-    rc = grow_bytes(ctx, &ctx->d_token_counts, &ctx->token_counts_bytes,
+    rc = grow_bytes(ctx, &w->d_token_counts, &w->token_counts_bytes,
                     length * static_cast<size_t>(k) * sizeof(unsigned int));
   return rc;
 }
 
-// the four stages over one device tensor with the context's scratch
+// the four stages over one device tensor with the stream workspace's scratch
 template <typename T>
-cudaError_t token_pipeline(cl_ctx* ctx, const T* d_values, uint64_t channels, uint64_t length,
-                           const cl_hist_spec& spec, double* d_out, cudaStream_t s) {
-  double* trange = ctx->d_token_range;
-  double* flag = ctx->d_token_range + 2 * length;
+cudaError_t token_pipeline(cl_ctx* ctx, cl_workspace* w, const T* d_values, uint64_t channels,
+                           uint64_t length, const cl_hist_spec& spec, double* d_out,
+                           cudaStream_t s) {
+  double* trange = w->d_token_range;
+  double* flag = w->d_token_range + 2 * length;
   cudaError_t e = launch_token_range_init(trange, flag, length, s);
   if (e == cudaSuccess)
     e = launch_token_minmax<T>(d_values, channels, length, 0, spec.sample_stride, trange, flag,
                                ctx->num_sms, s);
   if (e == cudaSuccess)
-    e = cudaMemsetAsync(ctx->d_token_counts, 0,
+    e = cudaMemsetAsync(w->d_token_counts, 0,
                         length * static_cast<size_t>(spec.bin_count) * sizeof(unsigned int), s);
   if (e == cudaSuccess)
-    e = launch_token_hist<T>(d_values, channels, length, 0, spec, trange, ctx->d_token_counts,
+    e = launch_token_hist<T>(d_values, channels, length, 0, spec, trange, w->d_token_counts,
                              ctx->num_sms, s);
   if (e == cudaSuccess)
-    e = launch_token_entropy(ctx->d_token_counts, length, samples_of(channels, spec.sample_stride),
-                             spec, flag, ctx->d_token_raw, d_out, s);
+    e = launch_token_entropy(w->d_token_counts, length, samples_of(channels, spec.sample_stride),
+                             spec, flag, w->d_token_raw, d_out, s);
   ctx->launches += 5;
   return e;
 }
@@ -468,12 +518,14 @@ int cl_token_entropy_counts(cl_ctx* ctx, const uint32_t* d_counts, const double*
   if (!d_counts || !d_trange || !d_out) return fail(ctx, CL_E_INVALID, "null argument");
   if (length == 0 || samples_per_position == 0) return fail(ctx, CL_E_INVALID, "no samples");
   DeviceGuard g(ctx->device);
-  if ((rc = grow_bytes(ctx, &ctx->d_token_raw, &ctx->token_raw_bytes, length * sizeof(double))))
+  cl_workspace* w = workspace(ctx, static_cast<cudaStream_t>(stream));
+  if (!w) return CL_E_CUDA;
+  if ((rc = grow_bytes(ctx, &w->d_token_raw, &w->token_raw_bytes, length * sizeof(double))))
     return rc;
   ctx->launches += 2;
   return check_launch(ctx,
                       launch_token_entropy(d_counts, length, samples_per_position, *spec,
-                                           d_trange + 2 * length, ctx->d_token_raw, d_out,
+                                           d_trange + 2 * length, w->d_token_raw, d_out,
                                            static_cast<cudaStream_t>(stream)),
                       "token_entropy");
 }
@@ -485,9 +537,11 @@ int cl_token_entropy_f32(cl_ctx* ctx, const float* d_values, uint64_t channels, 
   if (rc) return rc;
   if (!d_values || !d_out) return fail(ctx, CL_E_INVALID, "null argument");
   DeviceGuard g(ctx->device);
-  if ((rc = grow_token(ctx, length, spec->bin_count))) return rc;
+  cl_workspace* w = workspace(ctx, static_cast<cudaStream_t>(stream));
+  if (!w) return CL_E_CUDA;
+  if ((rc = grow_token(ctx, w, length, spec->bin_count))) return rc;
   return check_launch(ctx,
-                      token_pipeline<float>(ctx, d_values, channels, length, *spec, d_out,
+                      token_pipeline<float>(ctx, w, d_values, channels, length, *spec, d_out,
                                             static_cast<cudaStream_t>(stream)),
                       "token_entropy_f32");
 }
@@ -604,8 +658,9 @@ int cl_all_finite_host(cl_ctx* ctx, const double* h_values, uint64_t n, int* h_a
   *h_all_finite = 1;
   if (n == 0) return CL_OK;
   DeviceGuard g(ctx->device);
+  std::lock_guard<std::recursive_mutex> lk(ctx->host_mu);
   cudaStream_t s = ctx->own_stream;
-  DevBuf<double> dv;
+  DevBuf<double> dv(ctx);
   cudaError_t e = dv.alloc(n);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc");
   if ((e = cudaMemcpyAsync(dv.p, h_values, n * sizeof(double), cudaMemcpyHostToDevice, s)) !=
@@ -643,8 +698,9 @@ int cl_compute_histogram_host(cl_ctx* ctx, const double* h_values, uint64_t n,
     sp.sample_stride = 1;
   }
   DeviceGuard g(ctx->device);
+  std::lock_guard<std::recursive_mutex> lk(ctx->host_mu);
   cudaStream_t s = ctx->own_stream;
-  DevBuf<double> dv;
+  DevBuf<double> dv(ctx);
   cudaError_t e = dv.alloc(n);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc");
   if ((e = cudaMemcpyAsync(dv.p, h_values, n * sizeof(double), cudaMemcpyHostToDevice, s)) !=
@@ -689,18 +745,21 @@ int cl_token_entropy_host(cl_ctx* ctx, const double* h_values, uint64_t channels
   if (rc) return rc;
   if (!h_values) return fail(ctx, CL_E_INVALID, "null argument");
   DeviceGuard g(ctx->device);
+  std::lock_guard<std::recursive_mutex> lk(ctx->host_mu);
   cudaStream_t s = ctx->own_stream;
+  cl_workspace* w = workspace(ctx, s);
+  if (!w) return CL_E_CUDA;
   const uint64_t n = channels * length;
-  DevBuf<double> dv;
+  DevBuf<double> dv(ctx);
   cudaError_t e = dv.alloc(n);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc");
   if ((rc = grow_bytes(ctx, &ctx->d_token_out, &ctx->token_out_bytes, 4 * sizeof(double))))
     return rc;
-  if ((rc = grow_token(ctx, length, spec->bin_count))) return rc;
+  if ((rc = grow_token(ctx, w, length, spec->bin_count))) return rc;
   if ((e = cudaMemcpyAsync(dv.p, h_values, n * sizeof(double), cudaMemcpyHostToDevice, s)) !=
       cudaSuccess)
     return cuda_fail(ctx, e, "cudaMemcpyAsync");
-  if ((e = token_pipeline<double>(ctx, dv.p, channels, length, *spec, ctx->d_token_out, s)) !=
+  if ((e = token_pipeline<double>(ctx, w, dv.p, channels, length, *spec, ctx->d_token_out, s)) !=
       cudaSuccess)
     return cuda_fail(ctx, e, "token_entropy_f64");
   double out[4];
@@ -721,8 +780,9 @@ int cl_estimate_entropy_host(cl_ctx* ctx, const double* h_masses, int bin_count,
   if (bin_count < 2) return fail(ctx, CL_E_INVALID, "degenerate spec");
   if (!(epsilon > 0.0)) return fail(ctx, CL_E_INVALID, "epsilon must be positive");
   DeviceGuard g(ctx->device);
+  std::lock_guard<std::recursive_mutex> lk(ctx->host_mu);
   cudaStream_t s = ctx->own_stream;
-  DevBuf<double> dm;
+  DevBuf<double> dm(ctx);
   cudaError_t e = dm.alloc(size_t(bin_count) + 2);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc");
   if ((e = cudaMemcpyAsync(dm.p, h_masses, bin_count * sizeof(double), cudaMemcpyHostToDevice,
@@ -760,6 +820,7 @@ int cl_schedule_host(cl_ctx* ctx, const cl_rule_spec* rule, const cl_features* f
   if (kind == CL_POL_TOKEN_HIST && !features->has_token_entropy)
     return fail(ctx, CL_E_INVALID, "missing feature: token_entropy");
   DeviceGuard g(ctx->device);
+  std::lock_guard<std::recursive_mutex> lk(ctx->host_mu);
   cudaStream_t s = ctx->own_stream;
   cl_hist_spec spec{256, 1e-8, 0, 0.0, 0.0, 1};
   ++ctx->launches;
@@ -768,7 +829,7 @@ int cl_schedule_host(cl_ctx* ctx, const cl_rule_spec* rule, const cl_features* f
                                 ctx->d_scratch_decision, s);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "decide");
   rc = cl_decision_check(ctx, ctx->d_scratch_decision, h_out, s);
-  if (rc == CL_E_DEVICE) return fail(ctx, CL_E_INVALID, ctx->last_error);
+  if (rc == CL_E_DEVICE) return fail(ctx, CL_E_INVALID, std::string(thread_error()));
   return rc;
 }
 
@@ -784,9 +845,10 @@ int cl_scan_f64_host(cl_ctx* ctx, const cl_scan_params_f64* h, const double* h_h
       h->d_len != h->channels || h->x_len != h->channels * h->seq_len)
     return fail(ctx, CL_E_INVALID, "shape mismatch");
   DeviceGuard g(ctx->device);
+  std::lock_guard<std::recursive_mutex> lk(ctx->host_mu);
   cudaStream_t s = ctx->own_stream;
   const size_t total = h->a_len + h->b_len + h->c_len + h->d_len + h->x_len + cs;
-  DevBuf<double> buf;
+  DevBuf<double> buf(ctx);
   cudaError_t e = buf.alloc(total + h->x_len + cs);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc");
   double* p = buf.p;

@@ -3,23 +3,21 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "chunklab_capi.h"
 
-struct cl_ctx {
-  int device = 0;
-  int num_sms = 148;
-  std::string last_error;
-  uint64_t launches = 0;
-  // device scratch owned by the context
-  double* d_scratch_range = nullptr;   // 4 doubles
-  uint64_t* d_scratch_counts = nullptr;  // up to kMaxBinsScratch
-  cl_decision* d_scratch_decision = nullptr;
+// Device scratch that a launch sequence on ONE stream owns.  Kernels on the same stream
+// are ordered, so they may reuse it; two streams never share one (a scan's work ticket,
+// tagged carry and B/C transpose, or the fused histogram's arrival ticket, would race).
+struct cl_workspace {
   unsigned int* d_work = nullptr;  // scan work counters / flags (grown on demand)
   size_t work_bytes = 0;
-  float* d_carry = nullptr;  // scan segment carry (grown on demand)
+  float* d_carry = nullptr;  // scan segment carry of the row kernel (grown on demand)
   size_t carry_bytes = 0;
   // tagged segment carry of the warp-specialised scan: 64-bit words {tag, h}; tags are
   // epoch + segment with the epoch advanced past every launch's tags, so stale words from
@@ -29,16 +27,39 @@ struct cl_ctx {
   unsigned int carry_epoch = 0;
   float* d_bct = nullptr;  // B^T / C^T (b, L, N) for the TMA scan (grown on demand)
   size_t bct_bytes = 0;
-  // token_entropy scratch (grown on demand): per-position raw entropies [L], ranges
-  // [2L] + the finite flag, counts [L][K]; and the host path's 4-double result
+  // L-parallel scan: per-(tile, segment) aggregates {tag, h~_end[16], sum dt} words
+  unsigned long long* d_agg = nullptr;
+  size_t agg_bytes = 0;
+  unsigned int agg_epoch = 0;
+  // arrival ticket of the fused histogram -> decision launch: 0 between launches (the
+  // last CTA resets it), never visible to callers
+  unsigned long long* d_hist_ticket = nullptr;
+  // device-path token_entropy scratch
   double* d_token_raw = nullptr;
   size_t token_raw_bytes = 0;
   double* d_token_range = nullptr;
   size_t token_range_bytes = 0;
   unsigned int* d_token_counts = nullptr;
   size_t token_counts_bytes = 0;
+};
+
+struct cl_ctx {
+  int device = 0;
+  int num_sms = 148;
+  std::atomic<uint64_t> launches{0};
+  // one workspace per stream handle (created on first use, freed with the context)
+  std::mutex ws_mu;
+  std::map<cudaStream_t, cl_workspace*> ws;
+  // The host path (*_host) and its scratch: serialised per context, so the drop-in C++
+  // API (one process-wide context) stays reentrant and thread-safe (reference SPEC.md:86).
+  std::recursive_mutex host_mu;
+  double* d_scratch_range = nullptr;   // 4 doubles
+  uint64_t* d_scratch_counts = nullptr;  // up to kMaxBinsScratch
+  cl_decision* d_scratch_decision = nullptr;
   double* d_token_out = nullptr;
   size_t token_out_bytes = 0;
+  void* d_stage = nullptr;  // host-path upload buffer (grown on demand, reused across calls)
+  size_t stage_bytes = 0;
   cudaStream_t own_stream = nullptr;
 };
 
@@ -46,9 +67,25 @@ namespace cl {
 
 constexpr int kMaxBinsScratch = 1 << 16;
 
-// Set the error message and return the code.
+// Set the calling thread's error message (cl_last_error) and return the code.
 int fail(cl_ctx* ctx, int code, const std::string& msg);
 int cuda_fail(cl_ctx* ctx, cudaError_t e, const char* where);
+const std::string& thread_error();
+
+// The workspace of `stream` (created on first use); nullptr + error on allocation failure.
+cl_workspace* workspace(cl_ctx* ctx, cudaStream_t stream);
+
+template <typename T>
+int grow_scratch(cl_ctx* ctx, T** ptr, size_t* have, size_t need, const char* what) {
+  if (*have >= need) return 0;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *have = 0;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), need);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, what);
+  *have = need;
+  return 0;
+}
 
 // ---- kernel launchers (defined in the .cu files) ----
 // entropy.cu
@@ -58,12 +95,13 @@ cudaError_t launch_minmax_f32(const float* v, uint64_t n, uint64_t g0, uint64_t 
 cudaError_t launch_minmax_f64(const double* v, uint64_t n, uint64_t g0, uint64_t stride,
                               double* d_range, int num_sms, cudaStream_t s, int* launches);
 // Histogram + decision in one launch (single-GPU prefill): the decision's inputs
-// beyond the histogram's own.  The caller's range[3] must be 0 (range_init).
+// beyond the histogram's own.
 struct HistFuse {
   uint64_t n_samples;
   const cl_rule_spec* rule;
   uint64_t seq_len;
   cl_decision* d_out;
+  unsigned long long* ticket;  // the stream workspace's arrival ticket (0 on entry and exit)
 };
 cudaError_t launch_histogram_f32(const float* v, uint64_t n, uint64_t g0,
                                  const cl_hist_spec& spec, const double* d_range,

@@ -427,6 +427,9 @@ __device__ __forceinline__ void flush_warp(cnt_t* cnt, uint32_t* cta_hist, int l
 #ifndef CL_HIST_X2
 #define CL_HIST_X2 1
 #endif
+#ifndef CL_HIST_RANGE_CHECK
+#define CL_HIST_RANGE_CHECK 1
+#endif
 __device__ __forceinline__ uint64_t pack_f2(float a, float b) {
   return (static_cast<uint64_t>(__float_as_uint(b)) << 32) | __float_as_uint(a);
 }
@@ -464,6 +467,13 @@ __device__ __forceinline__ void lane_count_u8(const float (&val)[kLaneSamples], 
     any_slow |= !(fabsf(hi_f(d2)) <= p.thr);
     tb[e] = static_cast<uint32_t>(t2);
     tb[e + 1] = static_cast<uint32_t>(t2 >> 32);
+#if CL_HIST_RANGE_CHECK
+    // a sample outside the supplied range (a caller's d_range that does not cover the
+    // data) rounds to n < 0 or n >= k: take the exact, clamping path (entropy.hpp:91-92)
+    // instead of wrapping into bin n mod 256
+    any_slow |= tb[e] - 0x4B400000u >= static_cast<uint32_t>(p.k);
+    any_slow |= tb[e + 1] - 0x4B400000u >= static_cast<uint32_t>(p.k);
+#endif
   }
 #else
 #pragma unroll
@@ -472,6 +482,9 @@ __device__ __forceinline__ void lane_count_u8(const float (&val)[kLaneSamples], 
     const float t = x + 12582912.0f;
     any_slow |= !(fabsf(x - (t - 12582912.0f)) <= p.thr);
     tb[e] = __float_as_uint(t);
+#if CL_HIST_RANGE_CHECK
+    any_slow |= tb[e] - 0x4B400000u >= static_cast<uint32_t>(p.k);
+#endif
   }
 #endif
   if (__any_sync(0xffffffffu, any_slow)) {
@@ -965,14 +978,15 @@ constexpr int kRegWarps = 16;
 constexpr int kRegChunk = 32 * kLaneSamples;  // floats per warp-chunk
 constexpr size_t kRegSmem = size_t(kRegWarps) * kLaneBins * kBinStride + kLaneBins * 4 + 64;
 
-// FUSE: the CTA that finishes last (an arrival ticket in the range's spare word
-// range[3], zeroed by range_init and reset here) also runs the decision, so the
-// single-GPU prefill has no separate decide launch.
+// FUSE: the CTA that finishes last (an arrival ticket in the stream workspace, 0 on
+// entry and reset here by the last CTA) also runs the decision, so the single-GPU
+// prefill has no separate decide launch.
 template <bool FUSE>
 __global__ void __launch_bounds__(kRegWarps * 32, 1)
     hist_f32_reg_kernel(const float* __restrict__ v, uint64_t n, int range_mode, double fixed_lo,
                         double fixed_hi, int k, const double* __restrict__ d_range,
-                        unsigned long long* d_counts, DecideArgs da, cl_decision* d_out) {
+                        unsigned long long* d_counts, DecideArgs da, cl_decision* d_out,
+                        unsigned long long* ticket) {
   extern __shared__ __align__(128) unsigned char smem[];
   cnt_t* counters = reinterpret_cast<cnt_t*>(smem);
   uint32_t* cta_hist = reinterpret_cast<uint32_t*>(smem + size_t(kRegWarps) * kLaneBins * kBinStride);
@@ -1049,7 +1063,6 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1)
     __shared__ bool last;
     __threadfence();
     __syncthreads();
-    auto* ticket = reinterpret_cast<unsigned long long*>(const_cast<double*>(d_range) + 3);
     if (threadIdx.x == 0) last = atomicAdd(ticket, 1ull) == gridDim.x - 1;
     __syncthreads();
     if (last) {
@@ -1762,7 +1775,8 @@ cudaError_t launch_histogram_f32(const float* v, uint64_t n, uint64_t g0,
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(kRegSmem));
       kern<<<rgrid, kRegWarps * 32, kRegSmem, s>>>(v, n, spec.range_mode, spec.fixed_lo,
-                                                   spec.fixed_hi, k, d_range, counts, da, d_out);
+                                                   spec.fixed_hi, k, d_range, counts, da, d_out,
+                                                   fz ? fuse->ticket : nullptr);
       if (fused) *fused = fz;
     } else if (fixed) {
       if (mode == 0) launch(hist_f32_lane_kernel<0, true>);

@@ -1375,31 +1375,34 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     const size_t work_bytes = (size_t(n_tiles) + 32) * sizeof(unsigned int);
     const size_t carry_bytes = size_t(n_tiles) * rows_per_tile * kN * sizeof(float);
     const size_t bc_bytes = 2 * size_t(Bt) * L * kN * sizeof(float);
-    int rc = grow(ctx, &ctx->d_work, &ctx->work_bytes, work_bytes, "cudaMalloc(scan work)");
-    if (!rc) rc = grow(ctx, &ctx->d_carry, &ctx->carry_bytes, carry_bytes, "cudaMalloc(carry)");
-    if (!rc) rc = grow(ctx, &ctx->d_bct, &ctx->bct_bytes, bc_bytes, "cudaMalloc(B/C transpose)");
+    cl_workspace* w = workspace(ctx, s);  // scratch of this stream only
+    if (!w) return CL_E_CUDA;
+    int rc = grow(ctx, &w->d_work, &w->work_bytes, work_bytes, "cudaMalloc(scan work)");
+    if (!rc && !ws)
+      rc = grow(ctx, &w->d_carry, &w->carry_bytes, carry_bytes, "cudaMalloc(carry)");
+    if (!rc) rc = grow(ctx, &w->d_bct, &w->bct_bytes, bc_bytes, "cudaMalloc(B/C transpose)");
     if (rc) return rc;
     unsigned int epoch = 0;
     if (ws) {
       // tagged carry words: zeroed when (re)allocated or when the epoch would wrap; each
       // launch takes tags epoch + 1 .. epoch + (segments <= boxes), above every older tag
       const size_t tcarry_bytes = size_t(n_tiles) * kRowsP * kN * sizeof(unsigned long long);
-      const bool fresh = ctx->tcarry_bytes < tcarry_bytes;
-      rc = grow(ctx, &ctx->d_tcarry, &ctx->tcarry_bytes, tcarry_bytes, "cudaMalloc(tagged carry)");
+      const bool fresh = w->tcarry_bytes < tcarry_bytes;
+      rc = grow(ctx, &w->d_tcarry, &w->tcarry_bytes, tcarry_bytes, "cudaMalloc(tagged carry)");
       if (rc) return rc;
       const unsigned span = static_cast<unsigned>((L + cfg.box - 1) / cfg.box) + 2u;
-      if (fresh || ctx->carry_epoch == 0 || ctx->carry_epoch > 0xFFFFFFFFu - span) {
-        cudaError_t e = cudaMemsetAsync(ctx->d_tcarry, 0, ctx->tcarry_bytes, s);
+      if (fresh || w->carry_epoch == 0 || w->carry_epoch > 0xFFFFFFFFu - span) {
+        cudaError_t e = cudaMemsetAsync(w->d_tcarry, 0, w->tcarry_bytes, s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(tagged carry)");
-        ctx->carry_epoch = 1;
+        w->carry_epoch = 1;
       }
-      epoch = ctx->carry_epoch;
-      ctx->carry_epoch += span;
+      epoch = w->carry_epoch;
+      w->carry_epoch += span;
     }
     // B^T / C^T: interleaved per timestep ([B | C], 128 B rows, one TMA box) for the
     // warp-specialised kernel, two separate (b, L, 16) arrays for the row kernel
-    float* d_Bt = ctx->d_bct;
-    float* d_Ct = ws ? ctx->d_bct + kN : ctx->d_bct + size_t(Bt) * L * kN;
+    float* d_Bt = w->d_bct;
+    float* d_Ct = ws ? w->d_bct + kN : w->d_bct + size_t(Bt) * L * kN;
     const int box = cfg.box;
     const int sw = box == 32 ? 128 : (box == 16 ? 64 : 32);
     CUtensorMap m[6];  // u, delta, z, out, B^T (or [B|C]), C^T
@@ -1413,7 +1416,7 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       ok = make_map(&m[4], d_Bt, kN, L, Bt, kN, box, 0) &&
            make_map(&m[5], d_Ct, kN, L, Bt, kN, box, 0);
     if (!ok) return fail(ctx, CL_E_CUDA, "cuTensorMapEncodeTiled failed");
-    cudaError_t e = cudaMemsetAsync(ctx->d_work, 0, work_bytes, s);
+    cudaError_t e = cudaMemsetAsync(w->d_work, 0, work_bytes, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(scan work)");
     const dim3 tgrid(static_cast<unsigned>((L + 31) / 32), static_cast<unsigned>(Bt), 2);
     transpose_bc_kernel<<<tgrid, 256, 0, s>>>(a.B, a.C, d_Bt, d_Ct, static_cast<int>(L),
@@ -1428,13 +1431,13 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     t.bias = a.delta_bias;
     t.h0 = a.h0;
     t.h_last = a.h_last;
-    t.carry = ctx->d_carry;
-    t.tcarry = ctx->d_tcarry;
+    t.carry = w->d_carry;
+    t.tcarry = w->d_tcarry;
     t.epoch = epoch;
     t.stage_params = aligned16(a.A) && (!a.delta_bias || aligned16(a.delta_bias)) &&
                      (!a.D || aligned16(a.D));
-    t.ticket = ctx->d_work;
-    t.flags = ctx->d_work + 32;
+    t.ticket = w->d_work;
+    t.flags = w->d_work + 32;
     t.batch = Bt;
     t.dim = D;
     t.L = L;

@@ -48,14 +48,22 @@ def _check_f32(name, t, device):
         raise InvalidInput(f"{name} must be contiguous")
 
 
-def _mamba_args(u, delta, A, B, C_, D, z, delta_bias, h0, out, h_last, delta_softplus):
-    batch, dim, L = u.shape
-    N = A.shape[1]
-    dev = u.device
+def check_scan_inputs(u, delta, A, B, C_, D=None, z=None, delta_bias=None, h0=None, out=None,
+                      h_last=None, device=None):
+    """Every tensor a contiguous float32 CUDA tensor on one device, shapes consistent.
+    Runs before ANY kernel is queued: a bf16 or host tensor must never reach a launch
+    (the kernels would read past the allocation or dereference a host pointer)."""
+    if not isinstance(u, torch.Tensor) or u.dim() != 3:
+        raise InvalidInput("u must be a (batch, dim, L) tensor")
+    dev = u.device if device is None else device
     for name, t in (("u", u), ("delta", delta), ("A", A), ("B", B), ("C", C_), ("D", D),
                     ("z", z), ("delta_bias", delta_bias), ("h0", h0), ("out", out),
                     ("h_last", h_last)):
         _check_f32(name, t, dev)
+    batch, dim, L = u.shape
+    if A.dim() != 2:
+        raise InvalidInput("shape mismatch")
+    N = A.shape[1]
     if tuple(delta.shape) != (batch, dim, L) or (z is not None and tuple(z.shape) != (batch, dim, L)):
         raise InvalidInput("shape mismatch")
     if tuple(A.shape) != (dim, N) or tuple(B.shape) != (batch, N, L) or tuple(C_.shape) != (batch, N, L):
@@ -63,6 +71,17 @@ def _mamba_args(u, delta, A, B, C_, D, z, delta_bias, h0, out, h_last, delta_sof
     for t in (D, delta_bias):
         if t is not None and t.numel() != dim:
             raise InvalidInput("shape mismatch")
+    if out is not None and tuple(out.shape) != (batch, dim, L):
+        raise InvalidInput("shape mismatch")
+    for t in (h0, h_last):
+        if t is not None and t.numel() != batch * dim * N:
+            raise InvalidInput("shape mismatch")
+
+
+def _mamba_args(u, delta, A, B, C_, D, z, delta_bias, h0, out, h_last, delta_softplus):
+    check_scan_inputs(u, delta, A, B, C_, D, z, delta_bias, h0, out, h_last)
+    batch, dim, L = u.shape
+    N = A.shape[1]
     a = _lib.cl_mamba1_args()
     a.u, a.delta, a.A, a.B, a.C = _ptr(u), _ptr(delta), _ptr(A), _ptr(B), _ptr(C_)
     a.D, a.z, a.delta_bias, a.h0 = _ptr(D), _ptr(z), _ptr(delta_bias), _ptr(h0)
@@ -83,6 +102,7 @@ def selective_scan_fn(u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_
     chunk).  `decision` (a device cl_decision buffer from Prefill) makes
     the kernel read the chunk from device memory instead.
     """
+    check_scan_inputs(u, delta, A, B, C, D, z, delta_bias, h0, out)
     ctx = Context.get(u.device.index)
     if out is None:
         out = torch.empty_like(u)
@@ -207,8 +227,9 @@ class Prefill:
         self.bounds = bounds or ChunkBounds()
         self.cal = cal or CalibrationRef.log_k(self.spec.bin_count)
         self.policy = policy
-        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
-                                   else torch.device(device).index or 0)
+        idx = None if device is None else torch.device(device).index
+        # 'cuda' without an index means the current device, as everywhere in torch
+        self.device = torch.device("cuda", torch.cuda.current_device() if idx is None else idx)
         self.ctx = Context.get(self.device.index)
         self.cspec = self.spec.to_c()
         self.rule = rule_spec(policy, self.bounds, self.cal)
@@ -285,6 +306,7 @@ class Prefill:
 
     def __call__(self, u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_softplus=True,
                  out=None, return_last_state=False, h0=None) -> PrefillResult:
+        check_scan_inputs(u, delta, A, B, C, D, z, delta_bias, h0, out, device=self.device)
         if u.numel() == 0:
             raise InvalidInput("no samples")
         if self.token:
@@ -307,6 +329,10 @@ class Prefill:
                   h0=None, activation="silu"):
         """The prefill with its producer fused: conv1d(+SiLU) -> u with the min/max
         epilogue, then histogram -> decide -> scan.  Returns (PrefillResult, u)."""
+        # x stands in for u (same shape) until the conv has produced it
+        check_scan_inputs(x, delta, A, B, C, D, z, delta_bias, h0, out, device=self.device)
+        for name, t in (("conv_weight", conv_weight), ("conv_bias", conv_bias)):
+            _check_f32(name, t, self.device)
         if x.numel() == 0:
             raise InvalidInput("no samples")
         u = self.stage_conv(x, conv_weight, conv_bias, activation)

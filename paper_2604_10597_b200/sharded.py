@@ -237,6 +237,8 @@ class ShardedPrefill:
 
     def __call__(self, u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_softplus=True,
                  out=None, return_last_state=False):
+        from .mamba1 import check_scan_inputs
+        check_scan_inputs(u, delta, A, B, C, D, z, delta_bias, None, out, device=self.pf.device)
         if tuple(u.shape) != (self.plan.local_batch, self.plan.local_dim, self.plan.seq_len):
             raise ValueError("u does not match the shard plan")
         if self.pf.token:

@@ -12,12 +12,15 @@ CUDA_INC = "/usr/local/cuda/include"
 CUDA_LIB = "/usr/local/cuda/lib64"
 
 
-def build(out):
+THREADS_SRC = os.path.join(ROOT, "tests", "cpp", "test_threads.cpp")
+
+
+def build(out, src=SRC):
     from paper_2604_10597_b200 import build as b
     b.build()
-    cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), "-I" + CUDA_INC, SRC,
-           "-L" + PKG, "-lchunklab_b200", "-Wl,-rpath," + PKG, "-L" + CUDA_LIB, "-lcudart",
-           "-Wl,-rpath," + CUDA_LIB, "-o", out]
+    cmd = ["g++", "-std=c++20", "-O2", "-pthread", "-I" + os.path.join(ROOT, "include"),
+           "-I" + CUDA_INC, src, "-L" + PKG, "-lchunklab_b200", "-Wl,-rpath," + PKG,
+           "-L" + CUDA_LIB, "-lcudart", "-Wl,-rpath," + CUDA_LIB, "-o", out]
     subprocess.run(cmd, check=True)
     return out
 
@@ -34,3 +37,19 @@ def test_dropin_reference_cases(tmp_path, cuda):
     print(r.stdout[-3000:])
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "0 failed" in r.stdout
+
+
+def test_threads_program_compiles(tmp_path):
+    assert os.path.exists(build(str(tmp_path / "test_threads"), THREADS_SRC))
+
+
+@pytest.mark.gpu
+def test_dropin_threads_and_streams(tmp_path, cuda):
+    """SPEC.md:86 (pure, shareable across threads): 4 host threads through the drop-in's
+    one process-wide context, and two prefills in flight on two streams of it, give the
+    bits each gives alone."""
+    exe = build(str(tmp_path / "test_threads"), THREADS_SRC)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "threads ok" in r.stdout
