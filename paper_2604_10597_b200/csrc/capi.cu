@@ -26,19 +26,34 @@ int fail(cl_ctx*, int code, const std::string& msg) {
 const std::string& thread_error() { return g_error; }
 
 cl_workspace* workspace(cl_ctx* ctx, cudaStream_t stream) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  unsigned long long capture_id = 0;
+  if (cudaStreamGetCaptureInfo(stream, &cs, &capture_id) != cudaSuccess) {
+    cudaGetLastError();
+    cs = cudaStreamCaptureStatusNone;
+  }
+  if (cs != cudaStreamCaptureStatusActive) capture_id = 0;
+  const auto key = std::make_pair(stream, capture_id);
   std::lock_guard<std::mutex> lk(ctx->ws_mu);
-  auto it = ctx->ws.find(stream);
+  auto it = ctx->ws.find(key);
   if (it != ctx->ws.end()) return it->second;
   auto* w = new cl_workspace();
-  cudaError_t e = cudaMalloc(&w->d_hist_ticket, sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(w->d_hist_ticket, 0, sizeof(unsigned long long));
+  w->captured = capture_id != 0;
+  cudaError_t e;
+  {
+    CaptureRelaxed relax;
+    e = cudaMalloc(&w->d_hist_ticket, sizeof(unsigned long long));
+  }
+  // stream-ordered zero (recorded into the graph when capturing)
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(w->d_hist_ticket, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) {
     cudaFree(w->d_hist_ticket);
     delete w;
     cuda_fail(ctx, e, "cudaMalloc(stream workspace)");
     return nullptr;
   }
-  ctx->ws.emplace(stream, w);
+  ctx->ws.emplace(key, w);
   return w;
 }
 
@@ -53,6 +68,7 @@ void free_workspace(cl_workspace* w) {
   cudaFree(w->d_token_raw);
   cudaFree(w->d_token_range);
   cudaFree(w->d_token_counts);
+  for (void* p : w->retired) cudaFree(p);
   delete w;
 }
 }  // namespace
@@ -414,25 +430,18 @@ int validate_token(cl_ctx* ctx, const cl_hist_spec* spec, uint64_t channels, uin
 }
 
 template <typename P>
-int grow_bytes(cl_ctx* ctx, P** ptr, size_t* have, size_t need) {
-  if (*have >= need) return CL_OK;
-  cudaFree(*ptr);
-  *ptr = nullptr;
-  *have = 0;
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), need);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMalloc(token entropy scratch)");
-  *have = need;
-  return CL_OK;
+int grow_bytes(cl_ctx* ctx, P** ptr, size_t* have, size_t need, cl_workspace* w = nullptr) {
+  return grow_scratch(ctx, w, ptr, have, need, "cudaMalloc(token entropy scratch)");
 }
 
 int grow_token(cl_ctx* ctx, cl_workspace* w, uint64_t length, int k) {
-  int rc = grow_bytes(ctx, &w->d_token_raw, &w->token_raw_bytes, length * sizeof(double));
+  int rc = grow_bytes(ctx, &w->d_token_raw, &w->token_raw_bytes, length * sizeof(double), w);
   if (!rc)
     rc = grow_bytes(ctx, &w->d_token_range, &w->token_range_bytes,
-                    (2 * length + 1) * sizeof(double));
+                    (2 * length + 1) * sizeof(double), w);
   if (!rc)
     rc = grow_bytes(ctx, &w->d_token_counts, &w->token_counts_bytes,
-                    length * static_cast<size_t>(k) * sizeof(unsigned int));
+                    length * static_cast<size_t>(k) * sizeof(unsigned int), w);
   return rc;
 }
 
@@ -520,7 +529,7 @@ int cl_token_entropy_counts(cl_ctx* ctx, const uint32_t* d_counts, const double*
   DeviceGuard g(ctx->device);
   cl_workspace* w = workspace(ctx, static_cast<cudaStream_t>(stream));
   if (!w) return CL_E_CUDA;
-  if ((rc = grow_bytes(ctx, &w->d_token_raw, &w->token_raw_bytes, length * sizeof(double))))
+  if ((rc = grow_bytes(ctx, &w->d_token_raw, &w->token_raw_bytes, length * sizeof(double), w)))
     return rc;
   ctx->launches += 2;
   return check_launch(ctx,

@@ -8,6 +8,8 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "chunklab_capi.h"
 
@@ -34,6 +36,10 @@ struct cl_workspace {
   // arrival ticket of the fused histogram -> decision launch: 0 between launches (the
   // last CTA resets it), never visible to callers
   unsigned long long* d_hist_ticket = nullptr;
+  // created inside a CUDA-graph capture: its buffers are baked into that graph, which
+  // may replay many times, so per-launch state (tagged-carry epochs) is reset in-graph
+  bool captured = false;
+  std::vector<void*> retired;  // buffers outgrown during a capture (freed with the ctx)
   // device-path token_entropy scratch
   double* d_token_raw = nullptr;
   size_t token_raw_bytes = 0;
@@ -47,9 +53,10 @@ struct cl_ctx {
   int device = 0;
   int num_sms = 148;
   std::atomic<uint64_t> launches{0};
-  // one workspace per stream handle (created on first use, freed with the context)
+  // one workspace per (stream handle, CUDA-graph capture id -- 0 outside a capture),
+  // created on first use, freed with the context
   std::mutex ws_mu;
-  std::map<cudaStream_t, cl_workspace*> ws;
+  std::map<std::pair<cudaStream_t, unsigned long long>, cl_workspace*> ws;
   // The host path (*_host) and its scratch: serialised per context, so the drop-in C++
   // API (one process-wide context) stays reentrant and thread-safe (reference SPEC.md:86).
   std::recursive_mutex host_mu;
@@ -73,12 +80,26 @@ int cuda_fail(cl_ctx* ctx, cudaError_t e, const char* where);
 const std::string& thread_error();
 
 // The workspace of `stream` (created on first use); nullptr + error on allocation failure.
+// Inside a stream capture each capture gets its own workspace (keyed by capture id).
 cl_workspace* workspace(cl_ctx* ctx, cudaStream_t stream);
 
+// cudaMalloc is not allowed while a stream captures in the default (global) mode; a
+// library may switch the calling thread to relaxed mode around its own allocations.
+struct CaptureRelaxed {
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  CaptureRelaxed() { cudaThreadExchangeStreamCaptureMode(&mode); }
+  ~CaptureRelaxed() { cudaThreadExchangeStreamCaptureMode(&mode); }
+};
+
 template <typename T>
-int grow_scratch(cl_ctx* ctx, T** ptr, size_t* have, size_t need, const char* what) {
+int grow_scratch(cl_ctx* ctx, cl_workspace* w, T** ptr, size_t* have, size_t need,
+                 const char* what) {
   if (*have >= need) return 0;
-  if (*ptr) cudaFree(*ptr);
+  CaptureRelaxed relax;
+  if (*ptr) {
+    if (w && w->captured) w->retired.push_back(*ptr);  // no cudaFree inside a capture
+    else cudaFree(*ptr);
+  }
   *ptr = nullptr;
   *have = 0;
   cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), need);

@@ -118,6 +118,9 @@ __device__ __forceinline__ int bin_fast(float v, const BinParams& p, bool* slow)
   // written as !(d <= thr) so NaN / inf samples (flagged by minmax) take the exact path
   *slow = !(fabsf(x - rn) <= p.thr) || big;
   if (FIXED) n = min(max(n, 0), p.k - 1);
+  // Dynamic range: a sample outside the supplied range (a caller's d_range that does
+  // not cover the data) takes the exact, clamping path (entropy.hpp:91-92)
+  if (!FIXED) *slow |= static_cast<uint32_t>(n) >= static_cast<uint32_t>(p.k);
   return n;
 }
 

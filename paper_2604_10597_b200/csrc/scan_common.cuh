@@ -1,0 +1,679 @@
+// scan_common.cuh -- device and host building blocks shared by the fused Mamba-1 scan
+// kernels (scan_mamba1.cu: chained-carry kernels; scan_lookback.cu: the L-parallel
+// kernel for few-row shapes).  Everything is in an anonymous namespace: each
+// translation unit gets its own copy (device code is inlined anyway).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "cl_internal.h"
+
+namespace cl {
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// ---- canonical elementwise math ----
+// Every Mamba-1 path (generic scan, TMA scans, decode) evaluates softplus, SiLU and, for
+// N = 16, C.h with exactly these operation sequences, so the paths agree bit for bit
+// and a prefill followed by decode steps equals a longer prefill bit for bit (the
+// paper's passive-vs-routed claim is bitwise output equality).  The
+// FFMA2 versions further down (softplus2 / silu2 / the lane-pair C.h) are these
+// functions applied per lane of a register pair.
+
+// softplus(x) = max(x,0) + log1p(exp(-|x|)): one MUFU.EX2 and a degree-9 minimax
+// polynomial for log1p on [0,1] (max rel err 2e-7; equals x to fp32 above 20).
+__device__ __forceinline__ float softplus_canon(float a) {
+  const float e = ex2_approx(-fabsf(a) * kLog2e);
+  float q = 0.005253826278033571f;
+  q = fmaf(q, e, -0.02959069552080005f);
+  q = fmaf(q, e, 0.07836660226277938f);
+  q = fmaf(q, e, -0.13675328086246433f);
+  q = fmaf(q, e, 0.19111774195698683f);
+  q = fmaf(q, e, -0.24844483411506615f);
+  q = fmaf(q, e, 0.33319289806287417f);
+  q = fmaf(q, e, -0.49999502673812024f);
+  q = fmaf(q, e, 0.9999999706625772f);
+  return fmaf(q, e, fmaxf(a, 0.f));
+}
+
+// z * sigmoid(z): one MUFU.EX2, reciprocal by 3 Newton steps from the bit-trick seed.
+__device__ __forceinline__ float silu_canon(float z) {
+  const float e = ex2_approx(fmaxf(z, -80.f) * -kLog2e);
+  const float d = e + 1.f;
+  float r = __int_as_float(0x7EF311C7 - __float_as_int(d));
+  const float nd = d * -1.f;
+#pragma unroll
+  for (int it = 0; it < 3; ++it) {
+    const float en = fmaf(nd, r, 1.f);
+    r = fmaf(r, en, r);
+  }
+  return z * r;
+}
+
+// y = sum_s c[s] h[s] for N = 16 in the lane-pair kernel's order: lane half hf holds
+// states 8hf..8hf+7 and accumulates, as FFMA2 chains started from +0,
+//   ya = (s0,s1) then (s4,s5),   yb = (s2,s3) then (s6,s7)
+// then L_hf = (ya.lo + yb.lo) + (ya.hi + yb.hi); y = L_0 + L_1.  Every step is an
+// explicit fused multiply-add or a plain add of two values that are not products, so no
+// compiler can contract it differently on different paths.
+__device__ __forceinline__ float cdot16_canon(const float* c, const float* h) {
+  float L[2];
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+    const float* cc = c + 8 * hf;
+    const float* hh = h + 8 * hf;
+    const float ya_lo = fmaf(cc[4], hh[4], fmaf(cc[0], hh[0], 0.f));
+    const float ya_hi = fmaf(cc[5], hh[5], fmaf(cc[1], hh[1], 0.f));
+    const float yb_lo = fmaf(cc[6], hh[6], fmaf(cc[2], hh[2], 0.f));
+    const float yb_hi = fmaf(cc[7], hh[7], fmaf(cc[3], hh[3], 0.f));
+    L[hf] = __fadd_rn(__fadd_rn(ya_lo, yb_lo), __fadd_rn(ya_hi, yb_hi));
+  }
+  return __fadd_rn(L[0], L[1]);
+}
+
+__device__ __forceinline__ int read_chunk(const cl_decision* d, int fixed_chunk, int* status) {
+  if (d) {
+    *status = d->status;
+    return d->chunk;
+  }
+  *status = 0;
+  return fixed_chunk;
+}
+
+// ---------------------------------------------------------------------------
+// Generic kernel
+// ---------------------------------------------------------------------------
+struct GenericArgs {
+  const float *u, *delta, *A, *B, *C, *D, *z, *bias, *h0;
+  float *out, *h_last;
+  uint64_t batch, dim, L;
+  int N;
+  int softplus;
+  const cl_decision* decision;
+};
+
+template <int NS>
+__global__ void __launch_bounds__(128) generic_kernel(GenericArgs a) {
+  if (a.decision && a.decision->status != 0) return;
+  const uint64_t row = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= a.batch * a.dim) return;
+  const int N = NS > 0 ? NS : a.N;
+  const uint64_t b = row / a.dim, c = row % a.dim;
+  float h[NS > 0 ? NS : 64];
+  float A2[NS > 0 ? NS : 64];
+#pragma unroll
+  for (int s = 0; s < (NS > 0 ? NS : 64); ++s) {
+    if (s < N) {
+      h[s] = a.h0 ? a.h0[row * N + s] : 0.f;
+      A2[s] = a.A[c * N + s] * kLog2e;
+    }
+  }
+  const float bias = a.bias ? a.bias[c] : 0.f;
+  const float Dc = a.D ? a.D[c] : 0.f;
+  const float* Bb = a.B + b * N * a.L;
+  const float* Cb = a.C + b * N * a.L;
+  for (uint64_t t = 0; t < a.L; ++t) {
+    const float u = a.u[row * a.L + t];
+    float dt = a.delta[row * a.L + t] + bias;
+    if (a.softplus) dt = softplus_canon(dt);
+    const float x = __fmul_rn(dt, u);
+    float y = 0.f;
+    if (NS == 16) {
+      float cv[16];
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        const float dA = ex2_approx(A2[s] * dt);
+        h[s] = fmaf(dA, h[s], __fmul_rn(Bb[s * a.L + t], x));
+        cv[s] = Cb[s * a.L + t];
+      }
+      y = cdot16_canon(cv, h);
+    } else {
+#pragma unroll
+      for (int s = 0; s < (NS > 0 ? NS : 64); ++s) {
+        if (s < N) {
+          const float dA = ex2_approx(A2[s] * dt);
+          h[s] = fmaf(dA, h[s], __fmul_rn(Bb[s * a.L + t], x));
+          y = fmaf(Cb[s * a.L + t], h[s], y);
+        }
+      }
+    }
+    y = fmaf(Dc, u, y);
+    if (a.z) y *= silu_canon(a.z[row * a.L + t]);
+    a.out[row * a.L + t] = y;
+  }
+  if (a.h_last) {
+#pragma unroll
+    for (int s = 0; s < (NS > 0 ? NS : 64); ++s)
+      if (s < N) a.h_last[row * N + s] = h[s];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Decode step: one token through the recurrence, state updated in
+// place -- mamba_ssm's selective_state_update(state, x, dt, A, B, C, D, z, dt_bias,
+// dt_softplus) semantics, with the canonical math above so that prefill(L) followed by
+// decode steps reproduces prefill(L + k) bit for bit.  One thread per (b, d) row.
+// ---------------------------------------------------------------------------
+struct DecodeArgs {
+  float* state;  // (batch, dim, N), in/out
+  const float *x, *dt, *A, *B, *C, *D, *z, *dt_bias;
+  float* out;  // (batch, dim)
+  uint64_t batch, dim;
+  int N;
+  int softplus;
+};
+
+template <int NS>
+__global__ void __launch_bounds__(128) decode_kernel(DecodeArgs a) {
+  const uint64_t row = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= a.batch * a.dim) return;
+  const int N = NS > 0 ? NS : a.N;
+  const uint64_t b = row / a.dim, c = row - b * a.dim;
+  float dt = a.dt[row] + (a.dt_bias ? a.dt_bias[c] : 0.f);
+  if (a.softplus) dt = softplus_canon(dt);
+  const float u = a.x[row];
+  const float xx = __fmul_rn(dt, u);
+  float* st = a.state + row * N;
+  const float* Bb = a.B + b * N;
+  const float* Cb = a.C + b * N;
+  float y = 0.f;
+  if (NS == 16) {
+    float h[16], cv[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const float dA = ex2_approx((a.A[c * 16 + s] * kLog2e) * dt);
+      h[s] = fmaf(dA, st[s], __fmul_rn(Bb[s], xx));
+      cv[s] = Cb[s];
+    }
+    y = cdot16_canon(cv, h);
+#pragma unroll
+    for (int s = 0; s < 16; ++s) st[s] = h[s];
+  } else {
+    for (int s = 0; s < N; ++s) {
+      const float dA = ex2_approx((a.A[c * N + s] * kLog2e) * dt);
+      const float h = fmaf(dA, st[s], __fmul_rn(Bb[s], xx));
+      y = fmaf(Cb[s], h, y);
+      st[s] = h;
+    }
+  }
+  y = fmaf(a.D ? a.D[c] : 0.f, u, y);
+  if (a.z) y *= silu_canon(a.z[row]);
+  a.out[row] = y;
+}
+
+// ---------------------------------------------------------------------------
+// TMA kernels (N = 16): shared helpers, then the 32-row row-sequential kernel
+// ---------------------------------------------------------------------------
+constexpr int kN = 16;
+constexpr int kRows = 32;  // rows per tile = lanes per warp
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_le1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned int* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned int* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// two 64-bit words per access (each word single-copy atomic: a tag and its value)
+__device__ __forceinline__ void ld_relaxed_u64x2(const unsigned long long* p,
+                                                 unsigned long long& a, unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_u64x2(unsigned long long* p, unsigned long long a,
+                                                 unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+// ---- packed fp32x2 (FFMA2) helpers: a 64-bit register pair holds two fp32 lanes ----
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t pk(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk(f2_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// softplus for a pair, branch-free: max(x,0) + log1p(exp(-|x|)), log1p by a degree-9
+// minimax polynomial on [0,1] (max rel err 2e-7 in fp32).  Equals x to fp32 precision
+// above 20, matching mamba_ssm's threshold.
+__device__ __forceinline__ f2_t softplus2(f2_t x) {
+  float a, b;
+  upk(x, a, b);
+  const f2_t e = pk(ex2_approx(-fabsf(a) * kLog2e), ex2_approx(-fabsf(b) * kLog2e));
+  f2_t q = pk(0.005253826278033571f, 0.005253826278033571f);
+  q = fma2(q, e, pk(-0.02959069552080005f, -0.02959069552080005f));
+  q = fma2(q, e, pk(0.07836660226277938f, 0.07836660226277938f));
+  q = fma2(q, e, pk(-0.13675328086246433f, -0.13675328086246433f));
+  q = fma2(q, e, pk(0.19111774195698683f, 0.19111774195698683f));
+  q = fma2(q, e, pk(-0.24844483411506615f, -0.24844483411506615f));
+  q = fma2(q, e, pk(0.33319289806287417f, 0.33319289806287417f));
+  q = fma2(q, e, pk(-0.49999502673812024f, -0.49999502673812024f));
+  q = fma2(q, e, pk(0.9999999706625772f, 0.9999999706625772f));
+  return fma2(q, e, pk(fmaxf(a, 0.f), fmaxf(b, 0.f)));
+}
+
+// z * sigmoid(z) for a pair: one MUFU.EX2 per lane, reciprocal by Newton iterations
+// on the FMA pipe (3 steps from the bit-trick seed: rel err < 1e-7).
+__device__ __forceinline__ f2_t silu2(f2_t z) {
+  float a, b;
+  upk(z, a, b);
+  const f2_t e =
+      pk(ex2_approx(fmaxf(a, -80.f) * -kLog2e), ex2_approx(fmaxf(b, -80.f) * -kLog2e));
+  const f2_t d = add2(e, pk(1.f, 1.f));
+  float dl, dh;
+  upk(d, dl, dh);
+  f2_t r = pk(__int_as_float(0x7EF311C7 - __float_as_int(dl)),
+              __int_as_float(0x7EF311C7 - __float_as_int(dh)));
+  const f2_t one = pk(1.f, 1.f);
+  const f2_t nd = mul2(d, pk(-1.f, -1.f));
+#pragma unroll
+  for (int it = 0; it < 3; ++it) {
+    const f2_t e = fma2(nd, r, one);
+    r = fma2(r, e, r);
+  }
+  return mul2(z, r);
+}
+
+struct TmaArgs {
+  const float *A, *D, *bias, *h0;
+  float* out;              // y, for the direct-store (warp-specialised) kernel
+  float* h_last;
+  float* carry;            // [n_tiles][32][16]
+  unsigned int* flags;     // [n_tiles] completed segments
+  unsigned long long* tcarry;  // [n_tiles][16][16] {tag << 32 | h bits} (rowpair_ws_kernel)
+  unsigned int epoch;          // tag of segment s's carry-in = epoch + s
+  int stage_params;            // A / bias / D 16-byte aligned: the producer stages a full
+                               // tile's rows of them into shared memory with the item's first box
+  unsigned int* ticket;    // work counter
+  uint64_t batch, dim, L;
+  int tiles_per_batch;
+  int n_tiles;
+  const cl_decision* decision;
+  int fixed_chunk;
+};
+
+struct Item {
+  int tile, seg, nbox;
+  int t0;
+};
+
+// Geometry: BOX timesteps per TMA box (32/16/8 -> 128B/64B/32B swizzle),
+// WARPS independent warps per CTA, STAGES-deep per-warp TMA ring.
+template <int BOX>
+struct Geo {
+  static constexpr int kTileBytes = kRows * BOX * 4;            // u / delta / z / y
+  static constexpr int kBCBytes = BOX * kN * 4;                 // B^T or C^T  [BOX][16]
+  static constexpr int kStageBytes = 3 * kTileBytes + 2 * kBCBytes;
+  // 16B-chunk j (4 timesteps) of row r inside a swizzled [32 x BOX] box
+  static __device__ __forceinline__ int swz(int r, int j) {
+    if (BOX == 32) return r * 128 + ((j ^ (r & 7)) << 4);        // SWIZZLE_128B
+    if (BOX == 16) return r * 64 + ((j ^ ((r >> 1) & 3)) << 4);  // SWIZZLE_64B
+    return r * 32 + ((j ^ ((r >> 2) & 1)) << 4);                 // SWIZZLE_32B
+  }
+};
+
+// ---------------------------------------------------------------------------
+// lane-pair building blocks (a consumer warp owns a 16-row tile; lanes (2r, 2r+1) share
+// row r, states 0-7 / 8-15 in FFMA2 register pairs)
+// ---------------------------------------------------------------------------
+constexpr int kRowsP = 16;
+#ifndef CL_PROD_SLEEP_NS
+#define CL_PROD_SLEEP_NS 32
+#endif
+
+template <int BOX>
+struct GeoP {
+  static constexpr int kTileBytes = kRowsP * BOX * 4;  // u / delta / z: [16 rows][BOX]
+  static constexpr int kBCBytes = BOX * 2 * kN * 4;    // [BOX][B 0..15 | C 0..15]
+  static constexpr int kStageBytes = 3 * kTileBytes + kBCBytes;
+  // per-item parameters staged with an item's first box: A rows [16][16], bias [16], D [16]
+  static constexpr int kParamBytes = kRowsP * kN * 4 + 2 * kRowsP * 4;
+};
+constexpr int kStagedFlag = 1 << 30;  // meta.y bit: this item's parameters are in shared memory
+
+__device__ __forceinline__ f2_t shfl_xor2(f2_t v, int m) {
+  float lo, hi;
+  upk(v, lo, hi);
+  return pk(__shfl_xor_sync(0xffffffffu, lo, m), __shfl_xor_sync(0xffffffffu, hi, m));
+}
+
+// One 16-row x BOX-timestep box: lane (r, hf) owns row r's states 8hf..8hf+7.  Reads
+// u / delta / z / [B | C] from the TMA stage `st`, advances the carried state h2 and
+// stores y for timesteps (4j + 2hf, 4j + 2hf + 1) of row r to ydst (nullptr: pad row).
+template <int BOX, bool SP, bool HZ>
+__device__ __forceinline__ void pair_box(const unsigned char* st, float* ydst, int r, int hf,
+                                         int valid, float bias, float Dc,
+                                         const f2_t (&A2p)[kN / 4], f2_t (&h2)[kN / 4]) {
+  using G = GeoP<BOX>;
+  constexpr int kP = kN / 4;
+  constexpr int kBCRow = 2 * kN * 4;
+  const unsigned char* sB = st + 3 * G::kTileBytes + 32 * hf;  // this lane's 8 states
+  const unsigned char* sC = sB + kN * 4;
+  const f2_t bias2 = pk(bias, bias);
+  // fully unrolled over the box's 4-timestep groups: straight-line code lets the
+  // scheduler interleave group j+1's exponentials with group j's FFMA2 chains
+#pragma unroll
+  for (int j = 0; j < BOX / 4; ++j) {
+    if (4 * j >= valid) break;
+    const int off = Geo<BOX>::swz(r, j);
+    const float4 u4 = *reinterpret_cast<const float4*>(st + off);
+    const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
+    // softplus of timesteps (2hf, 2hf+1) here, the other pair from the partner lane
+    f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
+    if (SP) mine = softplus2(mine);
+    const f2_t other = shfl_xor2(mine, 1);
+    const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
+    const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
+    float dt[4], xs[4];
+    upk(dt01, dt[0], dt[1]);
+    upk(dt23, dt[2], dt[3]);
+    upk(x01, xs[0], xs[1]);
+    upk(x23, xs[2], xs[3]);
+    // the 4x8 transition factors exp(dt*A) do not depend on the state: issue them all
+    f2_t dA[4][kP];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const f2_t dd = pk(dt[k], dt[k]);
+#pragma unroll
+      for (int i = 0; i < kP; ++i) {
+        float al, ah;
+        upk(mul2(A2p[i], dd), al, ah);
+        dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+      }
+    }
+    float yp[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = 4 * j + k;
+      const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + t * kBCRow);
+      const ulonglong2* Ct = reinterpret_cast<const ulonglong2*>(sC + t * kBCRow);
+      const f2_t xx = pk(xs[k], xs[k]);
+      f2_t ya = 0ull, yb = 0ull;  // canonical FFMA2 chains (cdot16_canon)
+#pragma unroll
+      for (int q = 0; q < kP / 2; ++q) {
+        const ulonglong2 bq = Bt[q];
+        const ulonglong2 cq = Ct[q];
+        h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
+        h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
+        ya = fma2(cq.x, h2[2 * q], ya);
+        yb = fma2(cq.y, h2[2 * q + 1], yb);
+      }
+      float a0, a1;
+      upk(add2(ya, yb), a0, a1);
+      yp[k] = a0 + a1;
+    }
+    // lane hf finalises timesteps (2hf, 2hf+1): swap the partial sums it does not own
+    const f2_t keep = hf ? pk(yp[2], yp[3]) : pk(yp[0], yp[1]);
+    const f2_t give = hf ? pk(yp[0], yp[1]) : pk(yp[2], yp[3]);
+    const f2_t ysum = add2(keep, shfl_xor2(give, 1));
+    const f2_t u2 = hf ? pk(u4.z, u4.w) : pk(u4.x, u4.y);
+    f2_t yo = fma2(pk(Dc, Dc), u2, ysum);
+    if (HZ) {
+      const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
+      yo = mul2(yo, silu2(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y)));
+    }
+    if (ydst) {
+      float y0, y1;
+      upk(yo, y0, y1);
+      __stcs(reinterpret_cast<float2*>(ydst + 4 * j + 2 * hf), make_float2(y0, y1));
+    }
+  }
+}
+
+// pair_box for a full box (valid == BOX), software-pipelined by one 4-timestep group:
+// group j+1's serial prologue (LDS of u / delta / z, bias add, softplus -- one MUFU then
+// a 9-deep FFMA2 chain -- the partner-lane shuffle and the SiLU(z) gate) is issued between group j's
+// exponentials and its recurrence, so its latency hides under group j's MUFU work
+// instead of stalling the MUFU pipe at every group boundary.  Same operations on the
+// same values as pair_box, so the outputs are bit-identical.
+template <int BOX, bool SP, bool HZ>
+__device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* ydst, int r,
+                                              int hf, float bias, float Dc,
+                                              const f2_t (&A2p)[kN / 4], f2_t (&h2)[kN / 4]) {
+  using G = GeoP<BOX>;
+  constexpr int kP = kN / 4;
+  constexpr int kG = BOX / 4;
+  constexpr int kBCRow = 2 * kN * 4;
+  const unsigned char* sB = st + 3 * G::kTileBytes + 32 * hf;
+  const unsigned char* sC = sB + kN * 4;
+  const f2_t bias2 = pk(bias, bias);
+  // prologue of group j: dt (4 timesteps, softplus'd), x = dt*u, and this lane's u pair
+  auto prep = [&](int j, float (&dt)[4], float (&xs)[4], f2_t& u2, f2_t& g2) {
+    const int off = Geo<BOX>::swz(r, j);
+    const float4 u4 = *reinterpret_cast<const float4*>(st + off);
+    const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
+    f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
+    if (SP) mine = softplus2(mine);
+    const f2_t other = shfl_xor2(mine, 1);
+    const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
+    const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
+    upk(dt01, dt[0], dt[1]);
+    upk(dt23, dt[2], dt[3]);
+    upk(x01, xs[0], xs[1]);
+    upk(x23, xs[2], xs[3]);
+    u2 = hf ? pk(u4.z, u4.w) : pk(u4.x, u4.y);
+    if (HZ) {
+      const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
+      g2 = silu2(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y));
+    }
+  };
+  float dt[4], xs[4];
+  f2_t u2, g2 = 0ull;
+  prep(0, dt, xs, u2, g2);
+#pragma unroll
+  for (int j = 0; j < kG; ++j) {
+    f2_t dA[4][kP];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const f2_t dd = pk(dt[k], dt[k]);
+#pragma unroll
+      for (int i = 0; i < kP; ++i) {
+        float al, ah;
+        upk(mul2(A2p[i], dd), al, ah);
+        dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+      }
+    }
+    float ndt[4], nxs[4];
+    f2_t nu2 = 0ull, ng2 = 0ull;
+    if (j + 1 < kG) prep(j + 1, ndt, nxs, nu2, ng2);
+    float yp[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = 4 * j + k;
+      const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + t * kBCRow);
+      const ulonglong2* Ct = reinterpret_cast<const ulonglong2*>(sC + t * kBCRow);
+      const f2_t xx = pk(xs[k], xs[k]);
+      f2_t ya = 0ull, yb = 0ull;  // canonical FFMA2 chains (cdot16_canon)
+#pragma unroll
+      for (int q = 0; q < kP / 2; ++q) {
+        const ulonglong2 bq = Bt[q];
+        const ulonglong2 cq = Ct[q];
+        h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
+        h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
+        ya = fma2(cq.x, h2[2 * q], ya);
+        yb = fma2(cq.y, h2[2 * q + 1], yb);
+      }
+      float a0, a1;
+      upk(add2(ya, yb), a0, a1);
+      yp[k] = a0 + a1;
+    }
+    const f2_t keep = hf ? pk(yp[2], yp[3]) : pk(yp[0], yp[1]);
+    const f2_t give = hf ? pk(yp[0], yp[1]) : pk(yp[2], yp[3]);
+    const f2_t ysum = add2(keep, shfl_xor2(give, 1));
+    f2_t yo = fma2(pk(Dc, Dc), u2, ysum);
+    if (HZ) yo = mul2(yo, g2);
+    if (ydst) {
+      float y0, y1;
+      upk(yo, y0, y1);
+      __stcs(reinterpret_cast<float2*>(ydst + 4 * j + 2 * hf), make_float2(y0, y1));
+    }
+    if (j + 1 < kG) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        dt[k] = ndt[k];
+        xs[k] = nxs[k];
+      }
+      u2 = nu2;
+      g2 = ng2;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps through the driver entry point (no libcuda link)
+// ---------------------------------------------------------------------------
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const float* base, uint64_t d0, uint64_t d1, uint64_t d2,
+              uint32_t box0, uint32_t box1, int swizzle_bytes) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {d0 * 4, d0 * d1 * 4};
+  const cuuint32_t box[3] = {box0, box1, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                      : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool tma_eligible(const cl_mamba1_args& a) {
+  if (a.d_state != kN) return false;
+  if (a.seq_len % 4 != 0) return false;
+  if (a.seq_len > (1u << 30) || a.dim > (1u << 30) || a.batch > (1u << 30)) return false;
+  const void* ps[] = {a.u, a.delta, a.out, a.B, a.C, a.A};
+  for (const void* p : ps)
+    if (!aligned16(p)) return false;
+  if (a.z && !aligned16(a.z)) return false;
+  if (a.h0 && !aligned16(a.h0)) return false;
+  if (a.h_last && !aligned16(a.h_last)) return false;
+  return get_encode() != nullptr;
+}
+
+
+}  // namespace
+}  // namespace cl
