@@ -216,13 +216,36 @@ typedef struct {
   int delta_softplus;
 } cl_mamba1_args;
 
-/* Scan variants (all bit-identical): CL_SCAN_AUTO picks by shape.  CL_SCAN_CONFIG_BASE + i
- * forces row i of the TMA kernel table (scan_mamba1.cu kCfgs: lane-pair / quad / row
- * kernels and their warp counts) -- for A/B measurements and the bitwise cross-checks. */
-enum { CL_SCAN_AUTO = 0, CL_SCAN_ROWSEQ_TMA = 1, CL_SCAN_GENERIC = 2, CL_SCAN_CONFIG_BASE = 16 };
+/* Scan variants.  CL_SCAN_AUTO picks by shape: the chained-carry kernels for shapes with
+ * enough 16-row tiles to fill the GPU, the L-parallel kernel (scan_lookback.cu) for few
+ * rows.  Every chained variant (CL_SCAN_ROWSEQ_TMA, CL_SCAN_GENERIC, CL_SCAN_CHAINED,
+ * CL_SCAN_CONFIG_BASE + i = row i of scan_mamba1.cu's kCfgs) gives the same bits for every
+ * chunk.  The L-parallel kernel splits L by the shape, never by the chunk, so its bits are
+ * also chunk-independent; against the chained kernels it agrees to rounding (<= 1e-6
+ * normwise: the segment carry-in is a fold of segment aggregates).  CL_SCAN_LOOKBACK
+ * forces it, CL_SCAN_LOOKBACK_BASE + i forces its table row i. */
+enum {
+  CL_SCAN_AUTO = 0,
+  CL_SCAN_ROWSEQ_TMA = 1,
+  CL_SCAN_GENERIC = 2,
+  CL_SCAN_LOOKBACK = 3,
+  CL_SCAN_CHAINED = 4,
+  CL_SCAN_CONFIG_BASE = 16,
+  CL_SCAN_LOOKBACK_BASE = 64
+};
 int cl_selective_scan_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_decision* d_decision,
                           int fixed_chunk /* used when d_decision == NULL */, int variant,
                           void* stream);
+
+/* Which kernel cl_selective_scan_f32 runs for these arguments and variant (host-only
+ * query, no launch): kernel kind, its table row, TMA box (timesteps), consumer warps per
+ * CTA, ring stages, and for the L-parallel kernel its shape-tied split (n_seg segments of
+ * seg_len timesteps; -1 for the chained kernels, whose segment is the decided chunk). */
+enum { CL_KERNEL_GENERIC = 0, CL_KERNEL_CHAINED = 1, CL_KERNEL_ROWSEQ = 2, CL_KERNEL_LOOKBACK = 3 };
+typedef struct {
+  int kernel, config, box, warps, stages, n_seg, seg_len;
+} cl_scan_plan;
+int cl_scan_plan_f32(cl_ctx* ctx, const cl_mamba1_args* args, int variant, cl_scan_plan* out);
 
 /* Single-GPU convenience: range_init -> minmax -> histogram -> decide -> scan,
  * all on one stream, no host sync.  d_counts: K uint64 scratch; d_range: 4 doubles. */

@@ -18,7 +18,11 @@ CL_RANGE_DYNAMIC, CL_RANGE_FIXED = 0, 1
 (CL_POL_STATIC, CL_POL_MIDPOINT, CL_POL_FULL_HIST, CL_POL_SAMPLED_HIST, CL_POL_LEARNED_TABLE,
  CL_POL_GUARDED, CL_POL_RULE, CL_POL_TOKEN_HIST) = range(8)
 CL_SRC_GUARDED, CL_SRC_GUARDED_FALLBACK = 16, 32
-CL_SCAN_AUTO, CL_SCAN_ROWSEQ_TMA, CL_SCAN_GENERIC, CL_SCAN_CONFIG_BASE = 0, 1, 2, 16
+CL_SCAN_AUTO, CL_SCAN_ROWSEQ_TMA, CL_SCAN_GENERIC, CL_SCAN_LOOKBACK, CL_SCAN_CHAINED = range(5)
+CL_SCAN_CONFIG_BASE, CL_SCAN_LOOKBACK_BASE = 16, 64
+CL_KERNEL_GENERIC, CL_KERNEL_CHAINED, CL_KERNEL_ROWSEQ, CL_KERNEL_LOOKBACK = range(4)
+KERNEL_NAMES = {0: "generic_kernel", 1: "rowpair_ws_kernel", 2: "rowseq_tma_kernel",
+                3: "lookback_ws_kernel"}
 
 SOURCE_NAMES = {0: "static", 1: "no_entropy_midpoint", 2: "full_histogram",
                 3: "sampled_histogram", 4: "learned_table", 6: "rule", 7: "token_histogram"}
@@ -76,6 +80,11 @@ class cl_state_update_args(C.Structure):
                 ("dim", C.c_uint64), ("d_state", C.c_uint64), ("dt_softplus", C.c_int)]
 
 
+class cl_scan_plan(C.Structure):
+    _fields_ = [("kernel", C.c_int), ("config", C.c_int), ("box", C.c_int), ("warps", C.c_int),
+                ("stages", C.c_int), ("n_seg", C.c_int), ("seg_len", C.c_int)]
+
+
 class cl_scan_params_f64(C.Structure):
     _fields_ = [("channels", C.c_uint64), ("state_dim", C.c_uint64), ("seq_len", C.c_uint64),
                 ("a", C.c_void_p), ("b", C.c_void_p), ("c", C.c_void_p), ("d", C.c_void_p),
@@ -119,6 +128,7 @@ SIGNATURES = {
     "cl_selective_scan_f32": (C.c_int, [_P, C.POINTER(cl_mamba1_args), _P, C.c_int, C.c_int,
                                         _P]),
     "cl_selective_state_update_f32": (C.c_int, [_P, C.POINTER(cl_state_update_args), _P]),
+    "cl_scan_plan_f32": (C.c_int, [_P, C.POINTER(cl_mamba1_args), C.c_int, C.POINTER(cl_scan_plan)]),
     "cl_prefill_f32": (C.c_int, [_P, C.POINTER(cl_mamba1_args), C.POINTER(cl_hist_spec),
                                  C.POINTER(cl_rule_spec), _P, _P, _P, _P]),
     "cl_decision_check": (C.c_int, [_P, _P, C.POINTER(cl_decision), _P]),

@@ -586,6 +586,11 @@ int cl_selective_scan_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_deci
   return scan_mamba1(ctx, a, d_decision, fixed_chunk, variant, static_cast<cudaStream_t>(stream));
 }
 
+int cl_scan_plan_f32(cl_ctx* ctx, const cl_mamba1_args* args, int variant, cl_scan_plan* out) {
+  if (!ctx || !args || !out) return fail(ctx, CL_E_INVALID, "null argument");
+  return scan_plan(ctx, *args, variant, out);
+}
+
 int cl_selective_state_update_f32(cl_ctx* ctx, const cl_state_update_args* args, void* stream) {
   if (!ctx || !args) return fail(ctx, CL_E_INVALID, "null argument");
   const cl_state_update_args& a = *args;

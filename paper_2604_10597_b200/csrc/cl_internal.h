@@ -168,5 +168,6 @@ cudaError_t launch_scan_f64(const cl_scan_params_f64& p, const double* d_h0, uin
 int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decision,
                 int fixed_chunk, int variant, cudaStream_t s);
 int state_update_f32(cl_ctx* ctx, const cl_state_update_args& a, cudaStream_t s);
+int scan_plan(cl_ctx* ctx, const cl_mamba1_args& a, int variant, cl_scan_plan* p);
 
 }  // namespace cl

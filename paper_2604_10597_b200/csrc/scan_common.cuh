@@ -677,3 +677,24 @@ bool tma_eligible(const cl_mamba1_args& a) {
 
 }  // namespace
 }  // namespace cl
+
+namespace cl {
+// ---- the L-parallel kernel (scan_lookback.cu), launched by scan_mamba1() ----
+struct LookbackLaunch {
+  const float *A, *D, *bias, *h0;
+  float* out;
+  float* h_last;
+  unsigned long long* agg;  // [n_tiles][n_seg][16][18] tagged words
+  unsigned int epoch;
+  int stage_params;
+  unsigned int* ticket;
+  uint64_t batch, dim, L;
+  int tiles_per_batch, n_tiles, seg_len, n_seg;
+  const cl_decision* decision;
+};
+constexpr int kLookbackCfgs = 5;
+int lookback_warps(int cfg);
+int lookback_box(int cfg);
+cudaError_t launch_lookback(int cfg, bool sp, bool hz, const CUtensorMap* maps,
+                            const LookbackLaunch& p, int num_sms, cudaStream_t s);
+}  // namespace cl

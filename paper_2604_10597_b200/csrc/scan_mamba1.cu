@@ -691,21 +691,122 @@ int scan_cfg_index(uint64_t pair_tiles, int num_sms, int variant) {
   return kDefaultCfg;  // 12 consumers
 }
 
+// The L-parallel kernel (scan_lookback.cu) or not: its look-back costs a second pass of
+// exponentials over all but the last segment, so it only pays while the chained kernel
+// is parallelism-bound -- few 16-row tiles per SM (C1: 96 tiles, C2: 128, the B=1
+// serving requests).  Returns the lookback table row, or -1 for the chained kernel.
+// CL_LB_CFG=<row> / CL_LB_TILES=<max tiles> override (experiments).
+int lookback_choice(uint64_t pair_tiles, uint64_t L, int num_sms, int variant) {
+  if (variant >= CL_SCAN_LOOKBACK_BASE) return variant - CL_SCAN_LOOKBACK_BASE;
+  if (variant == CL_SCAN_CHAINED || variant == CL_SCAN_ROWSEQ_TMA ||
+      (variant >= CL_SCAN_CONFIG_BASE && variant < CL_SCAN_LOOKBACK_BASE))
+    return -1;
+  static const int forced_cfg = [] {
+    const char* e = getenv("CL_LB_CFG");
+    const int v = e ? atoi(e) : -1;
+    return v >= 0 && v < kLookbackCfgs ? v : -1;
+  }();
+  static const long max_tiles_env = [] {
+    const char* e = getenv("CL_LB_TILES");
+    return e ? atol(e) : -1L;
+  }();
+  const int cfg = forced_cfg >= 0 ? forced_cfg : 0;
+  if (variant == CL_SCAN_LOOKBACK) return cfg;
+  const uint64_t max_tiles = max_tiles_env >= 0 ? static_cast<uint64_t>(max_tiles_env)
+                                                 : 2ull * static_cast<uint64_t>(num_sms);
+  // at least two 32-step boxes per segment at the chosen split
+  if (pair_tiles <= max_tiles && L >= 4u * lookback_box(cfg)) return cfg;
+  return -1;
+}
+
+// Segment count of the L-parallel kernel: as many (tile, segment) items as there are
+// consumer warps (one wave), from the SHAPE only -- so every decided chunk gives the
+// same bits.  CL_LB_SEGS=<n> overrides (experiments).
+void lookback_split(uint64_t L, int n_tiles, int num_sms, int cfg, int* seg_len, int* n_seg) {
+  static const int forced = [] {
+    const char* e = getenv("CL_LB_SEGS");
+    return e ? atoi(e) : 0;
+  }();
+  const int box = lookback_box(cfg);
+  int target = forced > 0 ? forced : (num_sms * lookback_warps(cfg)) / (n_tiles > 0 ? n_tiles : 1);
+  if (target < 1) target = 1;
+  const int max_seg = static_cast<int>((L + box - 1) / box);
+  if (target > max_seg) target = max_seg;
+  int len = static_cast<int>((L + target - 1) / target);
+  len = (len + box - 1) / box * box;
+  *seg_len = len;
+  *n_seg = static_cast<int>((L + len - 1) / len);
+}
+
+struct Selection {
+  bool tma = false;
+  int lb = -1;       // lookback table row, or -1
+  int cfg_idx = -1;  // chained table row (kCfgs), or -1
+  ScanCfg cfg{};
+};
+
+// The kernel a scan call runs (shared by the launch and cl_scan_plan_f32); an error
+// message for an invalid variant.
+const char* select_kernel(const cl_mamba1_args& a, int num_sms, int variant, Selection* out) {
+  const bool tma_ok = tma_eligible(a);
+  const bool forced_tma = variant == CL_SCAN_ROWSEQ_TMA || variant == CL_SCAN_LOOKBACK ||
+                          variant == CL_SCAN_CHAINED || variant >= CL_SCAN_CONFIG_BASE;
+  if ((variant >= CL_SCAN_CONFIG_BASE && variant < CL_SCAN_LOOKBACK_BASE &&
+       variant - CL_SCAN_CONFIG_BASE >= kNumCfgs) ||
+      (variant >= CL_SCAN_LOOKBACK_BASE && variant - CL_SCAN_LOOKBACK_BASE >= kLookbackCfgs) ||
+      (variant > CL_SCAN_CHAINED && variant < CL_SCAN_CONFIG_BASE) || variant < 0)
+    return "scan variant: no such kernel configuration";
+  if (forced_tma && !tma_ok)
+    return "scan variant rowseq_tma needs d_state 16, L % 4 == 0 and 16-byte aligned buffers";
+  out->tma = forced_tma || (variant == CL_SCAN_AUTO && tma_ok);
+  if (!out->tma) return nullptr;
+  const uint64_t pair_tiles = ((a.dim + kRowsP - 1) / kRowsP) * a.batch;
+  out->lb = lookback_choice(pair_tiles, a.seq_len, num_sms, variant);
+  out->cfg_idx = out->lb >= 0 ? -1
+                              : scan_cfg_index(pair_tiles, num_sms,
+                                               variant == CL_SCAN_CHAINED ? CL_SCAN_AUTO : variant);
+  out->cfg = out->lb >= 0 ? ScanCfg{kWarpSpecPair, lookback_box(out->lb), lookback_warps(out->lb), 2}
+                          : kCfgs[out->cfg_idx];
+  return nullptr;
+}
+
 }  // namespace
+
+int scan_plan(cl_ctx* ctx, const cl_mamba1_args& a, int variant, cl_scan_plan* p) {
+  Selection sel;
+  const char* err = select_kernel(a, ctx->num_sms, variant, &sel);
+  if (err) return fail(ctx, CL_E_INVALID, err);
+  *p = cl_scan_plan{};
+  if (!sel.tma) {
+    p->kernel = CL_KERNEL_GENERIC;
+    return CL_OK;
+  }
+  p->box = sel.cfg.box;
+  p->warps = sel.cfg.warps;
+  p->stages = sel.cfg.stages;
+  if (sel.lb >= 0) {
+    p->kernel = CL_KERNEL_LOOKBACK;
+    p->config = sel.lb;
+    const int n_tiles = static_cast<int>(((a.dim + kRowsP - 1) / kRowsP) * a.batch);
+    lookback_split(a.seq_len, n_tiles, ctx->num_sms, sel.lb, &p->seg_len, &p->n_seg);
+  } else {
+    p->kernel = sel.cfg.kind == kRowSeq ? CL_KERNEL_ROWSEQ : CL_KERNEL_CHAINED;
+    p->config = sel.cfg_idx;
+    p->seg_len = -1;  // the decided chunk, rounded up to whole boxes (known on the device)
+    p->n_seg = -1;
+  }
+  return CL_OK;
+}
 
 int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decision,
                 int fixed_chunk, int variant, cudaStream_t s) {
-  const bool tma_ok = tma_eligible(a);
-  if (variant >= CL_SCAN_CONFIG_BASE && variant - CL_SCAN_CONFIG_BASE >= kNumCfgs)
-    return fail(ctx, CL_E_INVALID, "scan variant: no such kernel configuration");
-  if ((variant == CL_SCAN_ROWSEQ_TMA || variant >= CL_SCAN_CONFIG_BASE) && !tma_ok)
-    return fail(ctx, CL_E_INVALID, "scan variant rowseq_tma needs d_state 16, L % 4 == 0 and 16-byte aligned buffers");
-  const bool use_tma = variant == CL_SCAN_ROWSEQ_TMA || variant >= CL_SCAN_CONFIG_BASE ||
-                       (variant == CL_SCAN_AUTO && tma_ok);
-  if (use_tma) {
-    const uint64_t pair_tiles = ((a.dim + kRowsP - 1) / kRowsP) * a.batch;
-    const int cfg_idx = scan_cfg_index(pair_tiles, ctx->num_sms, variant);
-    const ScanCfg cfg = kCfgs[cfg_idx];
+  Selection sel;
+  const char* err = select_kernel(a, ctx->num_sms, variant, &sel);
+  if (err) return fail(ctx, CL_E_INVALID, err);
+  if (sel.tma) {
+    const int lb = sel.lb;
+    const int cfg_idx = sel.cfg_idx;
+    const ScanCfg cfg = sel.cfg;
     const bool ws = cfg.kind != kRowSeq;
     const uint64_t L = a.seq_len, D = a.dim, Bt = a.batch;
     const int rows_per_tile = ws ? kRowsP : kRows;
@@ -722,7 +823,23 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     if (!rc) rc = grow_scratch(ctx, w, &w->d_bct, &w->bct_bytes, bc_bytes, "cudaMalloc(B/C transpose)");
     if (rc) return rc;
     unsigned int epoch = 0;
-    if (ws) {
+    int lb_seg_len = 0, lb_n_seg = 0;
+    if (lb >= 0) {
+      // aggregate words {tag, value}: one tag per launch (every (tile, segment) slot is
+      // written once per launch); zeroed on allocation, on tag wrap, and in-graph before
+      // every launch of a captured graph
+      lookback_split(L, n_tiles, ctx->num_sms, lb, &lb_seg_len, &lb_n_seg);
+      const size_t agg_bytes = size_t(n_tiles) * lb_n_seg * kRowsP * 18 * sizeof(unsigned long long);
+      const bool fresh = w->agg_bytes < agg_bytes;
+      rc = grow_scratch(ctx, w, &w->d_agg, &w->agg_bytes, agg_bytes, "cudaMalloc(scan aggregates)");
+      if (rc) return rc;
+      if (fresh || w->captured || w->agg_epoch == 0 || w->agg_epoch == 0xFFFFFFFFu) {
+        cudaError_t e = cudaMemsetAsync(w->d_agg, 0, w->captured ? agg_bytes : w->agg_bytes, s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(scan aggregates)");
+        w->agg_epoch = 1;
+      }
+      epoch = w->agg_epoch++;
+    } else if (ws) {
       // tagged carry words: zeroed when (re)allocated or when the epoch would wrap; each
       // launch takes tags epoch + 1 .. epoch + (segments <= boxes), above every older tag
       const size_t tcarry_bytes = size_t(n_tiles) * kRowsP * kN * sizeof(unsigned long long);
@@ -788,6 +905,32 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     t.fixed_chunk = fixed_chunk;
     const bool sp = a.delta_softplus != 0, hz = a.z != nullptr;
     const int n = ctx->num_sms;
+    if (lb >= 0) {
+      LookbackLaunch p{};
+      p.A = a.A;
+      p.D = a.D;
+      p.bias = a.delta_bias;
+      p.h0 = a.h0;
+      p.out = a.out;
+      p.h_last = a.h_last;
+      p.agg = w->d_agg;
+      p.epoch = epoch;
+      p.stage_params = t.stage_params;
+      p.ticket = w->d_work;
+      p.batch = Bt;
+      p.dim = D;
+      p.L = L;
+      p.tiles_per_batch = tiles_per_batch;
+      p.n_tiles = n_tiles;
+      p.seg_len = lb_seg_len;
+      p.n_seg = lb_n_seg;
+      p.decision = d_decision;
+      const CUtensorMap lm[4] = {m[0], m[1], m[2], m[4]};
+      e = launch_lookback(lb, sp, hz, lm, p, n, s);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "lookback scan kernel launch");
+      ++ctx->launches;
+      return CL_OK;
+    }
     switch (cfg_idx) {
       case 1: e = dispatch<false, 32, 4, 3>(sp, hz, m, t, n, s); break;
       case 2: e = dispatch<false, 16, 8, 3>(sp, hz, m, t, n, s); break;

@@ -26,7 +26,8 @@ from .chunklab import (CalibrationRef, ChunkBounds, ChunkDecision, EntropyEstima
                        HistogramSpec, SchedulerPolicy, rule_spec)
 
 _VARIANTS = {"auto": _lib.CL_SCAN_AUTO, "rowseq_tma": _lib.CL_SCAN_ROWSEQ_TMA,
-             "generic": _lib.CL_SCAN_GENERIC}
+             "generic": _lib.CL_SCAN_GENERIC, "lookback": _lib.CL_SCAN_LOOKBACK,
+             "chained": _lib.CL_SCAN_CHAINED}
 
 
 def _stream_ptr(device) -> int:
@@ -117,10 +118,28 @@ def selective_scan_fn(u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_
 
 
 def _variant_code(variant: str) -> int:
-    """"auto" / "rowseq_tma" / "generic", or "cfg:<i>" for row i of the TMA kernel table."""
+    """"auto" / "chained" / "lookback" / "rowseq_tma" / "generic", "cfg:<i>" for row i of
+    the chained kernel table, "lb:<i>" for row i of the L-parallel kernel table."""
     if variant.startswith("cfg:"):
         return _lib.CL_SCAN_CONFIG_BASE + int(variant[4:])
+    if variant.startswith("lb:"):
+        return _lib.CL_SCAN_LOOKBACK_BASE + int(variant[3:])
     return _VARIANTS[variant]
+
+
+def scan_plan(u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_softplus=True,
+              variant: str = "auto", h0=None, out=None, return_last_state=False) -> dict:
+    """The kernel selective_scan_fn would run (cl_scan_plan_f32; no launch)."""
+    check_scan_inputs(u, delta, A, B, C, D, z, delta_bias, h0, out)
+    out = torch.empty_like(u) if out is None else out
+    h_last = (torch.empty(u.shape[0], u.shape[1], A.shape[1], device=u.device)
+              if return_last_state else None)
+    a = _mamba_args(u, delta, A, B, C, D, z, delta_bias, h0, out, h_last, delta_softplus)
+    p = _lib.cl_scan_plan()
+    Context.get(u.device.index).call("cl_scan_plan_f32", C_byref(a), _variant_code(variant),
+                                     C_byref(p))
+    return {"kernel": _lib.KERNEL_NAMES[p.kernel], "config": p.config, "box": p.box,
+            "warps": p.warps, "stages": p.stages, "n_seg": p.n_seg, "seg_len": p.seg_len}
 
 
 def selective_state_update(state, x, dt, A, B, C, D=None, z=None, dt_bias=None,

@@ -63,7 +63,10 @@ def test_enum_constants_match_the_header():
     """The Python constants mirror the header's enums (a drift would silently select the
     wrong kernel or policy)."""
     src = open(HEADER).read()
-    for name in ("CL_SCAN_AUTO", "CL_SCAN_ROWSEQ_TMA", "CL_SCAN_GENERIC", "CL_SCAN_CONFIG_BASE"):
+    for name in ("CL_SCAN_AUTO", "CL_SCAN_ROWSEQ_TMA", "CL_SCAN_GENERIC", "CL_SCAN_LOOKBACK",
+                 "CL_SCAN_CHAINED", "CL_SCAN_CONFIG_BASE", "CL_SCAN_LOOKBACK_BASE",
+                 "CL_KERNEL_GENERIC", "CL_KERNEL_CHAINED", "CL_KERNEL_ROWSEQ",
+                 "CL_KERNEL_LOOKBACK"):
         m = re.search(rf"\b{name}\s*=\s*(\d+)", src)
         assert m, name
         assert getattr(_lib, name) == int(m.group(1)), name
@@ -74,5 +77,8 @@ def test_scan_variant_codes():
     assert _variant_code("auto") == _lib.CL_SCAN_AUTO
     assert _variant_code("generic") == _lib.CL_SCAN_GENERIC
     assert _variant_code("cfg:11") == _lib.CL_SCAN_CONFIG_BASE + 11
+    assert _variant_code("lookback") == _lib.CL_SCAN_LOOKBACK
+    assert _variant_code("chained") == _lib.CL_SCAN_CHAINED
+    assert _variant_code("lb:2") == _lib.CL_SCAN_LOOKBACK_BASE + 2
     with pytest.raises(KeyError):
         _variant_code("nope")

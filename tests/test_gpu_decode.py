@@ -2,9 +2,13 @@
 passive-vs-routed equivalence the paper claims (bitwise output equality).
 
 All Mamba-1 paths share one elementwise math and (N = 16) one C.h order, so:
-  * prefill(L) followed by k decode steps == prefill(L + k), bit for bit;
-  * the generic scan == the TMA scan, bit for bit;
-  * any chunk policy (passive Static or routed by entropy) gives the same output bits."""
+  * prefill(L) followed by k decode steps == prefill(L + k), bit for bit, for the chained
+    kernels (the L-parallel kernel, which AUTO picks for few rows, folds segment
+    aggregates into its carry-ins: there the equality holds to rounding,
+    tests/test_gpu_lookback.py);
+  * the generic scan == the chained TMA scan, bit for bit;
+  * any chunk policy (passive Static or routed by entropy) gives the same output bits,
+    for every kernel AUTO can pick (the L-parallel split is tied to the shape)."""
 import numpy as np
 import pytest
 import torch
@@ -28,12 +32,13 @@ def test_prefill_then_decode_equals_longer_prefill(cuda, with_z, with_bias):
     z = d["z"] if with_z else None
     bias = d["delta_bias"] if with_bias else None
     full, h_full = selective_scan_fn(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], z, bias,
-                                     True, return_last_state=True, chunk_size=64)
+                                     True, return_last_state=True, chunk_size=64,
+                                     variant="chained")
     part, h = selective_scan_fn(d["u"][..., :L0].contiguous(), d["delta"][..., :L0].contiguous(),
                                 d["A"], d["B"][..., :L0].contiguous(),
                                 d["C"][..., :L0].contiguous(), d["D"],
                                 None if z is None else z[..., :L0].contiguous(), bias, True,
-                                return_last_state=True, chunk_size=128)
+                                return_last_state=True, chunk_size=128, variant="chained")
     assert torch.equal(part, full[..., :L0])
     state = h.clone()
     for t in range(L0, L0 + k):
@@ -50,7 +55,7 @@ def test_generic_equals_tma(cuda):
     x = mamba_inputs(32, 2, 40, 16, 512)
     d = dev(x, cuda)
     args = (d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"], True)
-    y_t, h_t = selective_scan_fn(*args, return_last_state=True, chunk_size=256)
+    y_t, h_t = selective_scan_fn(*args, return_last_state=True, chunk_size=256, variant="chained")
     y_g, h_g = selective_scan_fn(*args, return_last_state=True, chunk_size=256, variant="generic")
     assert torch.equal(y_t, y_g) and torch.equal(h_t, h_g)
 
