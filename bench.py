@@ -261,6 +261,9 @@ def main():
     ap.add_argument("--no-producer", action="store_true",
                     help="skip the side measurements (conv1d producer fusion, token entropy)")
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--eager", action="store_true",
+                    help="launch every stage from the host each step instead of replaying "
+                         "per-stage CUDA graphs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -290,7 +293,7 @@ def main():
             dist.init_process_group(backend)
 
     import paper_2604_10597_b200 as cl
-    from paper_2604_10597_b200.mamba1 import Prefill
+    from paper_2604_10597_b200.mamba1 import Prefill, scan_plan
 
     batch, dim, L, N, desc = CONFIGS[args.config]
     if args.scaling == "strong" and world > 1:
@@ -322,7 +325,11 @@ def main():
     assert plan.b0 * dim * L == g0 and plan.local_batch == batch
     stages = DeviceStages(pf)
 
-    def step(ev=None):
+    # ev: [start, after min/max, after histogram, after decision, after scan]; the timed
+    # loop records only slots 0, 3 and 4 (fine=False) -- each event record is a few
+    # microseconds of stream time on the few-row shapes -- and a separate untimed pass
+    # records all five for the stage breakdown
+    def step(ev=None, fine=True):
         if ev:
             ev[0].record()
         if world > 1:
@@ -330,22 +337,24 @@ def main():
             # of the counts, identical device decision on every rank
             sharded_entropy_decision(stages, uf, plan, int(spec.sample_stride))
             if ev:
-                ev[1].record()
-                ev[2].record()
+                if fine:
+                    ev[1].record()
+                    ev[2].record()
                 ev[3].record()
         else:
-            pf.stage_minmax(uf, g0)
-            if ev:
+            pf.stage_init()
+            pf.stage_minmax(uf, g0, init=False)
+            if ev and fine:
                 ev[1].record()
             if FUSED_DECIDE:
                 # histogram + decision in one launch (its last CTA decides): stage
                 # "histogram" includes the decision, "decide" is the empty interval
-                pf.stage_histogram_decide(uf, L)
-                if ev:
+                pf.stage_histogram_decide(uf, L, zero=False)
+                if ev and fine:
                     ev[2].record()
             else:
-                pf.stage_histogram(uf, g0)
-                if ev:
+                pf.stage_histogram(uf, g0, zero=False)
+                if ev and fine:
                     ev[2].record()
                 pf.stage_decide(n_total, L)
             if ev:
@@ -359,6 +368,55 @@ def main():
         step()
     torch.cuda.synchronize()
     rec = pf.decision()  # sync point outside the timed region; raises on device errors
+    plan_info = scan_plan(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"],
+                          x["delta_bias"], True, out=out, return_last_state=True)
+
+    # One GPU: each stage is captured once into a CUDA graph and the timed steps replay
+    # them (the production way to launch a fixed-shape layer: no Python / ctypes / tensor-
+    # map encoding per step, which on the few-row shapes takes as long as the device work).
+    # The graphs hold exactly the eager launches -- every kernel runs every step, the
+    # decision is taken on the device every step -- and the per-stage events sit between
+    # the replays, on the same stream.  N>1 keeps eager launches (NCCL between stages).
+    use_graphs = world == 1 and not args.eager
+    if use_graphs:
+        cap = torch.cuda.Stream(device)
+        cap.wait_stream(torch.cuda.current_stream(device))
+        graphs = []
+        captured0 = pf.ctx.launches
+        with torch.cuda.stream(cap):
+            for stage in (lambda: (pf.stage_init(), pf.stage_minmax(uf, g0, init=False)),
+                          lambda: pf.stage_histogram_decide(uf, L, zero=False),
+                          lambda: pf.stage_scan(x["u"], x["delta"], x["A"], x["B"], x["C"],
+                                                x["D"], x["z"], x["delta_bias"], True, out,
+                                                True)):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=cap):
+                    stage()
+                graphs.append(g)
+        torch.cuda.current_stream(device).wait_stream(cap)
+        torch.cuda.synchronize()
+        kernels_per_step = pf.ctx.launches - captured0  # this library's kernel nodes
+
+        def step(ev=None, fine=True):  # noqa: F811  (the graph-replay step)
+            if ev:
+                ev[0].record()
+            graphs[0].replay()
+            if ev and fine:
+                ev[1].record()
+            graphs[1].replay()
+            if ev:
+                if fine:
+                    ev[2].record()
+                ev[3].record()
+            graphs[2].replay()
+            if ev:
+                ev[4].record()
+
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        rec2 = pf.decision()
+        assert rec2.decision.chunk == rec.decision.chunk
 
     # per-stage CUDA events on the launching stream, read after the timed loop
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
@@ -380,20 +438,30 @@ def main():
         for i in range(args.steps):
             if l2_flush:
                 l2buf.zero_()
-            step(evs[i])
+            step(evs[i], fine=False)
         stop.record()
         torch.cuda.synchronize()
         clocks.mark("t_stop")
-    stage_ms = {"minmax": [e[0].elapsed_time(e[1]) for e in evs],
-                "histogram": [e[1].elapsed_time(e[2]) for e in evs],
-                "decide": [e[2].elapsed_time(e[3]) for e in evs],
+    stage_ms = {"entropy": [e[0].elapsed_time(e[3]) for e in evs],
                 "scan": [e[3].elapsed_time(e[4]) for e in evs]}
+    # stage breakdown (untimed pass, all five events per step)
+    bevs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(10)]
+    for bev in bevs:
+        if l2_flush:
+            l2buf.zero_()
+        step(bev, fine=True)
+    torch.cuda.synchronize()
+    breakdown = {"minmax": statistics.median(e[0].elapsed_time(e[1]) for e in bevs),
+                 "histogram_decide": statistics.median(e[1].elapsed_time(e[2]) for e in bevs),
+                 "scan": statistics.median(e[3].elapsed_time(e[4]) for e in bevs)}
     if world > 1:
         dist.barrier()
     elapsed_ms = start.elapsed_time(stop)
     if l2_flush:
         elapsed_ms = sum(e[0].elapsed_time(e[4]) for e in evs)
     launches = pf.ctx.launches - launches0
+    if use_graphs:  # replays enqueue no host-side launches: count the graphs' kernel nodes
+        launches = kernels_per_step * args.steps
     if world > 1:
         t = torch.tensor([elapsed_ms], device=device, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -405,7 +473,7 @@ def main():
     peak, peak_kind = peaks()
     ab = algorithmic_bytes(batch, dim, L, N)
     scan_ms = statistics.mean(stage_ms["scan"])
-    ent_ms = statistics.mean(stage_ms["minmax"]) + statistics.mean(stage_ms["histogram"])
+    ent_ms = statistics.mean(stage_ms["entropy"])
     scan_gbs = ab["scan"] / (scan_ms / 1e3) / 1e9
     step_gbs = ab["total"] / (ms_per_step / 1e3) / 1e9  # per rank
     traffic = None
@@ -434,19 +502,31 @@ def main():
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": ab["scan"]},
         "stage_ms": ({k: statistics.mean(v) for k, v in stage_ms.items()} if world == 1 else
-                     {"entropy_allreduce_decide": statistics.mean(stage_ms["minmax"]),
+                     {"entropy_allreduce_decide": statistics.mean(stage_ms["entropy"]),
                       "scan": statistics.mean(stage_ms["scan"])}),
+        "stage_breakdown_ms": breakdown,
         "entropy_gbs": ab["entropy"] / (ent_ms / 1e3) / 1e9,
         "chunk": rec.decision.chunk, "raw_nats": rec.entropy.raw_nats,
         "gpu_launches": launches,
+        "scan_plan": plan_info,
     }
+    result["config"]["launch"] = ("per-stage CUDA graphs replayed (captured once)" if use_graphs
+                                  else "eager launches")
+    result["roofline"]["kernel"] = plan_info["kernel"]
     result["clocks"] = clocks.summary()
     # SFU roofline of the scan: 18 MUFU per (b, d, l) -- 16 state
     # exponentials, one ex2 in softplus, one in SiLU -- at 16 MUFU/clk/SM x SMs x the
-    # SM clock sampled during the timed region (the scan's binding pipe; HBM is not)
+    # SM clock sampled during the timed region (the scan's binding pipe; HBM is not).
+    # The L-parallel kernel's extra aggregate pass counts as issued work.
     sm_mhz = result["clocks"].get("sm_mhz") or 1965.0
     n_sms = torch.cuda.get_device_properties(device).multi_processor_count
     mufu_per_launch = batch * dim * L * (N + 2)
+    if plan_info["kernel"] == "lookback_ws_kernel":
+        # + the aggregate pass over every segment but the last (16 state exps + the
+        # softplus ex2 per element) + the carry-in folds (16 exps per folded segment)
+        ns, sl = plan_info["n_seg"], plan_info["seg_len"]
+        last = L - (ns - 1) * sl
+        mufu_per_launch += batch * dim * ((L - last) * (N + 1) + N * ns * (ns - 1) // 2)
     sfu_peak = 16 * n_sms * sm_mhz * 1e6 / 1e12
     sfu_ach = mufu_per_launch / (scan_ms / 1e3) / 1e12
     result["roofline"]["sfu"] = {"achieved": sfu_ach, "peak": sfu_peak, "unit": "TMUFU/s",

@@ -167,6 +167,8 @@ int cl_conv1d_f32(cl_ctx* ctx, const float* d_x, const float* d_weight, const fl
  * (global) range in d_range, or the spec's fixed range.  d_counts must be
  * zeroed first (cl_counts_zero) when starting a new histogram. */
 int cl_counts_zero(cl_ctx* ctx, uint64_t* d_counts, int bin_count, void* stream);
+/* cl_range_init + cl_counts_zero as one launch (the first node of a prefill). */
+int cl_prefill_init(cl_ctx* ctx, double* d_range, uint64_t* d_counts, int bin_count, void* stream);
 int cl_histogram_f32(cl_ctx* ctx, const float* d_values, uint64_t n, uint64_t global_offset,
                      const cl_hist_spec* spec, const double* d_range, uint64_t* d_counts,
                      void* stream);

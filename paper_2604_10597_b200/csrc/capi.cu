@@ -343,6 +343,17 @@ int cl_counts_zero(cl_ctx* ctx, uint64_t* d_counts, int bin_count, void* stream)
                       "counts_zero");
 }
 
+int cl_prefill_init(cl_ctx* ctx, double* d_range, uint64_t* d_counts, int bin_count,
+                    void* stream) {
+  if (!ctx || !d_range || !d_counts || bin_count < 1) return fail(ctx, CL_E_INVALID, "null argument");
+  DeviceGuard g(ctx->device);
+  ++ctx->launches;
+  return check_launch(ctx,
+                      launch_prefill_init(d_range, d_counts, bin_count,
+                                          static_cast<cudaStream_t>(stream)),
+                      "prefill_init");
+}
+
 int cl_histogram_f32(cl_ctx* ctx, const float* d_values, uint64_t n, uint64_t global_offset,
                      const cl_hist_spec* spec, const double* d_range, uint64_t* d_counts,
                      void* stream) {
@@ -623,9 +634,8 @@ int cl_prefill_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_hist_spec* 
       return rc;
     return cl_selective_scan_f32(ctx, args, d_decision, 0, CL_SCAN_AUTO, stream);
   }
-  if ((rc = cl_range_init(ctx, d_range, stream))) return rc;
+  if ((rc = cl_prefill_init(ctx, d_range, d_counts, spec->bin_count, stream))) return rc;
   if ((rc = cl_minmax_f32(ctx, args->u, n, 0, spec->sample_stride, d_range, stream))) return rc;
-  if ((rc = cl_counts_zero(ctx, d_counts, spec->bin_count, stream))) return rc;
   if ((rc = cl_histogram_decide_f32(ctx, args->u, n, spec, d_range, d_counts, rule,
                                      args->seq_len, d_decision, stream)))
     return rc;

@@ -19,6 +19,7 @@
 struct cl_workspace {
   unsigned int* d_work = nullptr;  // scan work counters / flags (grown on demand)
   size_t work_bytes = 0;
+  bool ticket_dirty = false;  // the last scan on this stream left d_work non-zero
   float* d_carry = nullptr;  // scan segment carry of the row kernel (grown on demand)
   size_t carry_bytes = 0;
   // tagged segment carry of the warp-specialised scan: 64-bit words {tag, h}; tags are
@@ -111,6 +112,7 @@ int grow_scratch(cl_ctx* ctx, cl_workspace* w, T** ptr, size_t* have, size_t nee
 // ---- kernel launchers (defined in the .cu files) ----
 // entropy.cu
 cudaError_t launch_range_init(double* d_range, cudaStream_t s);
+cudaError_t launch_prefill_init(double* d_range, uint64_t* d_counts, int k, cudaStream_t s);
 cudaError_t launch_minmax_f32(const float* v, uint64_t n, uint64_t g0, uint64_t stride,
                               double* d_range, int num_sms, cudaStream_t s, int* launches);
 cudaError_t launch_minmax_f64(const double* v, uint64_t n, uint64_t g0, uint64_t stride,

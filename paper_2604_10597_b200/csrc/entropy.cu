@@ -251,6 +251,18 @@ __global__ void range_init_kernel(double* range) {
   range[3] = 0.0;
 }
 
+// range_init and zeroed counts in one launch (the prefill's first node)
+__global__ void __launch_bounds__(256) prefill_init_kernel(double* range,
+                                                           unsigned long long* counts, int k) {
+  if (threadIdx.x == 0) {
+    range[0] = -INFINITY;
+    range[1] = -INFINITY;
+    range[2] = 0.0;
+    range[3] = 0.0;
+  }
+  for (int b = threadIdx.x; b < k; b += blockDim.x) counts[b] = 0ull;
+}
+
 // ---------------------------------------------------------------------------
 // Stage 2: histogram, K <= 256.  Each lane owns private counters (no atomics): the
 // per-lane read-modify-write chain is broken into pairs (full chunks) or groups of four
@@ -1689,6 +1701,12 @@ int stride_mode(uint64_t stride) {
 
 cudaError_t launch_range_init(double* d_range, cudaStream_t s) {
   range_init_kernel<<<1, 1, 0, s>>>(d_range);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prefill_init(double* d_range, uint64_t* d_counts, int k, cudaStream_t s) {
+  prefill_init_kernel<<<1, 256, 0, s>>>(d_range, reinterpret_cast<unsigned long long*>(d_counts),
+                                        k);
   return cudaGetLastError();
 }
 

@@ -433,6 +433,18 @@ struct GeoP {
 };
 constexpr int kStagedFlag = 1 << 30;  // meta.y bit: this item's parameters are in shared memory
 
+// Self-resetting work ticket: ticket[0] is the item counter, ticket[1] counts finished
+// claimers; the last of `claimers` warps (after its final claim) zeroes both.
+__device__ __forceinline__ void ticket_retire(unsigned int* ticket, unsigned claimers, int lane) {
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(ticket + 1, 1u) == claimers - 1) {
+      atomicExch(ticket, 0u);
+      atomicExch(ticket + 1, 0u);
+    }
+  }
+}
+
 __device__ __forceinline__ f2_t shfl_xor2(f2_t v, int m) {
   float lo, hi;
   upk(v, lo, hi);

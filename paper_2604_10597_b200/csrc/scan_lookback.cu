@@ -27,6 +27,8 @@
 // Reference contract: chunklab::scan_chunked (scan.hpp:123-136) carries the state across
 // windows; the reference has no parallel prefix.  Parity: <= 1e-5
 // normwise vs the fp64 oracle (tests/test_gpu_lookback.py).
+#include <cstdlib>
+
 #include "scan_common.cuh"
 
 namespace cl {
@@ -46,6 +48,7 @@ struct LbArgs {
   uint64_t batch, dim, L;
   int tiles_per_batch, n_tiles;
   int seg_len, n_seg;
+  int pipe1;  // software-pipelined aggregate pass (A/B switch, CL_LB_PIPE1)
   const cl_decision* decision;
 };
 
@@ -108,6 +111,118 @@ __device__ __forceinline__ void agg_box(const unsigned char* st, int r, int hf, 
   }
 }
 
+// agg_box for a full box, software-pipelined by one 4-timestep group like
+// pair_box_pipe: group j+1's serial prologue (LDS, bias add, softplus, partner exchange)
+// is issued between group j's exponentials and its recurrence.  Same operations on the
+// same values as agg_box.
+template <int BOX, bool SP>
+__device__ __forceinline__ void agg_box_pipe(const unsigned char* st, int r, int hf, float bias,
+                                             const f2_t (&A2p)[kN / 4], f2_t (&h2)[kN / 4],
+                                             float& sdt) {
+  using G = GeoP<BOX>;
+  constexpr int kP = kN / 4;
+  constexpr int kG = BOX / 4;
+  constexpr int kBCRow = 2 * kN * 4;
+  const unsigned char* sB = st + 3 * G::kTileBytes + 32 * hf;
+  const f2_t bias2 = pk(bias, bias);
+  auto prep = [&](int j, float (&dt)[4], float (&xs)[4]) {
+    const int off = Geo<BOX>::swz(r, j);
+    const float4 u4 = *reinterpret_cast<const float4*>(st + off);
+    const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
+    f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
+    if (SP) mine = softplus2(mine);
+    const f2_t other = shfl_xor2(mine, 1);
+    const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
+    const f2_t x01 = mul2(dt01, pk(u4.x, u4.y)), x23 = mul2(dt23, pk(u4.z, u4.w));
+    upk(dt01, dt[0], dt[1]);
+    upk(dt23, dt[2], dt[3]);
+    upk(x01, xs[0], xs[1]);
+    upk(x23, xs[2], xs[3]);
+  };
+  float dt[4], xs[4];
+  prep(0, dt, xs);
+#pragma unroll
+  for (int j = 0; j < kG; ++j) {
+    f2_t dA[4][kP];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const f2_t dd = pk(dt[k], dt[k]);
+#pragma unroll
+      for (int i = 0; i < kP; ++i) {
+        float al, ah;
+        upk(mul2(A2p[i], dd), al, ah);
+        dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+      }
+    }
+    float ndt[4], nxs[4];
+    if (j + 1 < kG) prep(j + 1, ndt, nxs);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const ulonglong2* Bt = reinterpret_cast<const ulonglong2*>(sB + (4 * j + k) * kBCRow);
+      const f2_t xx = pk(xs[k], xs[k]);
+#pragma unroll
+      for (int q = 0; q < kP / 2; ++q) {
+        const ulonglong2 bq = Bt[q];
+        h2[2 * q] = fma2(dA[k][2 * q], h2[2 * q], mul2(bq.x, xx));
+        h2[2 * q + 1] = fma2(dA[k][2 * q + 1], h2[2 * q + 1], mul2(bq.y, xx));
+      }
+      sdt = __fadd_rn(sdt, dt[k]);
+    }
+    if (j + 1 < kG) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        dt[k] = ndt[k];
+        xs[k] = nxs[k];
+      }
+    }
+  }
+}
+
+// Carry-in fold over segments [j0, j1) of one tile: h = exp2(A2 S_j) h + h~_j in segment
+// order.  The aggregate words are loaded kBatch segments at a time (independent loads in
+// flight), then polled only where a tag was not yet current.
+constexpr int kFoldBatch = 4;
+
+template <int NB>
+__device__ __forceinline__ void fold_batch(const unsigned long long* base, int j0, int r, int hf,
+                                           unsigned epoch, const f2_t (&A2p)[kN / 4],
+                                           f2_t (&h)[kN / 4]) {
+  constexpr int kP = kN / 4;
+  unsigned long long w[NB][kN / 2], ws[NB][2];
+  auto load = [&](int b) {
+    const unsigned long long* w64 = base + size_t(j0 + b) * kRowsP * kAggWords;
+#pragma unroll
+    for (int i = 0; i < kN / 2; i += 2) ld_relaxed_u64x2(w64 + 8 * hf + i, w[b][i], w[b][i + 1]);
+    ld_relaxed_u64x2(w64 + 16, ws[b][0], ws[b][1]);
+  };
+  auto ready = [&](int b) {
+    bool ok = (ws[b][0] >> 32) == epoch;
+#pragma unroll
+    for (int i = 0; i < kN / 2; ++i) ok &= (w[b][i] >> 32) == epoch;
+    return ok;
+  };
+#pragma unroll
+  for (int b = 0; b < NB; ++b) load(b);
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    while (!__all_sync(0xffffffffu, ready(b))) {
+      __nanosleep(64);
+      load(b);
+    }
+    const float S = __uint_as_float(static_cast<unsigned>(ws[b][0]));
+    const f2_t SS = pk(S, S);
+#pragma unroll
+    for (int i = 0; i < kP; ++i) {
+      float al, ah;
+      upk(mul2(A2p[i], SS), al, ah);
+      const f2_t P = pk(ex2_approx(al), ex2_approx(ah));
+      const f2_t g = pk(__uint_as_float(static_cast<unsigned>(w[b][2 * i])),
+                        __uint_as_float(static_cast<unsigned>(w[b][2 * i + 1])));
+      h[i] = fma2(P, h[i], g);
+    }
+  }
+}
+
 template <int BOX, int WARPS, int STAGES, bool SP, bool HZ, int NPROD>
 __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     lookback_ws_kernel(const __grid_constant__ CUtensorMap map_u,
@@ -143,7 +258,9 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     it.seg = id / a.n_tiles;
     it.tile = id % a.n_tiles;
     it.t0 = it.seg * seg_len;
-    const int len = min(seg_len, L - it.t0);
+    // segments 0 .. n_seg-2 are seg_len long; the last one (no aggregate pass) takes the
+    // rest, about twice as long, so every item costs about the same
+    const int len = it.seg == n_seg - 1 ? L - it.t0 : seg_len;
     it.nbox = (len + BOX - 1) / BOX;
     return it;
   };
@@ -217,6 +334,9 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
       }
       if (!__any_sync(0xffffffffu, issued)) __nanosleep(CL_PROD_SLEEP_NS);
     }
+    // only producers claim tickets: the last producer warp of the grid to finish returns
+    // the ticket to 0, so the next launch on this stream needs no memset
+    ticket_retire(a.ticket, gridDim.x * NPROD, lane);
     return;
   }
 
@@ -277,7 +397,10 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     }
     const int tbox = cur.t0 + box * BOX;
     if (phase1) {
-      agg_box<BOX, SP>(st, r, hf, min(BOX, L - tbox), bias, A2p, h2, sdt);
+      if (a.pipe1 && tbox + BOX <= L)
+        agg_box_pipe<BOX, SP>(st, r, hf, bias, A2p, h2, sdt);
+      else
+        agg_box<BOX, SP>(st, r, hf, L - tbox, bias, A2p, h2, sdt);
       __syncwarp();
       if (lane == 0) mbar_arrive(wempty + slot);
       if (box == cur.nbox - 1) {
@@ -307,35 +430,12 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
         h[s / 2] = pk(q.x, q.y);
         h[s / 2 + 1] = pk(q.z, q.w);
       }
-      for (int j = 0; j < cur.seg; ++j) {
-        const unsigned long long* w64 =
-            a.agg + ((size_t(cur.tile) * n_seg + j) * kRowsP + r) * kAggWords;
-        unsigned long long w[kN / 2], ws0, ws1;
-        for (;;) {
-          bool ok = true;
-#pragma unroll
-          for (int i = 0; i < kN / 2; i += 2) {
-            ld_relaxed_u64x2(w64 + 8 * hf + i, w[i], w[i + 1]);
-            ok &= (w[i] >> 32) == a.epoch;
-            ok &= (w[i + 1] >> 32) == a.epoch;
-          }
-          ld_relaxed_u64x2(w64 + 16, ws0, ws1);
-          ok &= (ws0 >> 32) == a.epoch;
-          if (__all_sync(0xffffffffu, ok)) break;
-          __nanosleep(64);
-        }
-        const float S = __uint_as_float(static_cast<unsigned>(ws0));
-        const f2_t SS = pk(S, S);
-#pragma unroll
-        for (int i = 0; i < kP; ++i) {
-          float al, ah;
-          upk(mul2(A2p[i], SS), al, ah);
-          const f2_t P = pk(ex2_approx(al), ex2_approx(ah));
-          const f2_t g = pk(__uint_as_float(static_cast<unsigned>(w[2 * i])),
-                            __uint_as_float(static_cast<unsigned>(w[2 * i + 1])));
-          h[i] = fma2(P, h[i], g);
-        }
-      }
+      const unsigned long long* tb =
+          a.agg + (size_t(cur.tile) * n_seg * kRowsP + r) * kAggWords;
+      int j = 0;
+      for (; j + kFoldBatch <= cur.seg; j += kFoldBatch)
+        fold_batch<kFoldBatch>(tb, j, r, hf, a.epoch, A2p, h);
+      for (; j < cur.seg; ++j) fold_batch<1>(tb, j, r, hf, a.epoch, A2p, h);
 #pragma unroll
       for (int i = 0; i < kP; ++i) h2[i] = h[i];
     }
@@ -413,6 +513,11 @@ cudaError_t launch_lookback(int cfg, bool sp, bool hz, const CUtensorMap* maps,
   t.n_tiles = p.n_tiles;
   t.seg_len = p.seg_len;
   t.n_seg = p.n_seg;
+  static const int pipe1 = [] {
+    const char* e = getenv("CL_LB_PIPE1");
+    return e ? atoi(e) : 1;
+  }();
+  t.pipe1 = pipe1;
   t.decision = p.decision;
   const CUtensorMap m[4] = {maps[0], maps[1], maps[2], maps[3]};
   switch (cfg) {

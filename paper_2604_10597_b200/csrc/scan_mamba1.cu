@@ -421,6 +421,9 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
       }
       if (!__any_sync(0xffffffffu, issued)) __nanosleep(CL_PROD_SLEEP_NS);
     }
+    // only producers claim tickets: the last producer warp of the grid to finish returns
+    // the ticket to 0, so the next launch on this stream needs no memset
+    ticket_retire(a.ticket, gridDim.x * NPROD, lane);
     return;
   }
 
@@ -719,23 +722,57 @@ int lookback_choice(uint64_t pair_tiles, uint64_t L, int num_sms, int variant) {
   return -1;
 }
 
-// Segment count of the L-parallel kernel: as many (tile, segment) items as there are
-// consumer warps (one wave), from the SHAPE only -- so every decided chunk gives the
-// same bits.  CL_LB_SEGS=<n> overrides (experiments).
+// Split of the L-parallel kernel, from the SHAPE only (so every decided chunk gives the
+// same bits): n segments of seg_len timesteps (whole boxes; the last one takes the rest),
+// at most one (tile, segment) item per consumer warp of the grid (one wave), the split
+// whose longest item is shortest, then the fewest segments.  Items cost (1 + phi) seg_len
+// with an aggregate pass and `last` without; measured (profiles/r2b_lookback_ab.txt):
+// phi = 0 -- equal segments -- is best, because the last segment waits for its
+// predecessors' aggregate passes anyway (0.61 vs 0.70 ms-equivalents at C1 for phi = 0.6).
+// CL_LB_SEGS=<n> forces n, CL_LB_PHI=<phi> the cost model (experiments).
 void lookback_split(uint64_t L, int n_tiles, int num_sms, int cfg, int* seg_len, int* n_seg) {
   static const int forced = [] {
     const char* e = getenv("CL_LB_SEGS");
     return e ? atoi(e) : 0;
   }();
   const int box = lookback_box(cfg);
-  int target = forced > 0 ? forced : (num_sms * lookback_warps(cfg)) / (n_tiles > 0 ? n_tiles : 1);
-  if (target < 1) target = 1;
-  const int max_seg = static_cast<int>((L + box - 1) / box);
-  if (target > max_seg) target = max_seg;
-  int len = static_cast<int>((L + target - 1) / target);
-  len = (len + box - 1) / box * box;
-  *seg_len = len;
-  *n_seg = static_cast<int>((L + len - 1) / len);
+  const long Ll = static_cast<long>(L);
+  int n_max = (num_sms * lookback_warps(cfg)) / (n_tiles > 0 ? n_tiles : 1);
+  const int max_seg = static_cast<int>((Ll + box - 1) / box);
+  if (n_max > max_seg) n_max = max_seg;
+  if (n_max < 1) n_max = 1;
+  if (forced > 0) {
+    const int n = forced < max_seg ? forced : max_seg;
+    long len = (Ll + n - 1) / n;
+    len = (len + box - 1) / box * box;
+    *seg_len = static_cast<int>(len);
+    *n_seg = static_cast<int>((Ll + len - 1) / len);
+    return;
+  }
+  // cost of an item in units of full-pass timesteps: (1 + phi) seg_len for a segment with
+  // an aggregate pass (phi = its cost relative to the full pass), `last` for the last one
+  static const double phi = [] {
+    const char* e = getenv("CL_LB_PHI");
+    return e ? atof(e) : 0.0;
+  }();
+  double best_cost = static_cast<double>(Ll);
+  long best_len = ((Ll + box - 1) / box) * box;
+  int best_n = 1;  // a single segment: one full pass
+  for (long len = box; len < Ll; len += box) {
+    for (long n = 2; n <= n_max; ++n) {
+      const long last = Ll - (n - 1) * len;
+      if (last <= 0) break;
+      const double reg = (1.0 + phi) * static_cast<double>(len);
+      const double cost = reg > last ? reg : static_cast<double>(last);
+      if (cost < best_cost - 1e-9 || (cost < best_cost + 1e-9 && n < best_n)) {
+        best_cost = cost;
+        best_len = len;
+        best_n = static_cast<int>(n);
+      }
+    }
+  }
+  *seg_len = static_cast<int>(best_len);
+  *n_seg = best_n;
 }
 
 struct Selection {
@@ -817,6 +854,7 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     const size_t bc_bytes = 2 * size_t(Bt) * L * kN * sizeof(float);
     cl_workspace* w = workspace(ctx, s);  // scratch of this stream only
     if (!w) return CL_E_CUDA;
+    const bool fresh_work = w->work_bytes < work_bytes;
     int rc = grow_scratch(ctx, w, &w->d_work, &w->work_bytes, work_bytes, "cudaMalloc(scan work)");
     if (!rc && !ws)
       rc = grow_scratch(ctx, w, &w->d_carry, &w->carry_bytes, carry_bytes, "cudaMalloc(carry)");
@@ -874,8 +912,13 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       ok = make_map(&m[4], d_Bt, kN, L, Bt, kN, box, 0) &&
            make_map(&m[5], d_Ct, kN, L, Bt, kN, box, 0);
     if (!ok) return fail(ctx, CL_E_CUDA, "cuTensorMapEncodeTiled failed");
-    cudaError_t e = cudaMemsetAsync(w->d_work, 0, work_bytes, s);
+    // the warp-specialised kernels return their ticket to 0 themselves (ticket_retire);
+    // the row kernel's per-tile flags are zeroed every launch
+    cudaError_t e = cudaSuccess;
+    if (!ws || fresh_work || w->captured || w->ticket_dirty)
+      e = cudaMemsetAsync(w->d_work, 0, work_bytes, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(scan work)");
+    w->ticket_dirty = !ws;  // the row kernel leaves its ticket and flags behind
     const dim3 tgrid(static_cast<unsigned>((L + 31) / 32), static_cast<unsigned>(Bt), 2);
     transpose_bc_kernel<<<tgrid, 256, 0, s>>>(a.B, a.C, d_Bt, d_Ct, static_cast<int>(L),
                                               ws ? 2 * kN : kN);

@@ -265,6 +265,11 @@ class Prefill:
         self.token_buf = torch.zeros(4, dtype=torch.float64, device=self.device)
 
     # -- stages (exposed for the sharded path and for per-stage timing) --
+    def stage_init(self):
+        """range_init + counts zero in one launch (cl_prefill_init)."""
+        self.ctx.call("cl_prefill_init", self.range.data_ptr(), self.counts.data_ptr(),
+                      int(self.spec.bin_count), _stream_ptr(self.device))
+
     def stage_minmax(self, u_flat: torch.Tensor, global_offset: int = 0, init: bool = True):
         s = _stream_ptr(self.device)
         if init:
@@ -333,8 +338,9 @@ class Prefill:
             self.stage_decide_token(u.shape[-1])
         else:
             uf = u.reshape(-1)
-            self.stage_minmax(uf)
-            self.stage_histogram_decide(uf, u.shape[-1])
+            self.stage_init()
+            self.stage_minmax(uf, init=False)
+            self.stage_histogram_decide(uf, u.shape[-1], zero=False)
         res = self.stage_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, out,
                               return_last_state, h0)
         if return_last_state:
