@@ -24,6 +24,43 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// ---- exponentials of the elementwise terms (softplus, SiLU) ----
+// ex2.approx (MUFU) by default.  CL_ELEM_MUFU=0 moves the two elementwise exponentials
+// per element to the FMA pipe: 2^x = p(f) * 2^n, n = rint(x) by the 1.5 * 2^23 magic add,
+// f = x - n exactly, p a degree-5 minimax polynomial for 2^f on [-1/2, 1/2] (max rel err
+// 1.5e-7; ex2.approx's is 2.4e-7), 2^n added into the exponent field, x clamped below at
+// -125, NaN kept.  It takes the scan from 18 to 16 MUFU per element, and is SLOWER:
+// C3 scan 1.414 vs 1.351 ms (profiles/r2d_elem_exp_ab.txt) -- the longer dependent chain
+// sits in every group's prologue, and the FMA pipe is already half busy.
+#ifndef CL_ELEM_MUFU
+#define CL_ELEM_MUFU 1
+#endif
+constexpr float kE2c0 = 1.0000001192092896f, kE2c1 = 0.6931469440460205f,
+                kE2c2 = 0.24022120237350464f, kE2c3 = 0.05550713092088699f,
+                kE2c4 = 0.009675540961325169f, kE2c5 = 0.001327647129073739f;
+
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float y;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(y) : "f"(a), "f"(b));
+  return y;
+}
+
+__device__ __forceinline__ float exp2_elem(float x) {
+#if CL_ELEM_MUFU
+  return ex2_approx(x);
+#else
+  x = max_nan(x, -125.f);
+  const float t = __fadd_rn(x, 12582912.f);
+  const float f = __fadd_rn(x, -__fadd_rn(t, -12582912.f));
+  float p = fmaf(kE2c5, f, kE2c4);
+  p = fmaf(p, f, kE2c3);
+  p = fmaf(p, f, kE2c2);
+  p = fmaf(p, f, kE2c1);
+  p = fmaf(p, f, kE2c0);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+#endif
+}
+
 // ---- canonical elementwise math ----
 // Every Mamba-1 path (generic scan, TMA scans, decode) evaluates softplus, SiLU and, for
 // N = 16, C.h with exactly these operation sequences, so the paths agree bit for bit
@@ -32,10 +69,10 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // FFMA2 versions further down (softplus2 / silu2 / the lane-pair C.h) are these
 // functions applied per lane of a register pair.
 
-// softplus(x) = max(x,0) + log1p(exp(-|x|)): one MUFU.EX2 and a degree-9 minimax
-// polynomial for log1p on [0,1] (max rel err 2e-7; equals x to fp32 above 20).
+// softplus(x) = max(x,0) + log1p(exp(-|x|)): one exponential (exp2_elem) and a degree-9
+// minimax polynomial for log1p on [0,1] (max rel err 2e-7; equals x to fp32 above 20).
 __device__ __forceinline__ float softplus_canon(float a) {
-  const float e = ex2_approx(-fabsf(a) * kLog2e);
+  const float e = exp2_elem(-fabsf(a) * kLog2e);
   float q = 0.005253826278033571f;
   q = fmaf(q, e, -0.02959069552080005f);
   q = fmaf(q, e, 0.07836660226277938f);
@@ -48,9 +85,10 @@ __device__ __forceinline__ float softplus_canon(float a) {
   return fmaf(q, e, fmaxf(a, 0.f));
 }
 
-// z * sigmoid(z): one MUFU.EX2, reciprocal by 3 Newton steps from the bit-trick seed.
+// z * sigmoid(z): one exponential (exp2_elem), reciprocal by 3 Newton steps from the
+// bit-trick seed.
 __device__ __forceinline__ float silu_canon(float z) {
-  const float e = ex2_approx(fmaxf(z, -80.f) * -kLog2e);
+  const float e = exp2_elem(fmaxf(z, -80.f) * -kLog2e);
   const float d = e + 1.f;
   float r = __int_as_float(0x7EF311C7 - __float_as_int(d));
   const float nd = d * -1.f;
@@ -338,10 +376,35 @@ __device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
 // softplus for a pair, branch-free: max(x,0) + log1p(exp(-|x|)), log1p by a degree-9
 // minimax polynomial on [0,1] (max rel err 2e-7 in fp32).  Equals x to fp32 precision
 // above 20, matching mamba_ssm's threshold.
+// exp2_elem on both lanes of a pair (FFMA2 / FADD2: each lane rounds exactly like the
+// scalar sequence, so the pair and scalar paths agree bit for bit)
+__device__ __forceinline__ f2_t exp2_elem2(float xa, float xb) {
+#if CL_ELEM_MUFU
+  return pk(ex2_approx(xa), ex2_approx(xb));
+#else
+  const f2_t x = pk(max_nan(xa, -125.f), max_nan(xb, -125.f));
+  const f2_t t = add2(x, pk(12582912.f, 12582912.f));
+  const f2_t n = add2(t, pk(-12582912.f, -12582912.f));
+  float nl, nh;
+  upk(n, nl, nh);
+  const f2_t f = add2(x, pk(-nl, -nh));
+  f2_t p = fma2(pk(kE2c5, kE2c5), f, pk(kE2c4, kE2c4));
+  p = fma2(p, f, pk(kE2c3, kE2c3));
+  p = fma2(p, f, pk(kE2c2, kE2c2));
+  p = fma2(p, f, pk(kE2c1, kE2c1));
+  p = fma2(p, f, pk(kE2c0, kE2c0));
+  float pl, ph, tl, th;
+  upk(p, pl, ph);
+  upk(t, tl, th);
+  return pk(__int_as_float(__float_as_int(pl) + (__float_as_int(tl) << 23)),
+            __int_as_float(__float_as_int(ph) + (__float_as_int(th) << 23)));
+#endif
+}
+
 __device__ __forceinline__ f2_t softplus2(f2_t x) {
   float a, b;
   upk(x, a, b);
-  const f2_t e = pk(ex2_approx(-fabsf(a) * kLog2e), ex2_approx(-fabsf(b) * kLog2e));
+  const f2_t e = exp2_elem2(-fabsf(a) * kLog2e, -fabsf(b) * kLog2e);
   f2_t q = pk(0.005253826278033571f, 0.005253826278033571f);
   q = fma2(q, e, pk(-0.02959069552080005f, -0.02959069552080005f));
   q = fma2(q, e, pk(0.07836660226277938f, 0.07836660226277938f));
@@ -359,8 +422,7 @@ __device__ __forceinline__ f2_t softplus2(f2_t x) {
 __device__ __forceinline__ f2_t silu2(f2_t z) {
   float a, b;
   upk(z, a, b);
-  const f2_t e =
-      pk(ex2_approx(fmaxf(a, -80.f) * -kLog2e), ex2_approx(fmaxf(b, -80.f) * -kLog2e));
+  const f2_t e = exp2_elem2(fmaxf(a, -80.f) * -kLog2e, fmaxf(b, -80.f) * -kLog2e);
   const f2_t d = add2(e, pk(1.f, 1.f));
   float dl, dh;
   upk(d, dl, dh);
@@ -704,7 +766,7 @@ struct LookbackLaunch {
   int tiles_per_batch, n_tiles, seg_len, n_seg;
   const cl_decision* decision;
 };
-constexpr int kLookbackCfgs = 5;
+constexpr int kLookbackCfgs = 6;
 int lookback_warps(int cfg);
 int lookback_box(int cfg);
 cudaError_t launch_lookback(int cfg, bool sp, bool hz, const CUtensorMap* maps,

@@ -486,12 +486,13 @@ cudaError_t dispatch_lb(bool sp, bool hz, const CUtensorMap (&m)[4], const LbArg
 
 // Consumer warps per SM of each lookback kernel-table row (the launcher sizes segments
 // from it).  Rows: 0 {32-step boxes, 8 consumers, 2 stages}, 1 {32, 4, 3}, 2 {32, 6, 3},
-// 3 {16, 12, 2}, 4 {16, 16, 2}.
+// 3 {16, 12, 2}, 4 {16, 16, 2}, 5 {32, 10, 2} (10 x 2 x 11.1 KB stages: 229 KB of shared
+// memory, 12 warps x 168 registers: the SM's whole register file).
 int lookback_warps(int cfg) {
-  static const int kW[] = {8, 4, 6, 12, 16};
+  static const int kW[] = {8, 4, 6, 12, 16, 10};
   return kW[cfg < 0 || cfg >= kLookbackCfgs ? 0 : cfg];
 }
-int lookback_box(int cfg) { return cfg >= 3 ? 16 : 32; }
+int lookback_box(int cfg) { return cfg == 3 || cfg == 4 ? 16 : 32; }
 
 cudaError_t launch_lookback(int cfg, bool sp, bool hz, const CUtensorMap* maps,
                             const LookbackLaunch& p, int num_sms, cudaStream_t s) {
@@ -525,6 +526,7 @@ cudaError_t launch_lookback(int cfg, bool sp, bool hz, const CUtensorMap* maps,
     case 2: return dispatch_lb<32, 6, 3>(sp, hz, m, t, num_sms, s);
     case 3: return dispatch_lb<16, 12, 2>(sp, hz, m, t, num_sms, s);
     case 4: return dispatch_lb<16, 16, 2>(sp, hz, m, t, num_sms, s);
+    case 5: return dispatch_lb<32, 10, 2>(sp, hz, m, t, num_sms, s);
     default: return dispatch_lb<32, 8, 2>(sp, hz, m, t, num_sms, s);
   }
 }
