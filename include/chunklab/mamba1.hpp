@@ -97,8 +97,10 @@ class Prefill {
   }
 
   const cl_decision* device_decision() const { return d_decision_; }
+  const std::uint64_t* device_counts() const { return d_counts_; }
+  const double* device_range() const { return d_range_; }
 
- private:
+ protected:
   static void check_cuda(cudaError_t e) {
     if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
   }
@@ -138,6 +140,60 @@ class Prefill {
   double* d_range_ = nullptr;
   cl_decision* d_decision_ = nullptr;
   cudaStream_t stream_ = nullptr;
+};
+
+// One rank of a row-sharded prefill (one process -- or thread -- per GPU):
+// the rank owns `shard` of the global (batch, d_inner, L) tensors and `args` describe its
+// local tensors.  run() is cl_prefill_sharded_f32: the two allreduces (range MAX, counts
+// SUM) go through `coll` -- ShardedPrefill::nccl(comm) for NCCL over NVLink -- and every
+// rank ends with the identical decision (decision() as for Prefill) and its rows' scan.
+class ShardedPrefill : public Prefill {
+ public:
+  ShardedPrefill(const HistogramSpec& spec, const SchedulerPolicy* policy,
+                 const ChunkBounds& bounds, const CalibrationRef& cal, const cl_shard& shard,
+                 const cl_collectives& coll)
+      : Prefill(spec, policy, bounds, cal), shard_(shard), coll_(coll) {}
+
+  void run(const Mamba1Args& local_args, cudaStream_t stream = nullptr) {
+    b200::check(cl_prefill_sharded_f32(b200::Runtime::get().ctx(), &local_args, &shard_, &spec_,
+                                       &rule_, &coll_, d_counts_, d_range_, d_decision_, stream));
+    stream_ = stream;
+  }
+
+  // Hooks over an NCCL communicator (ncclComm_t; NCCL 2.27 in this image).
+  static cl_collectives nccl(void* nccl_comm) {
+    cl_collectives c{};
+    b200::check(cl_collectives_nccl(nccl_comm, &c));
+    return c;
+  }
+
+  // The shard of `rank` in a world of `world` ranks: whole batches when world divides the
+  // batch (C3, C4), else a contiguous d_inner range of every batch (C1, C2).
+  static cl_shard plan(std::uint64_t batch, std::uint64_t dim, int rank, int world) {
+    cl_shard s{};
+    s.global_batch = batch;
+    s.global_dim = dim;
+    if (world < 1 || rank < 0 || rank >= world) throw invalid_input("bad rank/world");
+    const auto w = static_cast<std::uint64_t>(world), r = static_cast<std::uint64_t>(rank);
+    if (batch % w == 0) {
+      s.b0 = r * (batch / w);
+      s.b1 = s.b0 + batch / w;
+      s.d0 = 0;
+      s.d1 = dim;
+    } else if (dim % w == 0) {
+      s.b0 = 0;
+      s.b1 = batch;
+      s.d0 = r * (dim / w);
+      s.d1 = s.d0 + dim / w;
+    } else {
+      throw invalid_input("neither batch nor d_inner divisible by world size");
+    }
+    return s;
+  }
+
+ private:
+  cl_shard shard_;
+  cl_collectives coll_;
 };
 
 }  // namespace chunklab

@@ -255,6 +255,43 @@ int cl_prefill_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_hist_spec* 
                    const cl_rule_spec* rule, uint64_t* d_counts, double* d_range,
                    cl_decision* d_decision, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU: one rank's share of a row-sharded layer call      */
+/* ------------------------------------------------------------------------ */
+/* The rank owns batches [b0, b1) x channels [d0, d1) of the global (global_batch,
+ * global_dim, L) tensors: whole batches (d0 = 0, d1 = global_dim; C3/C4 plans) or a
+ * channel range of every batch (b0 = 0, b1 = global_batch; C1/C2 plans, B and C
+ * replicated).  args describe the LOCAL tensors ((b1-b0), (d1-d0), L). */
+typedef struct {
+  uint64_t global_batch, global_dim;
+  uint64_t b0, b1, d0, d1;
+} cl_shard;
+
+/* Stream-ordered in-place allreduce hooks (device buffers, enqueued on `stream`; return
+ * CL_OK or a CL_E_* code).  cl_collectives_nccl binds them to ncclAllReduce; any other
+ * transport (MPI, a host-staged test harness) fills them itself. */
+typedef struct {
+  int (*allreduce_max_f64)(double* d_buf, size_t count, void* stream, void* user);
+  int (*allreduce_sum_u64)(uint64_t* d_buf, size_t count, void* stream, void* user);
+  int (*allreduce_sum_u32)(uint32_t* d_buf, size_t count, void* stream, void* user);
+  void* user;
+} cl_collectives;
+
+/* Hooks calling ncclAllReduce on the communicator (an ncclComm_t passed as void*);
+ * libnccl.so.2 is loaded on first use. */
+int cl_collectives_nccl(void* nccl_comm, cl_collectives* out);
+
+/* One rank's prefill: prefill_init -> min/max of every local run (stride sampling by
+ * GLOBAL flat index) -> allreduce MAX(d_range, 4) -> histogram -> allreduce SUM(d_counts,
+ * K) -> device decision (identical on every rank) -> scan of the local rows.
+ * TokenHistogram policies: MAX over the [2L+1] per-position range, SUM over the [L][K]
+ * uint32 counts (stream workspace), then the token decision.  Counts, range and the
+ * decision equal the single-GPU call's bit for bit. */
+int cl_prefill_sharded_f32(cl_ctx* ctx, const cl_mamba1_args* local_args, const cl_shard* shard,
+                           const cl_hist_spec* spec, const cl_rule_spec* rule,
+                           const cl_collectives* coll, uint64_t* d_counts, double* d_range,
+                           cl_decision* d_decision, void* stream);
+
 /* Sync point: copy the decision to the host and convert a device error into
  * CL_E_DEVICE with the reference's message. */
 int cl_decision_check(cl_ctx* ctx, const cl_decision* d_decision, cl_decision* h_out,

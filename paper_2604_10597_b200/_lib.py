@@ -85,6 +85,21 @@ class cl_scan_plan(C.Structure):
                 ("stages", C.c_int), ("n_seg", C.c_int), ("seg_len", C.c_int)]
 
 
+class cl_shard(C.Structure):
+    _fields_ = [("global_batch", C.c_uint64), ("global_dim", C.c_uint64), ("b0", C.c_uint64),
+                ("b1", C.c_uint64), ("d0", C.c_uint64), ("d1", C.c_uint64)]
+
+
+_MAXF64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_SUMU64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_SUMU32 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
+class cl_collectives(C.Structure):
+    _fields_ = [("allreduce_max_f64", _MAXF64), ("allreduce_sum_u64", _SUMU64),
+                ("allreduce_sum_u32", _SUMU32), ("user", C.c_void_p)]
+
+
 class cl_scan_params_f64(C.Structure):
     _fields_ = [("channels", C.c_uint64), ("state_dim", C.c_uint64), ("seq_len", C.c_uint64),
                 ("a", C.c_void_p), ("b", C.c_void_p), ("c", C.c_void_p), ("d", C.c_void_p),
@@ -133,6 +148,10 @@ SIGNATURES = {
     "cl_prefill_f32": (C.c_int, [_P, C.POINTER(cl_mamba1_args), C.POINTER(cl_hist_spec),
                                  C.POINTER(cl_rule_spec), _P, _P, _P, _P]),
     "cl_decision_check": (C.c_int, [_P, _P, C.POINTER(cl_decision), _P]),
+    "cl_collectives_nccl": (C.c_int, [_P, C.POINTER(cl_collectives)]),
+    "cl_prefill_sharded_f32": (C.c_int, [_P, C.POINTER(cl_mamba1_args), C.POINTER(cl_shard),
+                                         C.POINTER(cl_hist_spec), C.POINTER(cl_rule_spec),
+                                         C.POINTER(cl_collectives), _P, _P, _P, _P]),
     "cl_scan_f64": (C.c_int, [_P, C.POINTER(cl_scan_params_f64), _P, _u64, _P, _P, _P]),
     "cl_all_finite_host": (C.c_int, [_P, _P, _u64, C.POINTER(C.c_int)]),
     "cl_compute_histogram_host": (C.c_int, [_P, _P, _u64, C.POINTER(cl_hist_spec), _P, _P,

@@ -68,7 +68,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
             subprocess.run(cmd, check=True)
     if force or _newer(LIB, objs):
         cmd = [nv, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread", "-ldl",
-               "-lrt"]
+               "-lrt"]  # NCCL is dlopen'ed by cl_collectives_nccl (no link dependency)
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -13,14 +13,15 @@ CUDA_LIB = "/usr/local/cuda/lib64"
 
 
 THREADS_SRC = os.path.join(ROOT, "tests", "cpp", "test_threads.cpp")
+SHARDED_SRC = os.path.join(ROOT, "tests", "cpp", "test_sharded.cpp")
 
 
-def build(out, src=SRC):
+def build(out, src=SRC, extra=()):
     from paper_2604_10597_b200 import build as b
     b.build()
     cmd = ["g++", "-std=c++20", "-O2", "-pthread", "-I" + os.path.join(ROOT, "include"),
            "-I" + CUDA_INC, src, "-L" + PKG, "-lchunklab_b200", "-Wl,-rpath," + PKG,
-           "-L" + CUDA_LIB, "-lcudart", "-Wl,-rpath," + CUDA_LIB, "-o", out]
+           "-L" + CUDA_LIB, "-lcudart", "-Wl,-rpath," + CUDA_LIB, *extra, "-o", out]
     subprocess.run(cmd, check=True)
     return out
 
@@ -53,3 +54,20 @@ def test_dropin_threads_and_streams(tmp_path, cuda):
     print(r.stdout[-3000:])
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "threads ok" in r.stdout
+
+
+def test_sharded_program_compiles(tmp_path):
+    assert os.path.exists(build(str(tmp_path / "test_sharded"), SHARDED_SRC, ["-lnccl"]))
+
+
+@pytest.mark.gpu
+def test_sharded_prefill_cpp_world2_and_nccl(tmp_path, cuda):
+    """The C/C++ multi-GPU entry point (cl_prefill_sharded_f32 / chunklab::ShardedPrefill):
+    device stages on every rank, host-staged allreduces between rank threads (world 2 and
+    4; batch and d_inner splits; rule, guarded stride 8, token policies): range, counts and
+    decision bit-identical to the single-GPU call; then world 1 over real NCCL."""
+    exe = build(str(tmp_path / "test_sharded"), SHARDED_SRC, ["-lnccl"])
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "sharded ok" in r.stdout
