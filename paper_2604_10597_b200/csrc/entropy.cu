@@ -21,6 +21,10 @@
 #include <type_traits>
 
 #include "cl_internal.h"
+
+#ifndef CL_DEVICE_CHECKS
+#define CL_DEVICE_CHECKS 0
+#endif
 #include "range.cuh"
 
 namespace cl {
@@ -1078,7 +1082,16 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1)
     __shared__ bool last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(ticket, 1ull) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+      const unsigned long long old = atomicAdd(ticket, 1ull);
+#if CL_DEVICE_CHECKS
+      if (old >= gridDim.x) {  // a dirty ticket: the decision would never be written
+        printf("CL_DCHECK failed: histogram arrival ticket %llu >= grid %u\n", old, gridDim.x);
+        __trap();
+      }
+#endif
+      last = old == gridDim.x - 1;
+    }
     __syncthreads();
     if (last) {
       __threadfence();

@@ -8,10 +8,25 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
 #include "cl_internal.h"
+
+// Device-side invariant checks (A/B builds with -DCL_DEVICE_CHECKS=1; compute-sanitizer is
+// closed on this pool): a failed check prints and traps.
+#ifndef CL_DEVICE_CHECKS
+#define CL_DEVICE_CHECKS 0
+#endif
+#define CL_DCHECK(cond)                                                                 \
+  do {                                                                                  \
+    if (CL_DEVICE_CHECKS && !(cond)) {                                                  \
+      printf("CL_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__,   \
+             #cond, blockIdx.x, threadIdx.x);                                           \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
 
 namespace cl {
 namespace {
@@ -496,11 +511,16 @@ struct GeoP {
 constexpr int kStagedFlag = 1 << 30;  // meta.y bit: this item's parameters are in shared memory
 
 // Self-resetting work ticket: ticket[0] is the item counter, ticket[1] counts finished
-// claimers; the last of `claimers` warps (after its final claim) zeroes both.
-__device__ __forceinline__ void ticket_retire(unsigned int* ticket, unsigned claimers, int lane) {
+// claimers; the last of `claimers` warps (after its final claim) zeroes both.  Every
+// claiming lane ends with exactly one claim past the last item, so a ticket that started
+// at 0 ends at n_items + claiming lanes (checked in CL_DEVICE_CHECKS builds: a dirty
+// ticket would have skipped items and left consumers waiting for carries).
+__device__ __forceinline__ void ticket_retire(unsigned int* ticket, unsigned claimers, int lane,
+                                              unsigned expect_final) {
   if (lane == 0) {
     __threadfence();
     if (atomicAdd(ticket + 1, 1u) == claimers - 1) {
+      CL_DCHECK(atomicAdd(ticket, 0u) == expect_final);
       atomicExch(ticket, 0u);
       atomicExch(ticket + 1, 0u);
     }
@@ -591,6 +611,7 @@ __device__ __forceinline__ void pair_box(const unsigned char* st, float* ydst, i
     if (ydst) {
       float y0, y1;
       upk(yo, y0, y1);
+      CL_DCHECK(4 * j + 2 * hf + 1 < valid);
       __stcs(reinterpret_cast<float2*>(ydst + 4 * j + 2 * hf), make_float2(y0, y1));
     }
   }

@@ -196,6 +196,7 @@ __device__ __forceinline__ void fold_batch(const unsigned long long* base, int j
     ld_relaxed_u64x2(w64 + 16, ws[b][0], ws[b][1]);
   };
   auto ready = [&](int b) {
+    CL_DCHECK((ws[b][0] >> 32) <= epoch);
     bool ok = (ws[b][0] >> 32) == epoch;
 #pragma unroll
     for (int i = 0; i < kN / 2; ++i) ok &= (w[b][i] >> 32) == epoch;
@@ -336,7 +337,8 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     }
     // only producers claim tickets: the last producer warp of the grid to finish returns
     // the ticket to 0, so the next launch on this stream needs no memset
-    ticket_retire(a.ticket, gridDim.x * NPROD, lane);
+    ticket_retire(a.ticket, gridDim.x * NPROD, lane,
+                  static_cast<unsigned>(n_items) + gridDim.x * static_cast<unsigned>(WARPS));
     return;
   }
 
@@ -360,6 +362,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     if (m.x < 0) break;
     const int box = m.y & ~(kStagedFlag | kPhase1Flag);
     const bool phase1 = (m.y & kPhase1Flag) != 0;
+    CL_DCHECK(m.x < n_items && box < decode(m.x).nbox);
     const unsigned char* st = wbase + slot * G::kStageBytes;
     if (box == 0 && (phase1 || m.x / a.n_tiles == n_seg - 1)) {
       // the item's first box: its parameters

@@ -423,7 +423,8 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     }
     // only producers claim tickets: the last producer warp of the grid to finish returns
     // the ticket to 0, so the next launch on this stream needs no memset
-    ticket_retire(a.ticket, gridDim.x * NPROD, lane);
+    ticket_retire(a.ticket, gridDim.x * NPROD, lane,
+                  static_cast<unsigned>(n_items) + gridDim.x * static_cast<unsigned>(WARPS));
     return;
   }
 
@@ -445,6 +446,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     const int2 m = wmeta[slot];
     if (m.x < 0) break;
     const int box = m.y & ~kStagedFlag;
+    CL_DCHECK(m.x < n_items);
     if (box == 0) {
       cur = decode(m.x);
       const int b = cur.tile / a.tiles_per_batch;
@@ -500,6 +502,8 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
             ld_relaxed_u64x2(w64 + i, w[i], w[i + 1]);
             ok &= static_cast<unsigned>(w[i] >> 32) == want;
             ok &= static_cast<unsigned>(w[i + 1] >> 32) == want;
+            // tags only grow: a newer tag than this launch's would be a stale-epoch bug
+            CL_DCHECK(static_cast<unsigned>(w[i] >> 32) <= want);
           }
           if (__all_sync(0xffffffffu, ok)) break;
           __nanosleep(64);
