@@ -623,7 +623,46 @@ def producer_fusion_measure(torch, device, x, pf, reps=20):
     res["saved_ms"] = res["unfused_ms"] - res["fused_ms"]
     res["fused_gbs"] = fused_bytes / (res["fused_ms"] / 1e3) / 1e9
     res["workload"] = f"conv width 4 + SiLU over ({batch}, {dim}, {L}) fp32, stride 1"
-    del xin, u
+
+    # the whole layer: conv -> entropy -> decision -> scan, fused (cl_prefill_from_conv_f32)
+    # vs the conv followed by the unfused prefill on its u, for the calibrated rule
+    # (Dynamic range: min/max in the conv epilogue) and a Fixed range (the whole histogram
+    # in the conv epilogue: u is never re-read for the entropy)
+    import paper_2604_10597_b200 as cl
+    from paper_2604_10597_b200.mamba1 import Prefill
+    out = torch.empty_like(xin)
+    layer = {}
+    for tag, spec in (("dynamic", cl.HistogramSpec()),
+                      ("fixed", cl.HistogramSpec(range_mode=cl.RangeMode.Fixed, fixed_lo=-0.5,
+                                                 fixed_hi=4.0))):
+        lp = Prefill(spec, None, cl.ChunkBounds(32, 512), device=device)
+
+        def fused_layer():
+            lp.from_conv(xin, w, b, x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"],
+                         x["delta_bias"], True, out=out, u=u)
+
+        def unfused_layer():
+            causal_conv1d_fn(xin, w, b, "silu", out=u)
+            lp(u, x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"], x["delta_bias"], True,
+               out=out)
+
+        for name, fn in (("fused_ms", fused_layer), ("unfused_ms", unfused_layer)):
+            fn()
+            torch.cuda.synchronize()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(reps // 2)]
+            for a, e in evs:
+                a.record()
+                fn()
+                e.record()
+            torch.cuda.synchronize()
+            layer.setdefault(tag, {})[name] = statistics.median(a.elapsed_time(e) for a, e in evs)
+        layer[tag]["saved_ms"] = layer[tag]["unfused_ms"] - layer[tag]["fused_ms"]
+    layer["workload"] = ("conv1d(width 4) + SiLU -> K=256 entropy -> calibrated rule -> fused "
+                         "scan, cl_prefill_from_conv_f32 vs causal_conv1d + cl_prefill_f32; "
+                         "fixed range [-0.5, 4]")
+    res["layer"] = layer
+    del xin, u, out
     return res
 
 

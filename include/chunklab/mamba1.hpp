@@ -79,6 +79,16 @@ class Prefill {
     stream_ = stream;
   }
 
+  // The prefill with its producer fused (cl_prefill_from_conv_f32): args.u is the buffer
+  // the conv writes u = act(conv1d(conv.x)) into; the min/max (Dynamic range) or the whole
+  // histogram (Fixed range) runs in the conv's epilogue.  Same bits as causal_conv1d + run.
+  void run_from_conv(const cl_conv_args& conv, const Mamba1Args& args,
+                     cudaStream_t stream = nullptr) {
+    b200::check(cl_prefill_from_conv_f32(b200::Runtime::get().ctx(), &conv, &args, &spec_,
+                                         &rule_, d_counts_, d_range_, d_decision_, stream));
+    stream_ = stream;
+  }
+
   ChunkDecision decision(EntropyEstimate* entropy = nullptr) const {
     cl_decision d{};
     b200::check(cl_decision_check(b200::Runtime::get().ctx(), d_decision_, &d, stream_));

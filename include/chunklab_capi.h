@@ -292,6 +292,28 @@ int cl_prefill_sharded_f32(cl_ctx* ctx, const cl_mamba1_args* local_args, const 
                            const cl_collectives* coll, uint64_t* d_counts, double* d_range,
                            cl_decision* d_decision, void* stream);
 
+/* The prefill with its producer fused ("deeper
+ * kernel fusion of the entropy estimator"): u = act(causal_conv1d(x)) is produced into
+ * args->u (a caller buffer, (batch, dim, L)) and the entropy estimate rides on it:
+ *   Dynamic range: conv with the min/max epilogue -> histogram + decision -> scan
+ *                  (u is read once for the histogram instead of twice);
+ *   Fixed range:   conv with the HISTOGRAM epilogue (bin edges are known before u exists)
+ *                  -> decision -> scan (u is never re-read for the entropy);
+ *   TokenHistogram policies: conv -> token entropy -> decision -> scan.
+ * Results (u, counts, decision, scan output) equal cl_conv1d_f32 + cl_prefill_f32 bit for
+ * bit. */
+typedef struct {
+  const float* x;      /* (batch, dim, L) conv input */
+  const float* weight; /* (dim, width) */
+  const float* bias;   /* (dim) or NULL */
+  int width;           /* 1..4 */
+  int silu;            /* activation: SiLU (1) or identity (0) */
+} cl_conv_args;
+int cl_prefill_from_conv_f32(cl_ctx* ctx, const cl_conv_args* conv, const cl_mamba1_args* args,
+                             const cl_hist_spec* spec, const cl_rule_spec* rule,
+                             uint64_t* d_counts, double* d_range, cl_decision* d_decision,
+                             void* stream);
+
 /* Sync point: copy the decision to the host and convert a device error into
  * CL_E_DEVICE with the reference's message. */
 int cl_decision_check(cl_ctx* ctx, const cl_decision* d_decision, cl_decision* h_out,

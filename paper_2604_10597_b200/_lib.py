@@ -85,6 +85,11 @@ class cl_scan_plan(C.Structure):
                 ("stages", C.c_int), ("n_seg", C.c_int), ("seg_len", C.c_int)]
 
 
+class cl_conv_args(C.Structure):
+    _fields_ = [("x", C.c_void_p), ("weight", C.c_void_p), ("bias", C.c_void_p),
+                ("width", C.c_int), ("silu", C.c_int)]
+
+
 class cl_shard(C.Structure):
     _fields_ = [("global_batch", C.c_uint64), ("global_dim", C.c_uint64), ("b0", C.c_uint64),
                 ("b1", C.c_uint64), ("d0", C.c_uint64), ("d1", C.c_uint64)]
@@ -149,6 +154,9 @@ SIGNATURES = {
                                  C.POINTER(cl_rule_spec), _P, _P, _P, _P]),
     "cl_decision_check": (C.c_int, [_P, _P, C.POINTER(cl_decision), _P]),
     "cl_collectives_nccl": (C.c_int, [_P, C.POINTER(cl_collectives)]),
+    "cl_prefill_from_conv_f32": (C.c_int, [_P, C.POINTER(cl_conv_args), C.POINTER(cl_mamba1_args),
+                                           C.POINTER(cl_hist_spec), C.POINTER(cl_rule_spec),
+                                           _P, _P, _P, _P]),
     "cl_prefill_sharded_f32": (C.c_int, [_P, C.POINTER(cl_mamba1_args), C.POINTER(cl_shard),
                                          C.POINTER(cl_hist_spec), C.POINTER(cl_rule_spec),
                                          C.POINTER(cl_collectives), _P, _P, _P, _P]),

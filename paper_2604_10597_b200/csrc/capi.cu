@@ -642,6 +642,63 @@ int cl_prefill_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_hist_spec* 
   return cl_selective_scan_f32(ctx, args, d_decision, 0, CL_SCAN_AUTO, stream);
 }
 
+int cl_prefill_from_conv_f32(cl_ctx* ctx, const cl_conv_args* conv, const cl_mamba1_args* args,
+                             const cl_hist_spec* spec, const cl_rule_spec* rule,
+                             uint64_t* d_counts, double* d_range, cl_decision* d_decision,
+                             void* stream) {
+  if (!ctx || !conv || !args) return fail(ctx, CL_E_INVALID, "null argument");
+  int rc = validate_spec(ctx, spec);
+  if (rc) return rc;
+  if ((rc = validate_rule(ctx, rule))) return rc;
+  const uint64_t n = args->batch * args->dim * args->seq_len;
+  if (n == 0) return fail(ctx, CL_E_INVALID, "no samples");
+  if (!conv->x || !conv->weight || !args->u) return fail(ctx, CL_E_INVALID, "null argument");
+  if (conv->width < 1 || conv->width > 4)
+    return fail(ctx, CL_E_INVALID, "conv width must lie in [1, 4]");
+  float* u = const_cast<float*>(args->u);  // the conv's output buffer
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int kind = rule->kind == CL_POL_GUARDED ? rule->inner_kind : rule->kind;
+  if (kind == CL_POL_TOKEN_HIST) {
+    if ((rc = cl_conv1d_f32(ctx, conv->x, conv->weight, conv->bias, u, args->batch, args->dim,
+                            args->seq_len, conv->width, conv->silu, 0, 1, nullptr, stream)))
+      return rc;
+    return cl_prefill_f32(ctx, args, spec, rule, d_counts, d_range, d_decision, stream);
+  }
+  if ((rc = cl_prefill_init(ctx, d_range, d_counts, spec->bin_count, stream))) return rc;
+  if (spec->range_mode == CL_RANGE_FIXED) {
+    cudaError_t e = cudaSuccess;
+    bool fused;
+    {
+      DeviceGuard g(ctx->device);
+      fused = launch_conv_hist_fixed(conv->x, conv->weight, conv->bias, u, args->batch, args->dim,
+                                     args->seq_len, conv->width, conv->silu, *spec, d_counts,
+                                     d_range, ctx->num_sms, s, &e);
+    }
+    if ((rc = check_launch(ctx, e, "conv_hist_fixed"))) return rc;
+    if (fused) {
+      ++ctx->launches;
+    } else {
+      // conv with the range epilogue (its finite flag), then the histogram pass
+      if ((rc = cl_conv1d_f32(ctx, conv->x, conv->weight, conv->bias, u, args->batch, args->dim,
+                              args->seq_len, conv->width, conv->silu, 0, spec->sample_stride,
+                              d_range, stream)) ||
+          (rc = cl_histogram_f32(ctx, u, n, 0, spec, d_range, d_counts, stream)))
+        return rc;
+    }
+    if ((rc = cl_decide(ctx, d_counts, d_range, spec, samples_of(n, spec->sample_stride), rule,
+                        args->seq_len, d_decision, stream)))
+      return rc;
+  } else {
+    if ((rc = cl_conv1d_f32(ctx, conv->x, conv->weight, conv->bias, u, args->batch, args->dim,
+                            args->seq_len, conv->width, conv->silu, 0, spec->sample_stride,
+                            d_range, stream)) ||
+        (rc = cl_histogram_decide_f32(ctx, u, n, spec, d_range, d_counts, rule, args->seq_len,
+                                      d_decision, stream)))
+      return rc;
+  }
+  return cl_selective_scan_f32(ctx, args, d_decision, 0, CL_SCAN_AUTO, stream);
+}
+
 int cl_decision_check(cl_ctx* ctx, const cl_decision* d_decision, cl_decision* h_out,
                       void* stream) {
   if (!ctx || !d_decision) return fail(ctx, CL_E_INVALID, "null argument");

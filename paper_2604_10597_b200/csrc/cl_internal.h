@@ -158,6 +158,10 @@ cudaError_t launch_token_entropy(const unsigned int* d_counts, uint64_t length,
                                  cudaStream_t s);
 cudaError_t launch_entropy_from_masses(const double* d_masses, int k, double eps, double* d_out,
                                        cudaStream_t s);
+bool launch_conv_hist_fixed(const float* x, const float* w, const float* bias, float* u,
+                            uint64_t batch, uint64_t dim, uint64_t L, int width, int silu,
+                            const cl_hist_spec& spec, uint64_t* d_counts, double* d_range,
+                            int num_sms, cudaStream_t s, cudaError_t* err);
 // conv1d.cu
 cudaError_t launch_conv1d_f32(const float* x, const float* w, const float* bias, float* u,
                               uint64_t batch, uint64_t dim, uint64_t L, int width, int silu,

@@ -18,6 +18,7 @@
 #include <cstdint>
 
 #include "cl_internal.h"
+#include "conv_common.cuh"
 #include "range.cuh"
 
 namespace cl {
@@ -32,12 +33,7 @@ __device__ __forceinline__ bool sampled(uint64_t gi, uint64_t stride) {
   return gi % stride == 0;
 }
 
-__device__ __forceinline__ float act(float v, bool silu) {
-  // SiLU: v * sigmoid(v); MUFU exp + fast divide (a few ulp).  The exponent is clamped
-  // at 88 so the denominator stays finite (< 2^128) for v < -88, where the quotient
-  // is then 0 (the limit of v * sigmoid(v))
-  return silu ? __fdividef(v, 1.f + __expf(fminf(-v, 88.f))) : v;
-}
+__device__ __forceinline__ float act(float v, bool silu) { return conv_act(v, silu); }
 
 // Grid-stride cursor over (row, position-in-row, channel) without a 64-bit division per
 // step: the stride is decomposed once per thread.
@@ -167,23 +163,8 @@ __global__ void __launch_bounds__(kConvThreads) conv1d_warp_kernel(ConvArgs a) {
     for (int m = 0; m < kWQ; ++m) {
       if (m >= nb) break;
       // previous quad: lane-1's, or for lane 0 the last quad of the previous block
-      float4 pv;
-      pv.y = __shfl_up_sync(0xffffffffu, in[m].y, 1);
-      pv.z = __shfl_up_sync(0xffffffffu, in[m].z, 1);
-      pv.w = __shfl_up_sync(0xffffffffu, in[m].w, 1);
-      if (lane == 0) pv = prev31;
-      prev31.y = __shfl_sync(0xffffffffu, in[m].y, 31);
-      prev31.z = __shfl_sync(0xffffffffu, in[m].z, 31);
-      prev31.w = __shfl_sync(0xffffffffu, in[m].w, 31);
-      const float xs[8] = {0.f, pv.y, pv.z, pv.w, in[m].x, in[m].y, in[m].z, in[m].w};
       float o[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float s = bias;
-#pragma unroll
-        for (int k = 0; k < W; ++k) s = fmaf(wk[k], xs[4 + i - (W - 1) + k], s);
-        o[i] = act(s, a.silu != 0);
-      }
+      conv_block<W>(in[m], prev31, lane, wk, bias, a.silu != 0, o);
       const uint64_t q = qb + m * 32 + lane;
       __stcs(u4 + q, make_float4(o[0], o[1], o[2], o[3]));
       if (a.range) {

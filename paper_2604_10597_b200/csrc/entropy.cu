@@ -25,6 +25,7 @@
 #ifndef CL_DEVICE_CHECKS
 #define CL_DEVICE_CHECKS 0
 #endif
+#include "conv_common.cuh"
 #include "range.cuh"
 
 namespace cl {
@@ -1102,6 +1103,107 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1)
 }
 
 
+// Producer fusion with a Fixed range ("deeper kernel fusion of the
+// entropy estimator"): the conv1d (+ SiLU) that produces u bins every u it writes.  With a
+// Fixed range the bin edges are known before u exists (entropy.hpp:116-119), so u is
+// never read back for the histogram: x is read once, u written once, counts come out of
+// the same pass.  The conv arithmetic is conv1d.cu's (conv_common.cuh: identical bits of
+// u) in its warp-coalesced layout (a warp unit = kCHWQ 32-quad blocks of one row, lane l
+// holding quad l of each), so a full unit is exactly kLaneSamples values per lane: the
+// hot path's lane_count_u8 (u8 lane counters, exact fp64 fallback near edges and for
+// clipped outliers).  Every element is also checked for finiteness (validate_tensor,
+// entropy.hpp:42) into d_range[2].  Needs L % 128 == 0, 16-byte aligned x / u, K <= 256.
+constexpr int kCHWarps = 8;
+constexpr int kCHWQ = 4;  // = conv1d.cu kWQ
+static_assert(kCHWQ * 4 == kLaneSamples, "a full warp unit is one lane_count_u8 call");
+constexpr size_t kCHSmem = size_t(kCHWarps) * kLaneBins * kBinStride + kLaneBins * 4;
+
+template <int W>
+__global__ void __launch_bounds__(kCHWarps * 32)
+    conv_hist_fixed_kernel(const float* __restrict__ x, const float* __restrict__ wts,
+                           const float* __restrict__ cbias, float* __restrict__ u, uint64_t rows,
+                           uint64_t dim, uint64_t L, int silu, double fixed_lo, double fixed_hi,
+                           int k, unsigned long long* d_counts, double* d_range) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  cnt_t* counters = reinterpret_cast<cnt_t*>(smem);
+  uint32_t* cta_hist = reinterpret_cast<uint32_t*>(smem + size_t(kCHWarps) * kLaneBins * kBinStride);
+  __shared__ BinParams sp;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) sp = make_bin_params_lohi(fixed_lo, fixed_hi, k);
+  {
+    uint4* c4 = reinterpret_cast<uint4*>(smem);
+    for (int i = threadIdx.x; i < static_cast<int>(size_t(kCHWarps) * kLaneBins * kBinStride / 16);
+         i += blockDim.x)
+      c4[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < kLaneBins; i += blockDim.x) cta_hist[i] = 0;
+  }
+  __syncthreads();
+  const BinParams p = sp;
+  unsigned char* lane_base =
+      reinterpret_cast<unsigned char*>(counters + warp * kLaneBins * 32) + lane * 4;
+  const uint64_t qpr = L / 4;
+  const uint64_t runs_per_row = qpr / (32 * kCHWQ);
+  const uint64_t tail_blocks = (qpr / 32) % kCHWQ;
+  const uint64_t units_per_row = runs_per_row + (tail_blocks ? 1 : 0);
+  const uint64_t units = rows * units_per_row;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float4* u4 = reinterpret_cast<float4*>(u);
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * kCHWarps;
+  bool bad = false;
+  uint32_t since_flush = 0;
+  for (uint64_t unit = static_cast<uint64_t>(blockIdx.x) * kCHWarps + warp; unit < units;
+       unit += warps) {
+    const uint64_t row = unit / units_per_row;
+    const uint64_t ur = unit - row * units_per_row;
+    const int nb = ur < runs_per_row ? kCHWQ : static_cast<int>(tail_blocks);
+    const uint64_t qb = row * qpr + ur * 32 * kCHWQ;
+    const uint64_t d = row % dim;
+    float4 in[kCHWQ];
+#pragma unroll
+    for (int m = 0; m < kCHWQ; ++m)
+      in[m] = m < nb ? __ldcs(x4 + qb + m * 32 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 prev31 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (ur > 0) prev31 = __ldg(x4 + qb - 1);
+    float wk[W];
+#pragma unroll
+    for (int kk = 0; kk < W; ++kk) wk[kk] = __ldg(wts + d * W + kk);
+    const float bias = cbias ? __ldg(cbias + d) : 0.f;
+    float val[kLaneSamples];
+#pragma unroll
+    for (int m = 0; m < kCHWQ; ++m) {
+      if (m >= nb) break;
+      float o[4];
+      conv_block<W>(in[m], prev31, lane, wk, bias, silu != 0, o);
+      __stcs(u4 + qb + m * 32 + lane, make_float4(o[0], o[1], o[2], o[3]));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        val[4 * m + i] = o[i];
+        bad |= !range::finite_f32(o[i]);
+      }
+    }
+    if (nb == kCHWQ) {
+      lane_count_u8(val, p, reinterpret_cast<unsigned char*>(counters), warp, lane);
+    } else {
+#pragma unroll
+      for (int m = 0; m < kCHWQ; ++m) {
+        if (m >= nb) break;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cref(lane_base, bin_f32(val[4 * m + i], p, true)) += 1;
+      }
+    }
+    if (++since_flush == kFlushChunks) {
+      flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+      since_flush = 0;
+    }
+  }
+  flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+  bad = __any_sync(0xffffffffu, bad);
+  __syncthreads();
+  for (int b = threadIdx.x; b < k; b += blockDim.x)
+    if (cta_hist[b]) atomicAdd(d_counts + b, static_cast<unsigned long long>(cta_hist[b]));
+  if (bad && lane == 0) range::atomic_max_f64(d_range + 2, 1.0);
+}
+
 // K > 256 (or f64 input): shared-memory atomics on a CTA histogram.
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kThreads)
@@ -1884,6 +1986,39 @@ cudaError_t launch_histogram_f64(const double* v, uint64_t n, uint64_t g0,
         use_smem);
   ++*launches;
   return cudaGetLastError();
+}
+
+// The conv + Fixed-range histogram epilogue, when it applies (returns false otherwise;
+// the caller then runs cl_conv1d_f32 + the histogram).
+bool launch_conv_hist_fixed(const float* x, const float* w, const float* bias, float* u,
+                            uint64_t batch, uint64_t dim, uint64_t L, int width, int silu,
+                            const cl_hist_spec& spec, uint64_t* d_counts, double* d_range,
+                            int num_sms, cudaStream_t s, cudaError_t* err) {
+  *err = cudaSuccess;
+  if (!CL_HIST_U8 || spec.range_mode != CL_RANGE_FIXED || spec.sample_stride != 1 ||
+      spec.bin_count > kLaneBins || L % 128 != 0 || width < 1 || width > 4 ||
+      (reinterpret_cast<uintptr_t>(x) & 15u) || (reinterpret_cast<uintptr_t>(u) & 15u))
+    return false;
+  const uint64_t rows = batch * dim;
+  const uint64_t units = rows * ((L / 4) / (32 * kCHWQ) + ((L / 4 / 32) % kCHWQ ? 1 : 0));
+  const uint64_t want = (units + kCHWarps - 1) / kCHWarps;
+  const uint64_t cap = static_cast<uint64_t>(num_sms) * 3;  // 3 x 65 KB per SM
+  const int grid = static_cast<int>(want < cap ? (want < 1 ? 1 : want) : cap);
+  auto* counts = reinterpret_cast<unsigned long long*>(d_counts);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kCHSmem));
+    kern<<<grid, kCHWarps * 32, kCHSmem, s>>>(x, w, bias, u, rows, dim, L, silu, spec.fixed_lo,
+                                              spec.fixed_hi, spec.bin_count, counts, d_range);
+  };
+  switch (width) {
+    case 1: go(conv_hist_fixed_kernel<1>); break;
+    case 2: go(conv_hist_fixed_kernel<2>); break;
+    case 3: go(conv_hist_fixed_kernel<3>); break;
+    default: go(conv_hist_fixed_kernel<4>); break;
+  }
+  *err = cudaGetLastError();
+  return true;
 }
 
 cudaError_t launch_decide(const uint64_t* d_counts, const double* d_range,

@@ -351,23 +351,36 @@ class Prefill:
 
     def from_conv(self, x, conv_weight, conv_bias, delta, A, B, C, D=None, z=None,
                   delta_bias=None, delta_softplus=True, out=None, return_last_state=False,
-                  h0=None, activation="silu"):
-        """The prefill with its producer fused: conv1d(+SiLU) -> u with the min/max
-        epilogue, then histogram -> decide -> scan.  Returns (PrefillResult, u)."""
+                  h0=None, activation="silu", u=None):
+        """The prefill with its producer fused (cl_prefill_from_conv_f32): u =
+        act(causal_conv1d(x)) is produced with the entropy stage riding on it -- the
+        min/max epilogue (Dynamic range) or the whole histogram epilogue (Fixed range) --
+        then decide -> scan.  Returns (PrefillResult, u)."""
         # x stands in for u (same shape) until the conv has produced it
         check_scan_inputs(x, delta, A, B, C, D, z, delta_bias, h0, out, device=self.device)
-        for name, t in (("conv_weight", conv_weight), ("conv_bias", conv_bias)):
+        for name, t in (("conv_weight", conv_weight), ("conv_bias", conv_bias), ("u", u)):
             _check_f32(name, t, self.device)
+        if activation not in (None, "silu", "swish"):
+            raise InvalidInput("activation must be None, 'silu' or 'swish'")
         if x.numel() == 0:
             raise InvalidInput("no samples")
-        u = self.stage_conv(x, conv_weight, conv_bias, activation)
-        uf = u.reshape(-1)
-        self.stage_histogram(uf)
-        self.stage_decide(self.n_samples(uf.numel()), u.shape[-1])
-        res = self.stage_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, out,
-                              return_last_state, h0)
-        o, h = res if return_last_state else (res, None)
-        return PrefillResult(o, h, self.decision_buf), u
+        if conv_weight.dim() != 2 or conv_weight.shape[0] != x.shape[1] or (
+                conv_bias is not None and conv_bias.numel() != x.shape[1]):
+            raise InvalidInput("shape mismatch")
+        u = torch.empty_like(x) if u is None else u
+        out = torch.empty_like(x) if out is None else out
+        h_last = (torch.empty(x.shape[0], x.shape[1], A.shape[1], device=x.device)
+                  if return_last_state else None)
+        a = _mamba_args(u, delta, A, B, C, D, z, delta_bias, h0, out, h_last, delta_softplus)
+        cv = _lib.cl_conv_args()  # noqa: F841
+        cv.x, cv.weight, cv.bias = x.data_ptr(), conv_weight.data_ptr(), _ptr(conv_bias)
+        cv.width, cv.silu = int(conv_weight.shape[1]), int(activation is not None)
+        buf = self.token_buf if self.token else self.range
+        # (the parameter C shadows the ctypes module here: C_byref is module level)
+        self.ctx.call("cl_prefill_from_conv_f32", C_byref(cv), C_byref(a), C_byref(self.cspec),
+                      C_byref(self.rule), self.counts.data_ptr(), buf.data_ptr(),
+                      self.decision_buf.data_ptr(), _stream_ptr(self.device))
+        return PrefillResult(out, h_last, self.decision_buf), u
 
     def decision(self) -> DecisionRecord:
         return read_decision(self.decision_buf)

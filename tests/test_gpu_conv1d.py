@@ -85,25 +85,83 @@ def test_fused_range_flags_nonfinite(cuda):
     assert r[2].item() == 1.0
 
 
-@pytest.mark.parametrize("stride", [1, 8])
-def test_prefill_from_conv_equals_unfused(cuda, stride):
-    """Fused producer -> histogram -> decide -> scan gives the same decision, entropy
-    and output (bitwise) as conv, then the unfused prefill on the same u."""
-    m = mamba_inputs(21, 2, 64, 16, 512)
-    x, w, b = conv_inputs(22, 2, 64, 512, 4)
+FROM_CONV_CASES = {
+    # name: (spec, L, width, policy)
+    "dynamic": (dict(), 512, 4, None),
+    "dynamic-stride8": (dict(sample_stride=8), 512, 4, None),
+    "fixed-fused": (dict(range_mode=cl.RangeMode.Fixed, fixed_lo=-1.5, fixed_hi=2.5), 1024, 4,
+                    None),  # the conv + histogram epilogue kernel (clipped outliers too)
+    "fixed-fused-w3-k64": (dict(range_mode=cl.RangeMode.Fixed, fixed_lo=-3.0, fixed_hi=3.0,
+                                bin_count=64), 1152, 3, None),  # tail units (1152/4/32 = 9)
+    "fixed-fallback": (dict(range_mode=cl.RangeMode.Fixed, fixed_lo=-1.5, fixed_hi=2.5), 516, 4,
+                       None),  # L % 128 != 0: conv + separate histogram
+    "fixed-stride3": (dict(range_mode=cl.RangeMode.Fixed, fixed_lo=-1.5, fixed_hi=2.5,
+                           sample_stride=3), 512, 2, None),
+    "token": (dict(), 512, 4, "token"),
+}
+
+
+@pytest.mark.parametrize("case", sorted(FROM_CONV_CASES))
+def test_prefill_from_conv_equals_unfused(cuda, case):
+    """cl_prefill_from_conv_f32 (producer fused: min/max or the whole Fixed-range histogram
+    in the conv epilogue) gives the same u, counts, decision and scan output, bit for bit,
+    as the conv followed by the unfused prefill on the same u."""
+    kw, L, width, pol = FROM_CONV_CASES[case]
+    m = mamba_inputs(21, 2, 64, 16, L)
+    x, w, b = conv_inputs(22, 2, 64, L, width)
     d = {k: t(v, cuda) for k, v in m.items()}
-    spec = cl.HistogramSpec(sample_stride=stride)
-    pf_fused = Prefill(spec, device=cuda)
+    spec = cl.HistogramSpec(**kw)
+    policy = bounds = None
+    if pol == "token":
+        policy = cl.SchedulerPolicy(cl.TokenHistogramPolicy(), [128, 256, 512])
+        bounds = cl.ChunkBounds(128, 512)
+    pf_fused = Prefill(spec, policy, bounds, device=cuda)
     res_f, u = pf_fused.from_conv(t(x, cuda), t(w, cuda), t(b, cuda), d["delta"], d["A"],
-                                  d["B"], d["C"], d["D"], d["z"], d["delta_bias"], True)
+                                  d["B"], d["C"], d["D"], d["z"], d["delta_bias"], True,
+                                  return_last_state=True)
     rec_f = res_f.decision()
-    pf = Prefill(spec, device=cuda)
-    res = pf(u, d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"], True)
+    u_ref = causal_conv1d_fn(t(x, cuda), t(w, cuda), t(b, cuda), "silu")
+    assert torch.equal(u, u_ref)
+    pf = Prefill(spec, policy, bounds, device=cuda)
+    res = pf(u_ref, d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"], True,
+             return_last_state=True)
     rec = res.decision()
+    assert torch.equal(pf_fused.decision_buf, pf.decision_buf)
+    if pol is None:
+        assert torch.equal(pf_fused.counts, pf.counts)
     assert rec_f.decision.chunk == rec.decision.chunk
     assert rec_f.entropy.raw_nats == rec.entropy.raw_nats
     assert (rec_f.lo, rec_f.hi) == (rec.lo, rec.hi)
-    assert torch.equal(res_f.out, res.out)
+    assert torch.equal(res_f.out, res.out) and torch.equal(res_f.h_last, res.h_last)
+
+
+def test_prefill_from_conv_fixed_counts_vs_oracle(cuda, port):
+    """The conv + Fixed-range histogram epilogue's counts against the C oracle's
+    compute_histogram (Fixed mode, entropy.hpp:116-119) of the produced u."""
+    x, w, b = conv_inputs(23, 2, 96, 2048, 4)
+    m = mamba_inputs(24, 2, 96, 16, 2048)
+    d = {k: t(v, cuda) for k, v in m.items()}
+    spec = cl.HistogramSpec(range_mode=cl.RangeMode.Fixed, fixed_lo=-0.5, fixed_hi=1.0)
+    pf = Prefill(spec, device=cuda)
+    _, u = pf.from_conv(t(x, cuda), t(w, cuda), t(b, cuda), d["delta"], d["A"], d["B"], d["C"],
+                        d["D"], d["z"], d["delta_bias"], True)
+    ref, *_ = port.histogram(u.cpu().numpy().reshape(-1), 256, 1e-8, 1, fixed=(-0.5, 1.0))
+    assert (pf.counts.cpu().numpy().astype(np.uint64) == ref).all()
+
+
+def test_prefill_from_conv_nonfinite_defers_error(cuda):
+    x, w, b = conv_inputs(25, 1, 64, 512, 4)
+    x[0, 5, 100] = np.nan
+    m = mamba_inputs(26, 1, 64, 16, 512)
+    d = {k: t(v, cuda) for k, v in m.items()}
+    for kw in (dict(), dict(range_mode=cl.RangeMode.Fixed, fixed_lo=-1.0, fixed_hi=1.0)):
+        pf = Prefill(cl.HistogramSpec(**kw), device=cuda)
+        out = torch.full_like(d["u"], 3.0)
+        res, _ = pf.from_conv(t(x, cuda), t(w, cuda), t(b, cuda), d["delta"], d["A"], d["B"],
+                              d["C"], d["D"], d["z"], d["delta_bias"], True, out=out)
+        with pytest.raises(cl.InvalidInput, match="non-finite input"):
+            res.decision()
+        assert bool((out == 3.0).all())
 
 
 def test_conv_validation(cuda):
