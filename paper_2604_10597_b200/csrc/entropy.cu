@@ -27,6 +27,7 @@
 #endif
 #include "conv_common.cuh"
 #include "range.cuh"
+#include "tma_map.cuh"
 
 namespace cl {
 namespace {
@@ -1475,6 +1476,14 @@ constexpr int kTokMmRows = CL_TOK_MM_ROWS;  // min/max: channel rows per batch
 constexpr int kTokMmCols = CL_TOK_MM_COLS;  // min/max: 128-position slices per block tile
 constexpr int kTokHUnroll = CL_TOK_H_UNROLL;  // hist: channel rows per batch (2 in flight)
 constexpr int kTokHMaxPerFlush = 65000;     // u16 counters: flush before overflow
+// Token histogram kernel: the LDG-fed lane kernel (default) or the TMA-fed one
+// (CL_TOK_TMA=1).  Measured at C3 (channels 32768, L 8192, K 256; profiles/r2f_token_ab.txt):
+// lane 0.537 ms, TMA 0.670 ms -- the loop is instruction-bound (about 27 instructions per
+// sampled element: binning, the exact-path test, two u16 read-modify-writes), not load-bound,
+// and the TMA kernel's 8 consumer warps per SM issue them slower than the lane kernel's 12.
+#ifndef CL_TOK_TMA
+#define CL_TOK_TMA 0
+#endif
 
 __device__ __forceinline__ void tok_item_split(uint64_t item, uint64_t tiles, uint64_t splits,
                                                uint64_t channels, uint64_t* tile,
@@ -1510,12 +1519,25 @@ __global__ void __launch_bounds__(kTokMmWarps * 32) token_minmax_lane_kernel(
       uint64_t cm = (a.offset + w0) % a.stride;  // (offset + c) % stride, incremental
       uint64_t c = w0;
       const float* rp = v + w0 * a.length + t0;
+      // one batch of rows in flight ahead of the one being reduced
+      float4 qn[kTokMmRows];
+      if (c + kTokMmRows <= w1) {
+#pragma unroll
+        for (int i = 0; i < kTokMmRows; ++i) {
+          qn[i] = __ldcs(reinterpret_cast<const float4*>(rp));
+          rp += a.length;
+        }
+      }
       for (; c + kTokMmRows <= w1; c += kTokMmRows) {
         float4 q[kTokMmRows];
 #pragma unroll
-        for (int i = 0; i < kTokMmRows; ++i) {
-          q[i] = __ldcs(reinterpret_cast<const float4*>(rp));
-          rp += a.length;
+        for (int i = 0; i < kTokMmRows; ++i) q[i] = qn[i];
+        if (c + 2 * kTokMmRows <= w1) {
+#pragma unroll
+          for (int i = 0; i < kTokMmRows; ++i) {
+            qn[i] = __ldcs(reinterpret_cast<const float4*>(rp));
+            rp += a.length;
+          }
         }
 #pragma unroll
         for (int i = 0; i < kTokMmRows; ++i) {
@@ -1573,6 +1595,16 @@ __global__ void __launch_bounds__(kTokMmWarps * 32) token_minmax_lane_kernel(
   if (threadIdx.x == 0 && s_bad) atomic_max_f64(flag, 1.0);
 }
 
+// u16 counters of (warp w, bin b, lane l): lane l owns the 32-bit word (b/2)*32 + l of its
+// warp's 16 KB block, even bin in the low half, odd in the high -- every lane addresses
+// only its own bank (the earlier [bin][lane] halves put a lane pair in one bank with
+// different words whenever their bins differed with equal parity: 48% of shared wavefronts
+// were conflicts, ncu, profiles/r2f_token_ncu.txt).
+__device__ __forceinline__ uint32_t tok_cidx(int w, int b, int lane) {  // in u16 units
+  return static_cast<uint32_t>(w) * 8192u + ((static_cast<uint32_t>(b) >> 1) * 32u + lane) * 2u +
+         (static_cast<uint32_t>(b) & 1u);
+}
+
 // Adds the block's 4 warps' counters for its 32 positions into counts [L][K] and clears
 // them: warp w sums bins w, w+4, ... over the warps for position (tile*32 + lane).
 __device__ __forceinline__ void tok_flush(uint16_t* cnt, uint64_t t, bool t_ok, int k,
@@ -1582,7 +1614,7 @@ __device__ __forceinline__ void tok_flush(uint16_t* cnt, uint64_t t, bool t_ok, 
   for (int b = warp; b < k; b += kTokHWarps) {
     uint32_t sum = 0;
 #pragma unroll
-    for (int w = 0; w < kTokHWarps; ++w) sum += cnt[(w * 256 + b) * 32 + lane];
+    for (int w = 0; w < kTokHWarps; ++w) sum += cnt[tok_cidx(w, b, lane)];
     if (sum && t_ok) atomicAdd(counts + t * k + b, sum);
   }
   __syncthreads();
@@ -1596,7 +1628,7 @@ template <bool FIXED>
 __global__ void __launch_bounds__(kTokHWarps * 32) token_hist_lane_kernel(
     const float* __restrict__ v, TokArgs a, uint64_t tiles, uint64_t splits,
     const double* trange, double fixed_lo, double fixed_hi, unsigned int* counts) {
-  extern __shared__ __align__(16) uint16_t tcnt[];  // [warp][256 bins][32 lanes]
+  extern __shared__ __align__(16) uint16_t tcnt[];  // [warp][128 bin pairs][32 lanes][2]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int k = a.k;
   {
@@ -1606,7 +1638,7 @@ __global__ void __launch_bounds__(kTokHWarps * 32) token_hist_lane_kernel(
   }
   __syncthreads();
   const uint32_t cbase = static_cast<uint32_t>(__cvta_generic_to_shared(tcnt)) +
-                         static_cast<uint32_t>(warp) * (256 * 32 * 2) + lane * 2u;
+                         static_cast<uint32_t>(warp) * (256 * 32 * 2) + lane * 4u;
   for (uint64_t item = blockIdx.x; item < tiles * splits; item += gridDim.x) {
     uint64_t tile, c0, c1;
     tok_item_split(item, tiles, splits, a.channels, &tile, &c0, &c1);
@@ -1680,8 +1712,8 @@ __global__ void __launch_bounds__(kTokHWarps * 32) token_hist_lane_kernel(
         const uint32_t i0 = (full || i + 2 * g < n) ? inc : 0u;
         const uint32_t i1 = (full || i + 2 * g + 1 < n) ? inc : 0u;
         const int b0 = bin[2 * g], b1 = bin[2 * g + 1];
-        const uint32_t a0 = cbase + static_cast<uint32_t>(b0) * 64u;
-        const uint32_t a1 = cbase + static_cast<uint32_t>(b1) * 64u;
+        const uint32_t a0 = cbase + (static_cast<uint32_t>(b0) & ~1u) * 64u + (b0 & 1) * 2u;
+        const uint32_t a1 = cbase + (static_cast<uint32_t>(b1) & ~1u) * 64u + (b1 & 1) * 2u;
         uint32_t v0, v1;
         asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
         asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
@@ -1698,6 +1730,160 @@ __global__ void __launch_bounds__(kTokHWarps * 32) token_hist_lane_kernel(
       }
     }
     tok_flush(tcnt, t, t_ok, k, counts);
+  }
+}
+
+// TMA-fed token histogram (the fp32 / K <= 256 hot path of token_entropy stage 2).  A block
+// owns a tile of 128 positions and a channel range; its producer warp streams boxes of
+// {128 positions x kTokBoxRows channel rows} (8 KB) through a kTokStages-deep shared-memory
+// ring with cp.async.bulk.tensor, so the loads in flight per SM no longer live in consumer
+// registers (the LDG-fed lane kernel above sat on long-scoreboard stalls at 12 warps per SM,
+// profiles/r2f_token_ncu.txt).  Consumer warp w owns positions 32w .. 32w+31 of the tile (lane
+// = position) with private u16 counters in the bank-exclusive pair layout (tok_cidx), reads
+// its 32 floats of each sampled row from the stage (conflict-free), bins them exactly like the
+// lane kernel, and at the end of the item adds its counters into counts [L][K] (atomics; the
+// positions of different warps are disjoint, so no block reduction).
+constexpr int kTokTWarps = 4;                      // consumer warps: 128 positions
+constexpr int kTokBoxRows = 16;                    // channel rows per box
+constexpr int kTokStages = 5;                      // ring depth (2 blocks fit an SM)
+constexpr int kTokBoxBytes = 128 * kTokBoxRows * 4;  // 8 KB
+constexpr size_t kTokTSmem = size_t(kTokTWarps) * 256 * 32 * 2 + size_t(kTokStages) * kTokBoxBytes +
+                             2 * kTokStages * 8 + 1024;
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool FIXED>
+__global__ void __launch_bounds__((kTokTWarps + 1) * 32) token_hist_tma_kernel(
+    const __grid_constant__ CUtensorMap map, TokArgs a, uint64_t tiles, uint64_t splits,
+    const double* trange, double fixed_lo, double fixed_hi, unsigned int* counts) {
+  extern __shared__ __align__(128) unsigned char tsm[];
+  unsigned char* base = tsm + ((1024u - (smem_u32(tsm) & 1023u)) & 1023u);
+  uint16_t* tcnt = reinterpret_cast<uint16_t*>(base);  // [warp][128 bin pairs][32 lanes][2]
+  unsigned char* ring = base + size_t(kTokTWarps) * 256 * 32 * 2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(kTokStages) * kTokBoxBytes);
+  uint64_t* empty = full + kTokStages;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int k = a.k;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTokStages; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, kTokTWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  {
+    uint4* c4 = reinterpret_cast<uint4*>(tcnt);
+    for (int i = threadIdx.x; i < kTokTWarps * 256 * 32 * 2 / 16; i += blockDim.x)
+      c4[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  const uint64_t n_items = tiles * splits;
+  const uint64_t per_split = (a.channels + splits - 1) / splits;
+  if (warp == kTokTWarps) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)));
+      uint32_t it = 0;
+      for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const uint64_t tile = item % tiles, c0 = (item / tiles) * per_split;
+        const uint64_t c1 = umin64(a.channels, c0 + per_split);
+        for (uint64_t c = c0; c < c1; c += kTokBoxRows, ++it) {
+          const int st = it % kTokStages;
+          if (it >= static_cast<uint32_t>(kTokStages)) mbar_wait(empty + st, ((it / kTokStages) - 1) & 1);
+          mbar_expect_tx(full + st, kTokBoxBytes);
+          tma_load_3d(ring + size_t(st) * kTokBoxBytes, &map, static_cast<int>(tile * 128),
+                      static_cast<int>(c), 0, full + st);
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const uint32_t cbase = smem_u32(tcnt) + static_cast<uint32_t>(warp) * (256 * 32 * 2) + lane * 4u;
+  uint32_t it = 0;
+  for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const uint64_t tile = item % tiles, c0 = (item / tiles) * per_split;
+    const uint64_t c1 = umin64(a.channels, c0 + per_split);
+    const uint64_t t = tile * 128 + warp * 32 + lane;
+    const bool t_ok = t < a.length;
+    const BinParams P = FIXED ? make_bin_params_lohi(fixed_lo, fixed_hi, k)
+                        : t_ok ? make_bin_params_lohi(-trange[t], trange[a.length + t], k)
+                               : make_bin_params_lohi(0.0, 0.0, k);
+    const uint32_t inc = t_ok ? 1u : 0u;
+    uint64_t cm = (a.offset + c0) % a.stride;  // (offset + c) % stride of the box's first row
+    uint32_t since = 0;
+    for (uint64_t c = c0; c < c1; c += kTokBoxRows, ++it) {
+      const int st = it % kTokStages;
+      mbar_wait(full + st, (it / kTokStages) & 1);
+      const float* box = reinterpret_cast<const float*>(ring + size_t(st) * kTokBoxBytes);
+      const int rows = static_cast<int>(umin64(kTokBoxRows, c1 - c));
+      float x[kTokBoxRows];
+      uint32_t smp = 0;  // bit r: row r is sampled
+#pragma unroll
+      for (int r = 0; r < kTokBoxRows; ++r) {
+        x[r] = box[r * 128 + warp * 32 + lane];
+        const bool ok = r < rows && cm == 0;
+        smp |= (ok ? 1u : 0u) << r;
+        if (++cm == a.stride) cm = 0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);  // the stage's values are in registers
+      int bin[kTokBoxRows];
+      bool any_slow = P.exact_only != 0;
+#pragma unroll
+      for (int r = 0; r < kTokBoxRows; ++r) {
+        bool sl;
+        bin[r] = bin_fast<FIXED>(x[r], P, &sl);
+        any_slow |= sl && ((smp >> r) & 1u);
+      }
+      if (__any_sync(0xffffffffu, any_slow)) {
+#pragma unroll
+        for (int r = 0; r < kTokBoxRows; ++r) {
+          bool sl;
+          bin_fast<FIXED>(x[r], P, &sl);
+          if ((sl || P.exact_only) && ((smp >> r) & 1u))
+            bin[r] = bin_index_exact(static_cast<double>(x[r]), P.lo, P.width, k);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < kTokBoxRows / 2; ++g) {
+        const uint32_t i0 = (smp >> (2 * g)) & 1u ? inc : 0u;
+        const uint32_t i1 = (smp >> (2 * g + 1)) & 1u ? inc : 0u;
+        const int b0 = bin[2 * g] & 255, b1 = bin[2 * g + 1] & 255;
+        const uint32_t a0 = cbase + (static_cast<uint32_t>(b0) & ~1u) * 64u + (b0 & 1) * 2u;
+        const uint32_t a1 = cbase + (static_cast<uint32_t>(b1) & ~1u) * 64u + (b1 & 1) * 2u;
+        uint32_t v0, v1;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
+        v0 += i0;
+        v1 += i1 + (b0 == b1 ? i0 : 0u);
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(a0), "h"(static_cast<uint16_t>(v0)) : "memory");
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(a1), "h"(static_cast<uint16_t>(v1)) : "memory");
+      }
+      since += kTokBoxRows;
+      if (since > kTokHMaxPerFlush - kTokBoxRows || c + kTokBoxRows >= c1) {
+        // this warp's 32 positions into counts [L][K], counters cleared (warp-local)
+        __syncwarp();
+        if (t_ok) {
+          for (int b = 0; b < k; ++b) {
+            const uint32_t v = tcnt[tok_cidx(warp, b, lane)];
+            if (v) atomicAdd(counts + t * k + b, v);
+          }
+        }
+        __syncwarp();
+        uint4* c4 = reinterpret_cast<uint4*>(tcnt + tok_cidx(warp, 0, 0));
+        for (int i = lane; i < 256 * 32 * 2 / 16; i += 32) c4[i] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        since = 0;
+      }
+    }
   }
 }
 
@@ -2149,6 +2335,30 @@ template <typename T>
 cudaError_t launch_token_hist(const T* v, uint64_t channels, uint64_t length, uint64_t offset,
                               const cl_hist_spec& spec, const double* d_trange,
                               unsigned int* d_counts, int num_sms, cudaStream_t s) {
+  if (CL_TOK_TMA && tok_lane_ok(v, length, spec.bin_count) && length <= (1ull << 31) &&
+      channels <= (1ull << 31) && get_encode()) {
+    const TokArgs a{channels, length, offset, spec.sample_stride, spec.bin_count, 1};
+    CUtensorMap map;
+    if (!make_map(&map, reinterpret_cast<const float*>(v), length, channels, 1, 128, kTokBoxRows,
+                  0))
+      return cudaErrorInvalidValue;
+    uint64_t tiles, splits;
+    const int resident = num_sms * 2;  // 2 blocks (64 KB counters + 40 KB ring) per SM
+    tok_lane_items(channels, length, 128, resident, &tiles, &splits);
+    // at least a few boxes per item
+    const uint64_t max_sp = (channels + 4 * kTokBoxRows - 1) / (4 * kTokBoxRows);
+    if (splits > max_sp) splits = max_sp < 1 ? 1 : max_sp;
+    const uint64_t items = tiles * splits;
+    const unsigned grid = static_cast<unsigned>(items < static_cast<uint64_t>(resident) ? items : resident);
+    const bool fixed = spec.range_mode == CL_RANGE_FIXED;
+    auto kern = fixed ? token_hist_tma_kernel<true> : token_hist_tma_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kTokTSmem));
+    if (e != cudaSuccess) return e;
+    kern<<<grid, (kTokTWarps + 1) * 32, kTokTSmem, s>>>(map, a, tiles, splits, d_trange,
+                                                        spec.fixed_lo, spec.fixed_hi, d_counts);
+    return cudaGetLastError();
+  }
   if (tok_lane_ok(v, length, spec.bin_count)) {
     const TokArgs a{channels, length, offset, spec.sample_stride, spec.bin_count, 1};
     uint64_t tiles, splits;
