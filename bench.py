@@ -54,6 +54,27 @@ CONFIGS = {
 }
 
 
+def library_sha256():
+    import hashlib
+    from paper_2604_10597_b200 import _lib
+    h = hashlib.sha256()
+    with open(_lib.LIB_PATH, "rb") as f:
+        h.update(f.read())
+    return h.hexdigest()
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -239,6 +260,7 @@ def reference_arm(args):
                        "policy": "calibrated rule log K, bounds [32,512]"},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind,
+                             "cpu": cpu_model(),
                              "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
@@ -261,6 +283,9 @@ def main():
     ap.add_argument("--no-producer", action="store_true",
                     help="skip the side measurements (conv1d producer fusion, token entropy)")
     ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--pipelined", action="store_true",
+                    help="also measure two batches in flight (entropy of call i+1 in the lean "
+                         "kernels under call i's scan); measured slower on B200, see DESIGN.md")
     ap.add_argument("--eager", action="store_true",
                     help="launch every stage from the host each step instead of replaying "
                          "per-stage CUDA graphs")
@@ -476,13 +501,23 @@ def main():
     ent_ms = statistics.mean(stage_ms["entropy"])
     scan_gbs = ab["scan"] / (scan_ms / 1e3) / 1e9
     step_gbs = ab["total"] / (ms_per_step / 1e3) / 1e9  # per rank
+    # ncu DRAM bytes of the dominant kernel, captured by tools/scan_traffic.py for this
+    # exact library build (sha256 of libchunklab_b200.so), config and kernel; null when the
+    # record is for another build (a stale figure is worse than none)
     traffic = None
+    traffic_note = "no ncu record"
     prof = os.path.join(ROOT, "profiles", "scan_traffic.json")
     if os.path.exists(prof):
         with open(prof) as f:
-            pj = json.load(f)
-        if pj.get("config") == args.config:
-            traffic = pj.get("dram_bytes_per_launch")
+            recs = json.load(f)
+        recs = recs if isinstance(recs, list) else [recs]
+        lib_sha = library_sha256()
+        traffic_note = "ncu record is for another library build or config"
+        for pj in recs:
+            if (pj.get("config") == args.config and pj.get("lib_sha256") == lib_sha and
+                    pj.get("kernel_family") == plan_info["kernel"]):
+                traffic = pj.get("dram_bytes_per_launch")
+                traffic_note = "ncu --set full of this build: " + str(pj.get("source", ""))
 
     result = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -498,7 +533,8 @@ def main():
                           f"L2; no flush needed")},
         "hbm_gbs": step_gbs, "roofline_frac_step": step_gbs / peak,
         "roofline": {"bound": "hbm", "achieved": scan_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": scan_gbs / peak, "traffic": traffic, "kernel": "rowpair_ws_kernel",
+                     "frac": scan_gbs / peak, "traffic": traffic, "traffic_source": traffic_note,
+                     "kernel": "rowpair_ws_kernel",
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": ab["scan"]},
         "stage_ms": ({k: statistics.mean(v) for k, v in stage_ms.items()} if world == 1 else
@@ -533,6 +569,16 @@ def main():
                                  "frac": sfu_ach / sfu_peak,
                                  "mufu_per_launch": mufu_per_launch,
                                  "peak_basis": f"16/clk/SM x {n_sms} SMs x {sm_mhz:.0f} MHz"}
+
+    # ---- pipelined steady state (two batches in flight), a separately labelled figure
+    if world == 1 and args.pipelined and args.chunk_policy == "rule":
+        torch.cuda.synchronize()
+        pf(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"], x["delta_bias"], True,
+           out=out)  # the serial reference output of batch 0 (same decision buffers)
+        torch.cuda.synchronize()
+        result["pipelined"] = pipelined_measure(
+            torch, device, x, pf, out, max(args.steps // 2, 6),
+            lambda seed: make_inputs(torch, device, batch, dim, L, N, seed))
 
     # ---- producer fusion (conv1d + SiLU with the min/max epilogue), side measurement
     if not args.no_producer and world == 1:
@@ -570,6 +616,7 @@ def main():
             dt, _, _ = cpu_reference_step(kind, xh, dim, L, N, threads, ref, port)
             result["cpu_baseline"] = {
                 "value": L / dt, "unit": "tokens/s", "cores": threads, "kind": kind,
+                "cpu": cpu_model(),
                 "sample": f"1 batch of {args.config} ({dim} x {L}): entropy + rule + fp64 "
                           f"Mamba-1 scan, {threads} threads, {dt:.2f} s"}
             if kind == "reference":
@@ -663,6 +710,69 @@ def producer_fusion_measure(torch, device, x, pf, reps=20):
                          "fixed range [-0.5, 4]")
     res["layer"] = layer
     del xin, u, out
+    return res
+
+
+def pipelined_measure(torch, device, x, pf, out_serial, steps, make):
+    """Steady-state throughput with two independent batches in flight: call i+1's entropy
+    (cl_entropy_lean_f32: lean kernels sized to share SMs with a scan CTA) on one stream
+    while call i's scan runs on another.  Every call still does all of its own work
+    (min/max, histogram, device decision, scan); outputs are checked against the serial
+    step bit for bit.  A separately labelled figure beside the single-call latency."""
+    import paper_2604_10597_b200 as cl
+    from paper_2604_10597_b200.mamba1 import Prefill
+    batch, dim, L = x["u"].shape
+    xb = make(1234 + 777)
+    sets = [x, xb]
+    outs = [torch.empty_like(x["u"]), torch.empty_like(x["u"])]
+    pfs = [Prefill(pf.spec, pf.policy, pf.bounds, pf.cal, device=device) for _ in range(2)]
+    s_ent, s_scan = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    ent_done = [torch.cuda.Event(), torch.cuda.Event()]
+    scan_done = [torch.cuda.Event(), torch.cuda.Event()]
+    scanned = [False, False]
+
+    def entropy(j):
+        with torch.cuda.stream(s_ent):
+            if scanned[j]:
+                s_ent.wait_event(scan_done[j])  # its buffers are read by that scan
+            pfs[j].stage_entropy_lean(sets[j]["u"].reshape(-1), L)
+            ent_done[j].record(s_ent)
+
+    def scan(j):
+        X = sets[j]
+        with torch.cuda.stream(s_scan):
+            s_scan.wait_event(ent_done[j])
+            pfs[j].stage_scan(X["u"], X["delta"], X["A"], X["B"], X["C"], X["D"], X["z"],
+                              X["delta_bias"], True, outs[j])
+            scan_done[j].record(s_scan)
+            scanned[j] = True
+
+    def run(n):
+        entropy(0)
+        for i in range(n):
+            if i + 1 < n:
+                entropy((i + 1) % 2)
+            scan(i % 2)
+
+    torch.cuda.synchronize()
+    run(4)  # warm-up
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(s_ent)
+    s_scan.wait_event(t0)
+    run(steps)
+    t1.record(s_scan)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    # the serial step's output for batch 0 (same inputs, same decision) -- bit for bit
+    same = bool(torch.equal(outs[0], out_serial))
+    same_dec = bool(torch.equal(pfs[0].decision_buf, pf.decision_buf))
+    res = {"ms_per_step": ms, "value": batch * L / (ms / 1e3), "unit": "tokens/s",
+           "steps": steps, "matches_serial_bitwise": same and same_dec,
+           "workload": "two independent batches in flight: entropy(i+1) [lean kernels, stream "
+                       "2] under scan(i) [stream 1]; every call's own min/max + histogram + "
+                       "device decision + scan"}
+    del xb, outs, sets
     return res
 
 

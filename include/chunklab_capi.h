@@ -197,6 +197,17 @@ int cl_histogram_decide_f32(cl_ctx* ctx, const float* d_values, uint64_t n,
                             const cl_rule_spec* rule, uint64_t seq_len, cl_decision* d_decision,
                             void* stream);
 
+/* The entropy stages of a single-GPU prefill (range init, min/max, histogram + decision;
+ * results identical to cl_prefill_init + cl_minmax_f32 + cl_histogram_decide_f32) in LEAN
+ * kernels: one CTA per SM of 4 warps, <= 64 registers per thread and ~66 KB of shared
+ * memory, fed by cp.async.bulk rings -- small enough to run on the same SMs as another
+ * call's scan.  For pipelined serving: call i+1's entropy on one stream while call i's
+ * MUFU-bound scan runs on another (the scan leaves about half of HBM idle).  Configurations
+ * other than Dynamic range, stride 1, K <= 256 use the regular kernels. */
+int cl_entropy_lean_f32(cl_ctx* ctx, const float* d_values, uint64_t n, const cl_hist_spec* spec,
+                        const cl_rule_spec* rule, uint64_t seq_len, uint64_t* d_counts,
+                        double* d_range, cl_decision* d_decision, void* stream);
+
 /* Stage 4: fused Mamba-1 selective scan (fp32), chunk read from d_decision.
  * Layouts (mamba_ssm selective_scan_fn): u, delta, z, out: (batch, dim, L)
  * row-major; A: (dim, N); B, C: (batch, N, L); D, delta_bias: (dim) or NULL;

@@ -133,6 +133,8 @@ SIGNATURES = {
     "cl_prefill_init": (C.c_int, [_P, _P, _P, C.c_int, _P]),
     "cl_histogram_f32": (C.c_int, [_P, _P, _u64, _u64, C.POINTER(cl_hist_spec), _P, _P, _P]),
     "cl_histogram_f64": (C.c_int, [_P, _P, _u64, _u64, C.POINTER(cl_hist_spec), _P, _P, _P]),
+    "cl_entropy_lean_f32": (C.c_int, [_P, _P, _u64, C.POINTER(cl_hist_spec),
+                                      C.POINTER(cl_rule_spec), _u64, _P, _P, _P, _P]),
     "cl_decide": (C.c_int, [_P, _P, _P, C.POINTER(cl_hist_spec), _u64, C.POINTER(cl_rule_spec),
                             _u64, _P, _P]),
     "cl_histogram_decide_f32": (C.c_int, [_P, _P, _u64, C.POINTER(cl_hist_spec), _P, _P,

@@ -412,6 +412,36 @@ int cl_histogram_decide_f32(cl_ctx* ctx, const float* d_values, uint64_t n,
                    seq_len, d_decision, stream);
 }
 
+int cl_entropy_lean_f32(cl_ctx* ctx, const float* d_values, uint64_t n, const cl_hist_spec* spec,
+                        const cl_rule_spec* rule, uint64_t seq_len, uint64_t* d_counts,
+                        double* d_range, cl_decision* d_decision, void* stream) {
+  int rc = validate_spec(ctx, spec);
+  if (rc) return rc;
+  if ((rc = validate_rule(ctx, rule))) return rc;
+  if (!d_values || !d_range || !d_counts || !d_decision)
+    return fail(ctx, CL_E_INVALID, "null argument");
+  if (n == 0) return fail(ctx, CL_E_INVALID, "no samples");
+  if ((rc = cl_prefill_init(ctx, d_range, d_counts, spec->bin_count, stream))) return rc;
+  cudaError_t e = cudaSuccess;
+  bool lean;
+  {
+    DeviceGuard g(ctx->device);
+    cl_workspace* w = workspace(ctx, static_cast<cudaStream_t>(stream));
+    if (!w) return CL_E_CUDA;
+    lean = launch_entropy_lean(d_values, n, *spec, *rule, seq_len, d_range, d_counts, d_decision,
+                               w->d_hist_ticket, ctx->num_sms, static_cast<cudaStream_t>(stream),
+                               &e);
+  }
+  if ((rc = check_launch(ctx, e, "entropy_lean"))) return rc;
+  if (lean) {
+    ctx->launches += 2;
+    return CL_OK;
+  }
+  if ((rc = cl_minmax_f32(ctx, d_values, n, 0, spec->sample_stride, d_range, stream))) return rc;
+  return cl_histogram_decide_f32(ctx, d_values, n, spec, d_range, d_counts, rule, seq_len,
+                                 d_decision, stream);
+}
+
 int cl_decide(cl_ctx* ctx, const uint64_t* d_counts, const double* d_range,
               const cl_hist_spec* spec, uint64_t n_samples_total, const cl_rule_spec* rule,
               uint64_t seq_len, cl_decision* d_decision, void* stream) {

@@ -158,6 +158,10 @@ cudaError_t launch_token_entropy(const unsigned int* d_counts, uint64_t length,
                                  cudaStream_t s);
 cudaError_t launch_entropy_from_masses(const double* d_masses, int k, double eps, double* d_out,
                                        cudaStream_t s);
+bool launch_entropy_lean(const float* v, uint64_t n, const cl_hist_spec& spec,
+                         const cl_rule_spec& rule, uint64_t seq_len, double* d_range,
+                         uint64_t* d_counts, cl_decision* d_out, unsigned long long* ticket,
+                         int num_sms, cudaStream_t s, cudaError_t* err);
 bool launch_conv_hist_fixed(const float* x, const float* w, const float* bias, float* u,
                             uint64_t batch, uint64_t dim, uint64_t L, int width, int silu,
                             const cl_hist_spec& spec, uint64_t* d_counts, double* d_range,

@@ -466,10 +466,11 @@ __device__ __forceinline__ uint64_t add_mod(uint64_t r, uint64_t d, uint64_t str
 // bank-exclusive layout): the exact bin of every sample, as bits 0x4B400000 + n of the
 // magic-number rounded affine map (near-edge samples re-binned exactly in fp64), then
 // pairwise in-order read-modify-writes of the lane's counters.
-__device__ __forceinline__ void lane_count_u8(const float (&val)[kLaneSamples], const BinParams& p,
+template <int NS>
+__device__ __forceinline__ void lane_count_u8(const float (&val)[NS], const BinParams& p,
                                             unsigned char* cblk, int warp, int lane) {
   // t bits carry the bin (0x4B400000 + n); near-edge samples get the exact bin's bits
-  uint32_t tb[kLaneSamples];
+  uint32_t tb[NS];
   bool any_slow = p.exact_only != 0;
 #if CL_HIST_X2
   // the same per-sample fp32 operations on sample pairs (FFMA2 / FADD2: every f32x2
@@ -478,7 +479,7 @@ __device__ __forceinline__ void lane_count_u8(const float (&val)[kLaneSamples], 
   const uint64_t mp = pack_f2(12582912.0f, 12582912.0f);
   const uint64_t mn = pack_f2(-12582912.0f, -12582912.0f);
 #pragma unroll
-  for (int e = 0; e < kLaneSamples; e += 2) {
+  for (int e = 0; e < NS; e += 2) {
     uint64_t x2, t2, r2, d2;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(x2) : "l"(pack_f2(val[e], val[e + 1])), "l"(s2), "l"(c2));
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t2) : "l"(x2), "l"(mp));
@@ -498,7 +499,7 @@ __device__ __forceinline__ void lane_count_u8(const float (&val)[kLaneSamples], 
   }
 #else
 #pragma unroll
-  for (int e = 0; e < kLaneSamples; ++e) {
+  for (int e = 0; e < NS; ++e) {
     const float x = fmaf(val[e], p.s_f, p.c_f);
     const float t = x + 12582912.0f;
     any_slow |= !(fabsf(x - (t - 12582912.0f)) <= p.thr);
@@ -510,7 +511,7 @@ __device__ __forceinline__ void lane_count_u8(const float (&val)[kLaneSamples], 
 #endif
   if (__any_sync(0xffffffffu, any_slow)) {
 #pragma unroll
-    for (int e = 0; e < kLaneSamples; ++e) {
+    for (int e = 0; e < NS; ++e) {
       bool sl;
       bin_fast<false>(val[e], p, &sl);
       if (sl || p.exact_only)
@@ -522,7 +523,7 @@ __device__ __forceinline__ void lane_count_u8(const float (&val)[kLaneSamples], 
   // and the loads / stores below are LDS/STS [R + UR(base)] with no add
   const uint32_t wl = static_cast<uint32_t>(warp) * (kLaneBins * 32) + lane * 4u;
 #pragma unroll
-  for (int g = 0; g < kLaneSamples / 2; ++g) {
+  for (int g = 0; g < NS / 2; ++g) {
     // plain accesses: the offsets may alias, so the compiler keeps this order
     const uint32_t o0 = cofs_from_tbits(tb[2 * g], wl);
     const uint32_t o1 = cofs_from_tbits(tb[2 * g + 1], wl);
@@ -914,14 +915,17 @@ __device__ void decide_block(const DecideArgs& a, cl_decision* d_out) {
     const double inv_n = __ddiv_rn(1.0, static_cast<double>(a.n_samples));
     double raw = 0.0;
     for (int base = 0; base < a.k; base += kThreads) {
-      const int b = base + threadIdx.x;
-      double t = 0.0;
-      if (threadIdx.x < kThreads && b < a.k) {
-        const unsigned long long cb = COHERENT ? __ldcg(a.counts + b) : a.counts[b];
-        const double pm = __dmul_rn(static_cast<double>(cb), inv_n);
-        if (pm > 0.0) t = __dmul_rn(pm, log(__dadd_rn(pm, a.epsilon)));
+      // any block size: threads stride over the kThreads term slots
+      for (int i = threadIdx.x; i < kThreads; i += blockDim.x) {
+        const int b = base + i;
+        double t = 0.0;
+        if (b < a.k) {
+          const unsigned long long cb = COHERENT ? __ldcg(a.counts + b) : a.counts[b];
+          const double pm = __dmul_rn(static_cast<double>(cb), inv_n);
+          if (pm > 0.0) t = __dmul_rn(pm, log(__dadd_rn(pm, a.epsilon)));
+        }
+        terms[i] = t;
       }
-      if (threadIdx.x < kThreads) terms[threadIdx.x] = t;
       __syncthreads();
       if (threadIdx.x == 0) {
         // raw -= p*log(p+eps) in bin order (entropy.hpp:154-156).  Empty bins hold +0.0
@@ -1205,6 +1209,166 @@ __global__ void __launch_bounds__(kCHWarps * 32)
   if (bad && lane == 0) range::atomic_max_f64(d_range + 2, 1.0);
 }
 
+// ---------------------------------------------------------------------------
+// Lean entropy kernels, for co-scheduling under another call's scan (the pipelined
+// prefill: call i+1's min/max + histogram run while call i's MUFU-bound scan leaves half of
+// HBM idle; bench.py "pipelined").  Sized to fit beside a resident scan CTA (448 threads x
+// 128 registers, ~149 KB of shared memory): 4 warps x <= 64 registers = 8192 registers
+// and ~66 KB of shared memory, one CTA per SM.  The loads in flight live in a
+// cp.async.bulk ring (kLeanStages x 4 KB) instead of registers; warp 0's lane 0 refills it.
+// Dynamic range, stride 1, K <= 256 (the calibrated rule's configuration); results equal
+// cl_minmax_f32 + cl_histogram_decide_f32 bit for bit.
+// ---------------------------------------------------------------------------
+constexpr int kLeanWarps = 4;
+constexpr int kLeanSamples = 8;                             // per lane per chunk
+constexpr int kLeanChunk = kLeanWarps * 32 * kLeanSamples;  // 1024 floats = 4 KB
+constexpr int kLeanStages = 8;
+constexpr size_t kLeanRing = size_t(kLeanStages) * kLeanChunk * 4;  // 32 KB
+constexpr size_t kLeanMmSmem = kLeanRing + 2 * kLeanStages * 8 + 128;
+constexpr size_t kLeanHistSmem =
+    size_t(kLeanWarps) * kLaneBins * kBinStride + kLeanRing + kLaneBins * 4 + 2 * kLeanStages * 8 + 128;
+constexpr int kLeanFlush = 240 / kLeanSamples;  // u8 counters: flush before 255
+
+// The ring: chunk i of this CTA (global chunk blockIdx.x + i * gridDim.x) in stage i % S.
+struct LeanRing {
+  float* buf;
+  uint64_t* full;
+  uint64_t* empty;
+  const float* body;
+  uint64_t n_chunks;
+  __device__ uint64_t chunk(uint64_t i) const { return blockIdx.x + i * gridDim.x; }
+  __device__ void issue(uint64_t i) {  // one thread
+    const uint64_t c = chunk(i);
+    if (c >= n_chunks) return;
+    const int st = static_cast<int>(i % kLeanStages);
+    if (i >= static_cast<uint64_t>(kLeanStages))
+      mbar_wait(empty + st, static_cast<uint32_t>((i / kLeanStages - 1) & 1));
+    mbar_expect_tx(full + st, kLeanChunk * 4);
+    bulk_g2s(buf + size_t(st) * kLeanChunk, body + c * kLeanChunk, kLeanChunk * 4, full + st);
+  }
+  __device__ const float* wait(uint64_t i) {
+    const int st = static_cast<int>(i % kLeanStages);
+    mbar_wait(full + st, static_cast<uint32_t>((i / kLeanStages) & 1));
+    return buf + size_t(st) * kLeanChunk;
+  }
+  __device__ void release(uint64_t i, int lane) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + static_cast<int>(i % kLeanStages));
+  }
+};
+
+__device__ __forceinline__ LeanRing lean_ring_setup(unsigned char* ring_base, const float* body,
+                                                    uint64_t n_chunks) {
+  LeanRing r;
+  r.buf = reinterpret_cast<float*>(ring_base);
+  r.full = reinterpret_cast<uint64_t*>(ring_base + kLeanRing);
+  r.empty = r.full + kLeanStages;
+  r.body = body;
+  r.n_chunks = n_chunks;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kLeanStages; ++i) {
+      mbar_init(r.full + i, 1);
+      mbar_init(r.empty + i, kLeanWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kLeanWarps * 32, 8)
+    minmax_lean_kernel(const float* __restrict__ v, uint64_t n, double* range) {
+  extern __shared__ __align__(128) unsigned char lsm[];
+  range::Acc acc;
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  const uint64_t head = umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
+  const float* body = v + head;
+  const uint64_t n_chunks = (n - head) / kLeanChunk;
+  const uint64_t tail0 = head + n_chunks * kLeanChunk;
+  if (blockIdx.x == 0) {
+    for (uint64_t i = threadIdx.x; i < head; i += blockDim.x) acc.visit(v[i], true);
+    for (uint64_t i = tail0 + threadIdx.x; i < n; i += blockDim.x) acc.visit(v[i], true);
+  }
+  LeanRing ring = lean_ring_setup(lsm, body, n_chunks);
+  const uint64_t mine = blockIdx.x < n_chunks ? (n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0)
+    for (uint64_t i = 0; i + 1 < kLeanStages && i < mine; ++i) ring.issue(i);
+  for (uint64_t i = 0; i < mine; ++i) {
+    if (threadIdx.x == 0) ring.issue(i + kLeanStages - 1);
+    const float4* c4 = reinterpret_cast<const float4*>(ring.wait(i));
+    const float4 a = c4[warp * 64 + lane], b = c4[warp * 64 + 32 + lane];
+    ring.release(i, lane);
+    acc.visit(a.x, true), acc.visit(a.y, true), acc.visit(a.z, true), acc.visit(a.w, true);
+    acc.visit(b.x, true), acc.visit(b.y, true), acc.visit(b.z, true), acc.visit(b.w, true);
+  }
+  range::commit<kLeanWarps * 32>(acc, range);
+}
+
+// (min 8 blocks per SM caps the registers at 65536 / (128 * 8) = 64)
+__global__ void __launch_bounds__(kLeanWarps * 32, 8)
+    hist_lean_kernel(const float* __restrict__ v, uint64_t n, int k,
+                     const double* __restrict__ d_range, unsigned long long* d_counts,
+                     DecideArgs da, cl_decision* d_out, unsigned long long* ticket) {
+  extern __shared__ __align__(128) unsigned char lsm[];
+  cnt_t* counters = reinterpret_cast<cnt_t*>(lsm);
+  uint32_t* cta_hist =
+      reinterpret_cast<uint32_t*>(lsm + size_t(kLeanWarps) * kLaneBins * kBinStride);
+  unsigned char* ring_base = reinterpret_cast<unsigned char*>(cta_hist + kLaneBins);
+  __shared__ BinParams sp;
+  __shared__ bool last;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) sp = make_bin_params(d_range, CL_RANGE_DYNAMIC, 0.0, 0.0, k);
+  {
+    uint4* c4 = reinterpret_cast<uint4*>(lsm);
+    for (int i = threadIdx.x; i < static_cast<int>(size_t(kLeanWarps) * kLaneBins * kBinStride / 16);
+         i += blockDim.x)
+      c4[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < kLaneBins; i += blockDim.x) cta_hist[i] = 0;
+  }
+  const uint64_t head = umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
+  const float* body = v + head;
+  const uint64_t n_chunks = (n - head) / kLeanChunk;
+  const uint64_t tail0 = head + n_chunks * kLeanChunk;
+  LeanRing ring = lean_ring_setup(ring_base, body, n_chunks);  // (its __syncthreads publishes sp)
+  const BinParams p = sp;
+  unsigned char* lane_base =
+      reinterpret_cast<unsigned char*>(counters + warp * kLaneBins * 32) + lane * 4;
+  if (blockIdx.x == 0 && warp == 0) {
+    for (uint64_t i = lane; i < head; i += 32) cref(lane_base, bin_f32(v[i], p, false)) += 1;
+    for (uint64_t i = tail0 + lane; i < n; i += 32) cref(lane_base, bin_f32(v[i], p, false)) += 1;
+    flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+  }
+  const uint64_t mine = blockIdx.x < n_chunks ? (n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0)
+    for (uint64_t i = 0; i + 1 < kLeanStages && i < mine; ++i) ring.issue(i);
+  int since = 0;
+  for (uint64_t i = 0; i < mine; ++i) {
+    if (threadIdx.x == 0) ring.issue(i + kLeanStages - 1);
+    const float4* c4 = reinterpret_cast<const float4*>(ring.wait(i));
+    const float4 a = c4[warp * 64 + lane], b = c4[warp * 64 + 32 + lane];
+    ring.release(i, lane);
+    const float val[kLeanSamples] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    lane_count_u8(val, p, reinterpret_cast<unsigned char*>(counters), warp, lane);
+    if (++since == kLeanFlush) {
+      flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+      since = 0;
+    }
+  }
+  flush_warp(counters + warp * kLaneBins * 32, cta_hist, lane, k);
+  __syncthreads();
+  for (int b = threadIdx.x; b < k; b += blockDim.x)
+    if (cta_hist[b]) atomicAdd(d_counts + b, static_cast<unsigned long long>(cta_hist[b]));
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1ull) == gridDim.x - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    decide_block<true>(da, d_out);
+    if (threadIdx.x == 0) *ticket = 0ull;
+  }
+}
+
 // K > 256 (or f64 input): shared-memory atomics on a CTA histogram.
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kThreads)
@@ -1481,6 +1645,14 @@ constexpr int kTokHMaxPerFlush = 65000;     // u16 counters: flush before overfl
 // lane 0.537 ms, TMA 0.670 ms -- the loop is instruction-bound (about 27 instructions per
 // sampled element: binning, the exact-path test, two u16 read-modify-writes), not load-bound,
 // and the TMA kernel's 8 consumer warps per SM issue them slower than the lane kernel's 12.
+// min/max CTAs per SM (8 x 256 threads: a C1-sized input is one batch of 4 float4 loads per
+// thread, all in flight at once) and the register-fed histogram's minimum chunks per warp
+#ifndef CL_MM_CTAS_PER_SM
+#define CL_MM_CTAS_PER_SM 4
+#endif
+#ifndef CL_HIST_MIN_CHUNKS
+#define CL_HIST_MIN_CHUNKS 1
+#endif
 #ifndef CL_TOK_TMA
 #define CL_TOK_TMA 0
 #endif
@@ -2014,7 +2186,11 @@ cudaError_t launch_prefill_init(double* d_range, uint64_t* d_counts, int k, cuda
 cudaError_t launch_minmax_f32(const float* v, uint64_t n, uint64_t g0, uint64_t stride,
                               double* d_range, int num_sms, cudaStream_t s, int* launches) {
   if (n == 0) return cudaSuccess;
-  const int grid = grid_for(n / 4 + 1, kThreads * 4, num_sms, 4);
+  static const int per_sm = [] {
+    const char* e = getenv("CL_MM_CTAS_PER_SM");
+    return e ? atoi(e) : CL_MM_CTAS_PER_SM;
+  }();
+  const int grid = grid_for(n / 4 + 1, kThreads * 4, num_sms, per_sm);
   switch (stride_mode(stride)) {
     case 0: minmax_f32_kernel<0><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range); break;
     case 1: minmax_f32_kernel<1><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range); break;
@@ -2084,7 +2260,14 @@ cudaError_t launch_histogram_f32(const float* v, uint64_t n, uint64_t g0,
     if (CL_HIST_REG && !fixed && mode == 0 && CL_HIST_U8) {
       const bool fz = fuse != nullptr && g0 == 0;
       const uint64_t wchunks = n / kRegChunk + 1;
-      const uint64_t gmax = (wchunks + kRegWarps - 1) / kRegWarps;
+      // small inputs: give every warp at least a few chunks -- each warp pays a full 8 KB
+      // counter flush (and each CTA 256 global atomics) however little it bins
+      static const uint64_t min_chunks = [] {
+        const char* e = getenv("CL_HIST_MIN_CHUNKS");
+        return e ? static_cast<uint64_t>(atoi(e)) : uint64_t(CL_HIST_MIN_CHUNKS);
+      }();
+      const uint64_t per_cta = uint64_t(kRegWarps) * (min_chunks < 1 ? 1 : min_chunks);
+      const uint64_t gmax = (wchunks + per_cta - 1) / per_cta;
       const int rgrid = static_cast<int>(gmax < static_cast<uint64_t>(num_sms) ? gmax : num_sms);
       DecideArgs da{};
       cl_decision* d_out = nullptr;
@@ -2203,6 +2386,35 @@ bool launch_conv_hist_fixed(const float* x, const float* w, const float* bias, f
     case 3: go(conv_hist_fixed_kernel<3>); break;
     default: go(conv_hist_fixed_kernel<4>); break;
   }
+  *err = cudaGetLastError();
+  return true;
+}
+
+// The lean (co-schedulable) min/max and histogram + decision, one CTA per SM; returns
+// false when the configuration is not the one they serve (the caller falls back).
+bool launch_entropy_lean(const float* v, uint64_t n, const cl_hist_spec& spec,
+                         const cl_rule_spec& rule, uint64_t seq_len, double* d_range,
+                         uint64_t* d_counts, cl_decision* d_out, unsigned long long* ticket,
+                         int num_sms, cudaStream_t s, cudaError_t* err) {
+  *err = cudaSuccess;
+  if (!CL_HIST_U8 || spec.range_mode != CL_RANGE_DYNAMIC || spec.sample_stride != 1 ||
+      spec.bin_count > kLaneBins || n < uint64_t(kLeanChunk) * 8)
+    return false;
+  const int grid = num_sms;
+  cudaFuncSetAttribute(minmax_lean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kLeanMmSmem));
+  cudaFuncSetAttribute(hist_lean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kLeanHistSmem));
+  cudaFuncSetAttribute(minmax_lean_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(hist_lean_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  minmax_lean_kernel<<<grid, kLeanWarps * 32, kLeanMmSmem, s>>>(v, n, d_range);
+  if ((*err = cudaGetLastError()) != cudaSuccess) return true;
+  const DecideArgs da = make_decide_args(d_counts, d_range, spec, n, rule, seq_len, nullptr);
+  hist_lean_kernel<<<grid, kLeanWarps * 32, kLeanHistSmem, s>>>(
+      v, n, spec.bin_count, d_range, reinterpret_cast<unsigned long long*>(d_counts), da, d_out,
+      ticket);
   *err = cudaGetLastError();
   return true;
 }

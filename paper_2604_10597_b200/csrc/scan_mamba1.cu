@@ -637,6 +637,10 @@ cudaError_t launch_ws(const CUtensorMap (&m)[6], const TmaArgs& t, int num_sms, 
                       1024 + size_t(WARPS) * STAGES * (16 + 8);
   cudaError_t e = set_smem(kern, smem);
   if (e != cudaSuccess) return e;
+  // keep the SM's shared-memory carveout at its maximum, so lean entropy kernels of
+  // another call (cl_entropy_lean_f32) can sit beside a scan CTA
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
   kern<<<grid_for(t.n_tiles, WARPS, num_sms), (WARPS + kProducers) * 32, smem, s>>>(
       m[0], m[1], m[2], m[4], t);
   return cudaGetLastError();

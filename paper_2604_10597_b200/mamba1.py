@@ -303,6 +303,14 @@ class Prefill:
                       C.byref(self.rule), int(seq_len), self.decision_buf.data_ptr(),
                       _stream_ptr(self.device))
 
+    def stage_entropy_lean(self, u_flat: torch.Tensor, seq_len: int):
+        """init + min/max + histogram + decision in the lean, co-schedulable kernels
+        (cl_entropy_lean_f32): for running this call's entropy under another call's scan."""
+        self.ctx.call("cl_entropy_lean_f32", u_flat.data_ptr(), u_flat.numel(), C.byref(self.cspec),
+                      C.byref(self.rule), int(seq_len), self.counts.data_ptr(),
+                      self.range.data_ptr(), self.decision_buf.data_ptr(),
+                      _stream_ptr(self.device))
+
     def stage_histogram_decide(self, u_flat: torch.Tensor, seq_len: int, zero: bool = True):
         """Single-GPU stages 2+3 in one launch (the histogram's last CTA decides);
         needs this call's stage_minmax (range_init) before it."""
