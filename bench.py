@@ -94,16 +94,38 @@ def algorithmic_bytes(batch, dim, L, N, stride=1):
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: an NVML polling thread
+    (a sample every ~2 ms, so even a 10 ms timed region of the few-row configs gets
+    samples), else `nvidia-smi -lms 20`.  summary() keeps the samples between mark("t_start")
+    and mark("t_stop")."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device_index=0):
         self.proc = None
-        self.lines = []
+        self.nvml = None
+        self.samples = []  # (time, sm_mhz, max_mhz, set of reasons)
         self.dev = device_index
+        self.stop = False
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.nvml = (pynvml, h, bits, mx)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.FIELDS,
@@ -115,14 +137,34 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        pynvml, h, bits, mx = self.nvml
+        while not self.stop:
+            try:
+                sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((time.time(), sm, mx, {n for n, b in bits.items() if r & b}))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append((time.time(), line.strip()))
+            parts = [p.strip() for p in line.strip().split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm, mx = float(parts[1]), float(parts[2])
+            except ValueError:
+                continue
+            reasons = {n for n, v in zip(self.NAMES, parts[5:9]) if v.lower().startswith("active")}
+            self.samples.append((time.time(), sm, mx, reasons))
 
     def mark(self, which):
         setattr(self, which, time.time())
 
     def __exit__(self, *a):
+        self.stop = True
         if self.proc:
             self.proc.terminate()
             try:
@@ -132,24 +174,16 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         t0, t1 = getattr(self, "t_start", 0.0), getattr(self, "t_stop", 1e30)
-        for ts, line in self.lines:
-            if not (t0 <= ts <= t1 + 0.05):
+        for ts, s_mhz, m_mhz, rs in list(self.samples):
+            if not (t0 <= ts <= t1 + 0.002):
                 continue
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
+            sm.append(s_mhz)
+            mx = m_mhz
+            reasons |= rs
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------- data
