@@ -401,7 +401,7 @@ def main():
                     ev[2].record()
                 ev[3].record()
         else:
-            pf.stage_init()
+            pf.stage_init((x["u"], x["delta"], x["A"], x["B"], x["C"]))
             pf.stage_minmax(uf, g0, init=False)
             if ev and fine:
                 ev[1].record()
@@ -443,6 +443,8 @@ def main():
         graphs = []
         captured0 = pf.ctx.launches
         with torch.cuda.stream(cap):
+            # (each graph has its own stream workspace, so the B / C re-layout stays in the
+            # scan's graph rather than being folded into the init launch)
             for stage in (lambda: (pf.stage_init(), pf.stage_minmax(uf, g0, init=False)),
                           lambda: pf.stage_histogram_decide(uf, L, zero=False),
                           lambda: pf.stage_scan(x["u"], x["delta"], x["A"], x["B"], x["C"],

@@ -250,6 +250,12 @@ int cl_selective_scan_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_deci
                           int fixed_chunk /* used when d_decision == NULL */, int variant,
                           void* stream);
 
+/* cl_prefill_init plus the scan's B / C re-layout for `scan_args` in the same launch: the
+ * next cl_selective_scan_f32 on this stream with the same B, C, batch and seq_len reuses it
+ * instead of launching its own transpose (B and C must not change in between). */
+int cl_prefill_init_prepare_f32(cl_ctx* ctx, double* d_range, uint64_t* d_counts, int bin_count,
+                                const cl_mamba1_args* scan_args, void* stream);
+
 /* Which kernel cl_selective_scan_f32 runs for these arguments and variant (host-only
  * query, no launch): kernel kind, its table row, TMA box (timesteps), consumer warps per
  * CTA, ring stages, and for the L-parallel kernel its shape-tied split (n_seg segments of

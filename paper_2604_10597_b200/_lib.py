@@ -131,6 +131,7 @@ SIGNATURES = {
                                 _u64, _P, _P]),
     "cl_counts_zero": (C.c_int, [_P, _P, C.c_int, _P]),
     "cl_prefill_init": (C.c_int, [_P, _P, _P, C.c_int, _P]),
+    "cl_prefill_init_prepare_f32": (C.c_int, [_P, _P, _P, C.c_int, C.POINTER(cl_mamba1_args), _P]),
     "cl_histogram_f32": (C.c_int, [_P, _P, _u64, _u64, C.POINTER(cl_hist_spec), _P, _P, _P]),
     "cl_histogram_f64": (C.c_int, [_P, _P, _u64, _u64, C.POINTER(cl_hist_spec), _P, _P, _P]),
     "cl_entropy_lean_f32": (C.c_int, [_P, _P, _u64, C.POINTER(cl_hist_spec),

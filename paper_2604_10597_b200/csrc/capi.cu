@@ -25,6 +25,14 @@ int fail(cl_ctx*, int code, const std::string& msg) {
 
 const std::string& thread_error() { return g_error; }
 
+int zero_now(cl_ctx* ctx, void* p, size_t bytes) {
+  std::lock_guard<std::recursive_mutex> lk(ctx->host_mu);  // own_stream is the host path's
+  CaptureRelaxed relax;
+  cudaError_t e = cudaMemsetAsync(p, 0, bytes, ctx->own_stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->own_stream);
+  return e == cudaSuccess ? CL_OK : cuda_fail(ctx, e, "zero scratch");
+}
+
 cl_workspace* workspace(cl_ctx* ctx, cudaStream_t stream) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   unsigned long long capture_id = 0;
@@ -43,14 +51,20 @@ cl_workspace* workspace(cl_ctx* ctx, cudaStream_t stream) {
   {
     CaptureRelaxed relax;
     e = cudaMalloc(&w->d_hist_ticket, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&w->d_epoch, 4 * sizeof(unsigned int));
   }
-  // stream-ordered zero (recorded into the graph when capturing)
-  if (e == cudaSuccess)
-    e = cudaMemsetAsync(w->d_hist_ticket, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) {
     cudaFree(w->d_hist_ticket);
+    cudaFree(w->d_epoch);
     delete w;
     cuda_fail(ctx, e, "cudaMalloc(stream workspace)");
+    return nullptr;
+  }
+  if (zero_now(ctx, w->d_hist_ticket, sizeof(unsigned long long)) ||
+      zero_now(ctx, w->d_epoch, 4 * sizeof(unsigned int))) {
+    cudaFree(w->d_hist_ticket);
+    cudaFree(w->d_epoch);
+    delete w;
     return nullptr;
   }
   ctx->ws.emplace(key, w);
@@ -65,6 +79,7 @@ void free_workspace(cl_workspace* w) {
   cudaFree(w->d_bct);
   cudaFree(w->d_agg);
   cudaFree(w->d_hist_ticket);
+  cudaFree(w->d_epoch);
   cudaFree(w->d_token_raw);
   cudaFree(w->d_token_range);
   cudaFree(w->d_token_counts);
@@ -352,6 +367,18 @@ int cl_prefill_init(cl_ctx* ctx, double* d_range, uint64_t* d_counts, int bin_co
                       launch_prefill_init(d_range, d_counts, bin_count,
                                           static_cast<cudaStream_t>(stream)),
                       "prefill_init");
+}
+
+int cl_prefill_init_prepare_f32(cl_ctx* ctx, double* d_range, uint64_t* d_counts, int bin_count,
+                                const cl_mamba1_args* a, void* stream) {
+  if (!ctx || !d_range || !d_counts || bin_count < 1 || !a)
+    return fail(ctx, CL_E_INVALID, "null argument");
+  if (a->batch == 0 || a->dim == 0 || a->seq_len == 0 || a->d_state == 0)
+    return fail(ctx, CL_E_INVALID, "shape mismatch");
+  if (!a->B || !a->C) return fail(ctx, CL_E_INVALID, "null argument");
+  DeviceGuard g(ctx->device);
+  return scan_prepare_with_init(ctx, *a, d_range, d_counts, bin_count,
+                                static_cast<cudaStream_t>(stream));
 }
 
 int cl_histogram_f32(cl_ctx* ctx, const float* d_values, uint64_t n, uint64_t global_offset,
@@ -664,7 +691,8 @@ int cl_prefill_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_hist_spec* 
       return rc;
     return cl_selective_scan_f32(ctx, args, d_decision, 0, CL_SCAN_AUTO, stream);
   }
-  if ((rc = cl_prefill_init(ctx, d_range, d_counts, spec->bin_count, stream))) return rc;
+  if ((rc = cl_prefill_init_prepare_f32(ctx, d_range, d_counts, spec->bin_count, args, stream)))
+    return rc;
   if ((rc = cl_minmax_f32(ctx, args->u, n, 0, spec->sample_stride, d_range, stream))) return rc;
   if ((rc = cl_histogram_decide_f32(ctx, args->u, n, spec, d_range, d_counts, rule,
                                      args->seq_len, d_decision, stream)))
@@ -694,7 +722,8 @@ int cl_prefill_from_conv_f32(cl_ctx* ctx, const cl_conv_args* conv, const cl_mam
       return rc;
     return cl_prefill_f32(ctx, args, spec, rule, d_counts, d_range, d_decision, stream);
   }
-  if ((rc = cl_prefill_init(ctx, d_range, d_counts, spec->bin_count, stream))) return rc;
+  if ((rc = cl_prefill_init_prepare_f32(ctx, d_range, d_counts, spec->bin_count, args, stream)))
+    return rc;
   if (spec->range_mode == CL_RANGE_FIXED) {
     cudaError_t e = cudaSuccess;
     bool fused;

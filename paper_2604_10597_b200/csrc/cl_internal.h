@@ -30,6 +30,13 @@ struct cl_workspace {
   unsigned int carry_epoch = 0;
   float* d_bct = nullptr;  // B^T / C^T (b, L, N) for the TMA scan (grown on demand)
   size_t bct_bytes = 0;
+  // d_bct already holds the interleaved [B | C] re-layout of these inputs, written by
+  // cl_prefill_init_prepare_f32 earlier on this stream; the next scan with the same B, C,
+  // batch and L consumes it (and clears it) instead of launching its own transpose
+  bool bct_ready = false;
+  const float* bct_B = nullptr;
+  const float* bct_C = nullptr;
+  uint64_t bct_batch = 0, bct_L = 0;
   // L-parallel scan: per-(tile, segment) aggregates {tag, h~_end[16], sum dt} words
   unsigned long long* d_agg = nullptr;
   size_t agg_bytes = 0;
@@ -37,6 +44,11 @@ struct cl_workspace {
   // arrival ticket of the fused histogram -> decision launch: 0 between launches (the
   // last CTA resets it), never visible to callers
   unsigned long long* d_hist_ticket = nullptr;
+  // captured workspaces: a device-side epoch parity per tag scheme ([0] chained carry,
+  // [1] L-parallel aggregates), flipped by each launch's last work claimer, so a graph's
+  // replays alternate between two tag bases (0x80000000 / 0xC0000000) and never need an
+  // in-graph memset of the tagged words
+  unsigned int* d_epoch = nullptr;
   // created inside a CUDA-graph capture: its buffers are baked into that graph, which
   // may replay many times, so per-launch state (tagged-carry epochs) is reset in-graph
   bool captured = false;
@@ -79,6 +91,14 @@ constexpr int kMaxBinsScratch = 1 << 16;
 int fail(cl_ctx* ctx, int code, const std::string& msg);
 int cuda_fail(cl_ctx* ctx, cudaError_t e, const char* where);
 const std::string& thread_error();
+
+// Zero a freshly allocated device buffer right now, outside any stream capture (on the
+// context's own stream, synchronised), so graphs never replay an initialisation memset.
+int zero_now(cl_ctx* ctx, void* p, size_t bytes);
+
+// Zero a freshly allocated device buffer right now, outside any stream capture (on the
+// context's own stream, synchronised), so graphs never replay an initialisation memset.
+int zero_now(cl_ctx* ctx, void* p, size_t bytes);
 
 // The workspace of `stream` (created on first use); nullptr + error on allocation failure.
 // Inside a stream capture each capture gets its own workspace (keyed by capture id).
@@ -179,5 +199,7 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
                 int fixed_chunk, int variant, cudaStream_t s);
 int state_update_f32(cl_ctx* ctx, const cl_state_update_args& a, cudaStream_t s);
 int scan_plan(cl_ctx* ctx, const cl_mamba1_args& a, int variant, cl_scan_plan* p);
+int scan_prepare_with_init(cl_ctx* ctx, const cl_mamba1_args& a, double* d_range,
+                           uint64_t* d_counts, int bin_count, cudaStream_t s);
 
 }  // namespace cl

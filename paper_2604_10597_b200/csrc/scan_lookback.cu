@@ -42,7 +42,8 @@ struct LbArgs {
   float* out;
   float* h_last;
   unsigned long long* agg;  // [n_tiles][n_seg][16 rows][kAggWords]
-  unsigned int epoch;       // tag of this launch's aggregate words
+  unsigned int epoch;       // tag of this launch's aggregate words (eager)
+  unsigned int* epoch_parity;  // captured graphs: the device-side parity (launch_epoch)
   int stage_params;
   unsigned int* ticket;
   uint64_t batch, dim, L;
@@ -196,7 +197,7 @@ __device__ __forceinline__ void fold_batch(const unsigned long long* base, int j
     ld_relaxed_u64x2(w64 + 16, ws[b][0], ws[b][1]);
   };
   auto ready = [&](int b) {
-    CL_DCHECK((ws[b][0] >> 32) <= epoch);
+    CL_DCHECK(epoch >= kGraphEpochA || (ws[b][0] >> 32) <= epoch);
     bool ok = (ws[b][0] >> 32) == epoch;
 #pragma unroll
     for (int i = 0; i < kN / 2; ++i) ok &= (w[b][i] >> 32) == epoch;
@@ -338,7 +339,8 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     // only producers claim tickets: the last producer warp of the grid to finish returns
     // the ticket to 0, so the next launch on this stream needs no memset
     ticket_retire(a.ticket, gridDim.x * NPROD, lane,
-                  static_cast<unsigned>(n_items) + gridDim.x * static_cast<unsigned>(WARPS));
+                  static_cast<unsigned>(n_items) + gridDim.x * static_cast<unsigned>(WARPS),
+                  a.epoch_parity);
     return;
   }
 
@@ -354,7 +356,8 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
   LbItem cur{};
   int row = 0;
   bool row_valid = false;
-  const unsigned long long tag = static_cast<unsigned long long>(a.epoch) << 32;
+  const unsigned epoch = launch_epoch(a.epoch, a.epoch_parity);
+  const unsigned long long tag = static_cast<unsigned long long>(epoch) << 32;
   for (int iter = 0;; ++iter) {
     const int slot = iter % STAGES;
     mbar_wait(wfull + slot, (iter / STAGES) & 1);
@@ -437,8 +440,8 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
           a.agg + (size_t(cur.tile) * n_seg * kRowsP + r) * kAggWords;
       int j = 0;
       for (; j + kFoldBatch <= cur.seg; j += kFoldBatch)
-        fold_batch<kFoldBatch>(tb, j, r, hf, a.epoch, A2p, h);
-      for (; j < cur.seg; ++j) fold_batch<1>(tb, j, r, hf, a.epoch, A2p, h);
+        fold_batch<kFoldBatch>(tb, j, r, hf, epoch, A2p, h);
+      for (; j < cur.seg; ++j) fold_batch<1>(tb, j, r, hf, epoch, A2p, h);
 #pragma unroll
       for (int i = 0; i < kP; ++i) h2[i] = h[i];
     }
@@ -508,6 +511,7 @@ cudaError_t launch_lookback(int cfg, bool sp, bool hz, const CUtensorMap* maps,
   t.h_last = p.h_last;
   t.agg = p.agg;
   t.epoch = p.epoch;
+  t.epoch_parity = p.epoch_parity;
   t.stage_params = p.stage_params;
   t.ticket = p.ticket;
   t.batch = p.batch;

@@ -424,7 +424,8 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     // only producers claim tickets: the last producer warp of the grid to finish returns
     // the ticket to 0, so the next launch on this stream needs no memset
     ticket_retire(a.ticket, gridDim.x * NPROD, lane,
-                  static_cast<unsigned>(n_items) + gridDim.x * static_cast<unsigned>(WARPS));
+                  static_cast<unsigned>(n_items) + gridDim.x * static_cast<unsigned>(WARPS),
+                  a.epoch_parity);
     return;
   }
 
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
   uint64_t* wempty = empty + warp * STAGES;
   const int2* wmeta = meta + warp * STAGES;
   constexpr int kP = kN / 4;
+  const unsigned epoch = launch_epoch(a.epoch, a.epoch_parity);
   f2_t h2[kP], A2p[kP];
   float bias = 0.f, Dc = 0.f;
   Item cur{};
@@ -493,7 +495,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
         // (the writer's release would also wait for all of its y stores to land)
         const unsigned long long* w64 =
             a.tcarry + (size_t(cur.tile) * kRowsP + r) * kN + 8 * hf;
-        const unsigned want = a.epoch + static_cast<unsigned>(cur.seg);
+        const unsigned want = epoch + static_cast<unsigned>(cur.seg);
         unsigned long long w[kN / 2];
         for (;;) {
           bool ok = true;
@@ -502,8 +504,8 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
             ld_relaxed_u64x2(w64 + i, w[i], w[i + 1]);
             ok &= static_cast<unsigned>(w[i] >> 32) == want;
             ok &= static_cast<unsigned>(w[i + 1] >> 32) == want;
-            // tags only grow: a newer tag than this launch's would be a stale-epoch bug
-            CL_DCHECK(static_cast<unsigned>(w[i] >> 32) <= want);
+            // eager tags only grow: a newer tag than this launch's would be a stale-epoch bug
+            CL_DCHECK(a.epoch_parity || static_cast<unsigned>(w[i] >> 32) <= want);
           }
           if (__all_sync(0xffffffffu, ok)) break;
           __nanosleep(64);
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
       } else {
         unsigned long long* w64 = a.tcarry + (size_t(cur.tile) * kRowsP + r) * kN + 8 * hf;
         const unsigned long long tag =
-            static_cast<unsigned long long>(a.epoch + static_cast<unsigned>(cur.seg + 1)) << 32;
+            static_cast<unsigned long long>(epoch + static_cast<unsigned>(cur.seg + 1)) << 32;
 #pragma unroll
         for (int i = 0; i < kN / 2; i += 2)
           st_relaxed_u64x2(w64 + i, tag | __float_as_uint(hs[i]), tag | __float_as_uint(hs[i + 1]));
@@ -571,6 +573,45 @@ __global__ void __launch_bounds__(256) transpose_bc_kernel(const float* __restri
   }
 }
 
+
+// The prefill's first launch when the scan's B / C re-layout is folded into it: blocks
+// with blockIdx.z < 2 transpose B (z = 0) and C (z = 1) exactly as transpose_bc_kernel,
+// block (0, 0, 2) initialises the entropy range {-inf, -inf, 0, 0} and zeroes the K counts
+// (cl_prefill_init).  One launch instead of two, and the transpose leaves the scan.
+__global__ void __launch_bounds__(256) init_transpose_kernel(const float* __restrict__ B,
+                                                             const float* __restrict__ C,
+                                                             float* __restrict__ Bt,
+                                                             float* __restrict__ Ct, int L,
+                                                             int row_stride, double* range,
+                                                             unsigned long long* counts, int k) {
+  if (blockIdx.z == 2) {
+    if (blockIdx.x != 0 || blockIdx.y != 0) return;
+    if (threadIdx.x == 0) {
+      range[0] = -INFINITY;
+      range[1] = -INFINITY;
+      range[2] = 0.0;
+      range[3] = 0.0;
+    }
+    for (int b = threadIdx.x; b < k; b += blockDim.x) counts[b] = 0ull;
+    return;
+  }
+  __shared__ float tile[kN][33];
+  const float* src = blockIdx.z ? C : B;
+  float* dst = blockIdx.z ? Ct : Bt;
+  if (!dst) return;  // init only (no TMA scan to feed)
+  const int b = blockIdx.y, t0 = blockIdx.x * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  for (int s = ty; s < kN; s += 8) {
+    const int t = t0 + tx;
+    tile[s][tx] = t < L ? src[(size_t(b) * kN + s) * L + t] : 0.f;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * kN; e += 256) {
+    const int tt = e / kN, s2 = e % kN;
+    const int t = t0 + tt;
+    if (t < L) dst[(size_t(b) * L + t) * row_stride + s2] = tile[s2][tt];
+  }
+}
 
 // ---- kernel table (CL_SCAN_CFG=<index> selects a row, for experiments) ----
 enum ScanKind { kWarpSpecPair = 0, kRowSeq = 1, kWarpSpecPairNoPipe = 2 };
@@ -843,6 +884,39 @@ int scan_plan(cl_ctx* ctx, const cl_mamba1_args& a, int variant, cl_scan_plan* p
   return CL_OK;
 }
 
+int scan_prepare_with_init(cl_ctx* ctx, const cl_mamba1_args& a, double* d_range,
+                           uint64_t* d_counts, int bin_count, cudaStream_t s) {
+  Selection sel;
+  const char* err = select_kernel(a, ctx->num_sms, CL_SCAN_AUTO, &sel);
+  if (err) return fail(ctx, CL_E_INVALID, err);
+  cl_workspace* w = workspace(ctx, s);
+  if (!w) return CL_E_CUDA;
+  const uint64_t L = a.seq_len, Bt = a.batch;
+  const bool ws = sel.tma && sel.cfg.kind != kRowSeq;
+  int rc = CL_OK;
+  if (ws)
+    rc = grow_scratch(ctx, w, &w->d_bct, &w->bct_bytes, 2 * size_t(Bt) * L * kN * sizeof(float),
+                      "cudaMalloc(B/C transpose)");
+  if (rc) return rc;
+  // without a TMA scan to feed, only the init block runs (grid z = 2 alone)
+  const dim3 grid(ws ? static_cast<unsigned>((L + 31) / 32) : 1u, ws ? static_cast<unsigned>(Bt) : 1u,
+                  3);
+  init_transpose_kernel<<<grid, 256, 0, s>>>(a.B, a.C, ws ? w->d_bct : nullptr,
+                                             ws ? w->d_bct + kN : nullptr, static_cast<int>(L),
+                                             2 * kN, d_range,
+                                             reinterpret_cast<unsigned long long*>(d_counts),
+                                             bin_count);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "init_transpose_kernel launch");
+  ++ctx->launches;
+  w->bct_ready = ws;
+  w->bct_B = a.B;
+  w->bct_C = a.C;
+  w->bct_batch = Bt;
+  w->bct_L = L;
+  return CL_OK;
+}
+
 int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decision,
                 int fixed_chunk, int variant, cudaStream_t s) {
   Selection sel;
@@ -879,12 +953,15 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       const bool fresh = w->agg_bytes < agg_bytes;
       rc = grow_scratch(ctx, w, &w->d_agg, &w->agg_bytes, agg_bytes, "cudaMalloc(scan aggregates)");
       if (rc) return rc;
-      if (fresh || w->captured || w->agg_epoch == 0 || w->agg_epoch == 0xFFFFFFFFu) {
-        cudaError_t e = cudaMemsetAsync(w->d_agg, 0, w->captured ? agg_bytes : w->agg_bytes, s);
+      if (fresh) {
+        if ((rc = zero_now(ctx, w->d_agg, w->agg_bytes))) return rc;
+        w->agg_epoch = 1;
+      } else if (!w->captured && (w->agg_epoch == 0 || w->agg_epoch >= 0x7FFFFFFFu)) {
+        cudaError_t e = cudaMemsetAsync(w->d_agg, 0, w->agg_bytes, s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(scan aggregates)");
         w->agg_epoch = 1;
       }
-      epoch = w->agg_epoch++;
+      epoch = w->captured ? 0u : w->agg_epoch++;
     } else if (ws) {
       // tagged carry words: zeroed when (re)allocated or when the epoch would wrap; each
       // launch takes tags epoch + 1 .. epoch + (segments <= boxes), above every older tag
@@ -893,15 +970,18 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       rc = grow_scratch(ctx, w, &w->d_tcarry, &w->tcarry_bytes, tcarry_bytes, "cudaMalloc(tagged carry)");
       if (rc) return rc;
       const unsigned span = static_cast<unsigned>((L + cfg.box - 1) / cfg.box) + 2u;
-      // in a captured graph the epoch is baked into every replay: zero the words in-graph
-      // before each launch instead (a replay must never see its predecessor's tags)
-      if (fresh || w->captured || w->carry_epoch == 0 || w->carry_epoch > 0xFFFFFFFFu - span) {
-        cudaError_t e = cudaMemsetAsync(w->d_tcarry, 0, w->captured ? tcarry_bytes : w->tcarry_bytes, s);
+      // eager: host epochs below 0x80000000; a captured graph takes its tag base from the
+      // device-side parity instead (launch_epoch), so its replays need no memset
+      if (fresh) {
+        if ((rc = zero_now(ctx, w->d_tcarry, w->tcarry_bytes))) return rc;
+        w->carry_epoch = 1;
+      } else if (!w->captured && (w->carry_epoch == 0 || w->carry_epoch > 0x7FFFFFFFu - span)) {
+        cudaError_t e = cudaMemsetAsync(w->d_tcarry, 0, w->tcarry_bytes, s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(tagged carry)");
         w->carry_epoch = 1;
       }
-      epoch = w->carry_epoch;
-      w->carry_epoch += span;
+      epoch = w->captured ? 0u : w->carry_epoch;
+      if (!w->captured) w->carry_epoch += span;
     }
     // B^T / C^T: interleaved per timestep ([B | C], 128 B rows, one TMA box) for the
     // warp-specialised kernel, two separate (b, L, 16) arrays for the row kernel
@@ -923,16 +1003,23 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     // the warp-specialised kernels return their ticket to 0 themselves (ticket_retire);
     // the row kernel's per-tile flags are zeroed every launch
     cudaError_t e = cudaSuccess;
-    if (!ws || fresh_work || w->captured || w->ticket_dirty)
-      e = cudaMemsetAsync(w->d_work, 0, work_bytes, s);
+    if (fresh_work) {
+      if ((rc = zero_now(ctx, w->d_work, w->work_bytes))) return rc;
+    }
+    if (!ws || w->ticket_dirty) e = cudaMemsetAsync(w->d_work, 0, work_bytes, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(scan work)");
     w->ticket_dirty = !ws;  // the row kernel leaves its ticket and flags behind
-    const dim3 tgrid(static_cast<unsigned>((L + 31) / 32), static_cast<unsigned>(Bt), 2);
-    transpose_bc_kernel<<<tgrid, 256, 0, s>>>(a.B, a.C, d_Bt, d_Ct, static_cast<int>(L),
-                                              ws ? 2 * kN : kN);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "transpose_bc_kernel launch");
-    ++ctx->launches;
+    const bool prepared = ws && w->bct_ready && w->bct_B == a.B && w->bct_C == a.C &&
+                          w->bct_batch == Bt && w->bct_L == L;
+    w->bct_ready = false;  // consumed (or stale) either way
+    if (!prepared) {
+      const dim3 tgrid(static_cast<unsigned>((L + 31) / 32), static_cast<unsigned>(Bt), 2);
+      transpose_bc_kernel<<<tgrid, 256, 0, s>>>(a.B, a.C, d_Bt, d_Ct, static_cast<int>(L),
+                                                ws ? 2 * kN : kN);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "transpose_bc_kernel launch");
+      ++ctx->launches;
+    }
     TmaArgs t{};
     t.out = a.out;
     t.A = a.A;
@@ -943,6 +1030,7 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     t.carry = w->d_carry;
     t.tcarry = w->d_tcarry;
     t.epoch = epoch;
+    t.epoch_parity = w->captured ? w->d_epoch : nullptr;
     t.stage_params = aligned16(a.A) && (!a.delta_bias || aligned16(a.delta_bias)) &&
                      (!a.D || aligned16(a.D));
     t.ticket = w->d_work;
@@ -966,6 +1054,7 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       p.h_last = a.h_last;
       p.agg = w->d_agg;
       p.epoch = epoch;
+      p.epoch_parity = w->captured ? w->d_epoch + 1 : nullptr;
       p.stage_params = t.stage_params;
       p.ticket = w->d_work;
       p.batch = Bt;

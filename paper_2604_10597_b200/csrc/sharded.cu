@@ -175,7 +175,8 @@ int cl_prefill_sharded_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_sha
       return rc;
     return cl_selective_scan_f32(ctx, args, d_decision, 0, CL_SCAN_AUTO, stream);
   }
-  if ((rc = cl_prefill_init(ctx, d_range, d_counts, spec->bin_count, stream))) return rc;
+  if ((rc = cl_prefill_init_prepare_f32(ctx, d_range, d_counts, spec->bin_count, args, stream)))
+    return rc;
   for (const Segment& s : segs)
     if ((rc = cl_minmax_f32(ctx, u + s.local_offset, s.numel, s.global_offset,
                             spec->sample_stride, d_range, stream)))

@@ -265,10 +265,21 @@ class Prefill:
         self.token_buf = torch.zeros(4, dtype=torch.float64, device=self.device)
 
     # -- stages (exposed for the sharded path and for per-stage timing) --
-    def stage_init(self):
-        """range_init + counts zero in one launch (cl_prefill_init)."""
-        self.ctx.call("cl_prefill_init", self.range.data_ptr(), self.counts.data_ptr(),
-                      int(self.spec.bin_count), _stream_ptr(self.device))
+    def stage_init(self, scan_inputs=None):
+        """range_init + counts zero in one launch (cl_prefill_init); with scan_inputs
+        (u, delta, A, B, C) the same launch also re-lays B / C for the following scan
+        (cl_prefill_init_prepare_f32)."""
+        if scan_inputs is None:
+            self.ctx.call("cl_prefill_init", self.range.data_ptr(), self.counts.data_ptr(),
+                          int(self.spec.bin_count), _stream_ptr(self.device))
+            return
+        u, delta, A, B, C_ = scan_inputs
+        a = _lib.cl_mamba1_args()
+        a.u, a.delta, a.A, a.B, a.C = u.data_ptr(), delta.data_ptr(), A.data_ptr(), B.data_ptr(), \
+            C_.data_ptr()
+        a.batch, a.dim, a.seq_len, a.d_state = u.shape[0], u.shape[1], u.shape[2], A.shape[1]
+        self.ctx.call("cl_prefill_init_prepare_f32", self.range.data_ptr(), self.counts.data_ptr(),
+                      int(self.spec.bin_count), C.byref(a), _stream_ptr(self.device))
 
     def stage_minmax(self, u_flat: torch.Tensor, global_offset: int = 0, init: bool = True):
         s = _stream_ptr(self.device)
@@ -346,7 +357,7 @@ class Prefill:
             self.stage_decide_token(u.shape[-1])
         else:
             uf = u.reshape(-1)
-            self.stage_init()
+            self.stage_init((u, delta, A, B, C))
             self.stage_minmax(uf, init=False)
             self.stage_histogram_decide(uf, u.shape[-1], zero=False)
         res = self.stage_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, out,
