@@ -1640,11 +1640,12 @@ constexpr int kTokMmRows = CL_TOK_MM_ROWS;  // min/max: channel rows per batch
 constexpr int kTokMmCols = CL_TOK_MM_COLS;  // min/max: 128-position slices per block tile
 constexpr int kTokHUnroll = CL_TOK_H_UNROLL;  // hist: channel rows per batch (2 in flight)
 constexpr int kTokHMaxPerFlush = 65000;     // u16 counters: flush before overflow
-// Token histogram kernel: the LDG-fed lane kernel (default) or the TMA-fed one
-// (CL_TOK_TMA=1).  Measured at C3 (channels 32768, L 8192, K 256; profiles/r2f_token_ab.txt):
-// lane 0.537 ms, TMA 0.670 ms -- the loop is instruction-bound (about 27 instructions per
-// sampled element: binning, the exact-path test, two u16 read-modify-writes), not load-bound,
-// and the TMA kernel's 8 consumer warps per SM issue them slower than the lane kernel's 12.
+// Token histogram kernel: the TMA-fed one (default, CL_TOK_TMA=1) or the LDG-fed lane
+// kernel (CL_TOK_TMA=0).  Measured at C3 (channels 32768, L 8192, K 256;
+// profiles/r2f_token_ab.txt): lane 0.537 ms; TMA first version 0.670 ms (ALU-bound: 64% of the
+// ALU pipe, 42 instructions per 32-sample step -- per-row sampling masks, pair-layout
+// addressing); with the stride-1 mask computed once, [bin][lane] addressing and constant
+// increments for full boxes: below.
 // min/max CTAs per SM (8 x 256 threads: a C1-sized input is one batch of 4 float4 loads per
 // thread, all in flight at once) and the register-fed histogram's minimum chunks per warp
 #ifndef CL_MM_CTAS_PER_SM
@@ -1654,7 +1655,7 @@ constexpr int kTokHMaxPerFlush = 65000;     // u16 counters: flush before overfl
 #define CL_HIST_MIN_CHUNKS 1
 #endif
 #ifndef CL_TOK_TMA
-#define CL_TOK_TMA 0
+#define CL_TOK_TMA 1
 #endif
 
 __device__ __forceinline__ void tok_item_split(uint64_t item, uint64_t tiles, uint64_t splits,
@@ -1937,7 +1938,7 @@ __global__ void __launch_bounds__((kTokTWarps + 1) * 32) token_hist_tma_kernel(
     const double* trange, double fixed_lo, double fixed_hi, unsigned int* counts) {
   extern __shared__ __align__(128) unsigned char tsm[];
   unsigned char* base = tsm + ((1024u - (smem_u32(tsm) & 1023u)) & 1023u);
-  uint16_t* tcnt = reinterpret_cast<uint16_t*>(base);  // [warp][128 bin pairs][32 lanes][2]
+  uint16_t* tcnt = reinterpret_cast<uint16_t*>(base);  // [warp][256 bins][32 lanes]
   unsigned char* ring = base + size_t(kTokTWarps) * 256 * 32 * 2;
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(kTokStages) * kTokBoxBytes);
   uint64_t* empty = full + kTokStages;
@@ -1978,7 +1979,7 @@ __global__ void __launch_bounds__((kTokTWarps + 1) * 32) token_hist_tma_kernel(
     return;
   }
   // ---------------- consumers ----------------
-  const uint32_t cbase = smem_u32(tcnt) + static_cast<uint32_t>(warp) * (256 * 32 * 2) + lane * 4u;
+  const uint32_t cbase = smem_u32(tcnt) + static_cast<uint32_t>(warp) * (256 * 32 * 2) + lane * 2u;
   uint32_t it = 0;
   for (uint64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
     const uint64_t tile = item % tiles, c0 = (item / tiles) * per_split;
@@ -1997,40 +1998,66 @@ __global__ void __launch_bounds__((kTokTWarps + 1) * 32) token_hist_tma_kernel(
       const float* box = reinterpret_cast<const float*>(ring + size_t(st) * kTokBoxBytes);
       const int rows = static_cast<int>(umin64(kTokBoxRows, c1 - c));
       float x[kTokBoxRows];
-      uint32_t smp = 0;  // bit r: row r is sampled
 #pragma unroll
-      for (int r = 0; r < kTokBoxRows; ++r) {
-        x[r] = box[r * 128 + warp * 32 + lane];
-        const bool ok = r < rows && cm == 0;
-        smp |= (ok ? 1u : 0u) << r;
-        if (++cm == a.stride) cm = 0;
-      }
+      for (int r = 0; r < kTokBoxRows; ++r) x[r] = box[r * 128 + warp * 32 + lane];
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + st);  // the stage's values are in registers
+      // bit r: row r is one of this item's channels and sampled (stride 1: all of them)
+      uint32_t smp;
+      if (a.stride == 1) {
+        smp = rows == kTokBoxRows ? 0xFFFFu : (1u << rows) - 1u;
+      } else {
+        smp = 0;
+#pragma unroll
+        for (int r = 0; r < kTokBoxRows; ++r) {
+          smp |= (r < rows && cm == 0 ? 1u : 0u) << r;
+          if (++cm == a.stride) cm = 0;
+        }
+      }
+      if (!t_ok) smp = 0;
+      // every row is binned (exactly where needed), so every bin is in [0, k): rows outside
+      // the item or unsampled only add 0
       int bin[kTokBoxRows];
       bool any_slow = P.exact_only != 0;
 #pragma unroll
       for (int r = 0; r < kTokBoxRows; ++r) {
         bool sl;
         bin[r] = bin_fast<FIXED>(x[r], P, &sl);
-        any_slow |= sl && ((smp >> r) & 1u);
+        any_slow |= sl;
       }
       if (__any_sync(0xffffffffu, any_slow)) {
 #pragma unroll
         for (int r = 0; r < kTokBoxRows; ++r) {
           bool sl;
           bin_fast<FIXED>(x[r], P, &sl);
-          if ((sl || P.exact_only) && ((smp >> r) & 1u))
-            bin[r] = bin_index_exact(static_cast<double>(x[r]), P.lo, P.width, k);
+          if (sl || P.exact_only) bin[r] = bin_index_exact(static_cast<double>(x[r]), P.lo, P.width, k);
         }
       }
+      // u16 counters [bin][lane] (address = base + bin * 64: one IMAD; the lane pair sharing
+      // a bank word conflicts only on different bins of equal parity -- this loop is
+      // ALU-bound, not shared-memory-bound, ncu r2f)
+      if (__all_sync(0xffffffffu, smp == 0xFFFFu)) {
+        // full box, every row sampled (stride 1): constant increments
+#pragma unroll
+        for (int g = 0; g < kTokBoxRows / 2; ++g) {
+          const int b0 = bin[2 * g], b1 = bin[2 * g + 1];
+          const uint32_t a0 = cbase + static_cast<uint32_t>(b0) * 64u;
+          const uint32_t a1 = cbase + static_cast<uint32_t>(b1) * 64u;
+          uint32_t v0, v1;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
+          v1 += b0 == b1 ? 2u : 1u;
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(a0), "h"(static_cast<uint16_t>(v0 + 1u)) : "memory");
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(a1), "h"(static_cast<uint16_t>(v1)) : "memory");
+        }
+      } else
 #pragma unroll
       for (int g = 0; g < kTokBoxRows / 2; ++g) {
-        const uint32_t i0 = (smp >> (2 * g)) & 1u ? inc : 0u;
-        const uint32_t i1 = (smp >> (2 * g + 1)) & 1u ? inc : 0u;
-        const int b0 = bin[2 * g] & 255, b1 = bin[2 * g + 1] & 255;
-        const uint32_t a0 = cbase + (static_cast<uint32_t>(b0) & ~1u) * 64u + (b0 & 1) * 2u;
-        const uint32_t a1 = cbase + (static_cast<uint32_t>(b1) & ~1u) * 64u + (b1 & 1) * 2u;
+        const uint32_t i0 = (smp >> (2 * g)) & 1u;
+        const uint32_t i1 = (smp >> (2 * g + 1)) & 1u;
+        const int b0 = bin[2 * g], b1 = bin[2 * g + 1];
+        const uint32_t a0 = cbase + static_cast<uint32_t>(b0) * 64u;
+        const uint32_t a1 = cbase + static_cast<uint32_t>(b1) * 64u;
         uint32_t v0, v1;
         asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
         asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
@@ -2045,12 +2072,12 @@ __global__ void __launch_bounds__((kTokTWarps + 1) * 32) token_hist_tma_kernel(
         __syncwarp();
         if (t_ok) {
           for (int b = 0; b < k; ++b) {
-            const uint32_t v = tcnt[tok_cidx(warp, b, lane)];
+            const uint32_t v = tcnt[(warp * 256 + b) * 32 + lane];
             if (v) atomicAdd(counts + t * k + b, v);
           }
         }
         __syncwarp();
-        uint4* c4 = reinterpret_cast<uint4*>(tcnt + tok_cidx(warp, 0, 0));
+        uint4* c4 = reinterpret_cast<uint4*>(tcnt + warp * 256 * 32);
         for (int i = lane; i < 256 * 32 * 2 / 16; i += 32) c4[i] = make_uint4(0, 0, 0, 0);
         __syncwarp();
         since = 0;
