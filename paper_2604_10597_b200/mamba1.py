@@ -263,6 +263,9 @@ class Prefill:
         kind = self.rule.inner_kind if self.rule.kind == _lib.CL_POL_GUARDED else self.rule.kind
         self.token = kind == _lib.CL_POL_TOKEN_HIST
         self.token_buf = torch.zeros(4, dtype=torch.float64, device=self.device)
+        # scan kernel family for __call__ / from_conv-free paths ("auto": by shape; "chained"
+        # makes the decided chunk the scan's segment length on every shape -- chunk sweeps)
+        self.scan_variant = "auto"
 
     # -- stages (exposed for the sharded path and for per-stage timing) --
     def stage_init(self, scan_inputs=None):
@@ -361,7 +364,7 @@ class Prefill:
             self.stage_minmax(uf, init=False)
             self.stage_histogram_decide(uf, u.shape[-1], zero=False)
         res = self.stage_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, out,
-                              return_last_state, h0)
+                              return_last_state, h0, variant=self.scan_variant)
         if return_last_state:
             o, h = res
         else:

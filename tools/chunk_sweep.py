@@ -57,30 +57,34 @@ def args_of(x):
     return (x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"], x["delta_bias"], True)
 
 
-def sweep(cfg, reps):
+def sweep(cfg, reps, variant="auto"):
     batch, dim, L, N, desc = bench.CONFIGS[cfg]
     dev = torch.device("cuda", 0)
     x = bench.make_inputs(torch, dev, batch, dim, L, N, 1)
     out = torch.empty_like(x["u"])
     scan_ms = {}
     for c in BUCKETS:
-        scan_ms[c] = timed(lambda: selective_scan_fn(*args_of(x), chunk_size=c, out=out), reps)
+        scan_ms[c] = timed(lambda: selective_scan_fn(*args_of(x), chunk_size=c, out=out,
+                                                     variant=variant), reps)
     best = min(scan_ms, key=scan_ms.get)
     bounds, cal = cl.ChunkBounds(64, 2048), cl.CalibrationRef.log_k(256)
     rule_pol = cl.SchedulerPolicy(cl.FullHistogramPolicy(), BUCKETS)
     pf_rule = Prefill(cl.HistogramSpec(), rule_pol, bounds, cal)
+    pf_rule.scan_variant = variant
     rule_ms = timed(lambda: pf_rule(*args_of(x), out=out), reps)
     rule_chunk = pf_rule.decision().decision.chunk
     pf_static = Prefill(cl.HistogramSpec(), cl.SchedulerPolicy(cl.StaticPolicy(best), BUCKETS),
                         bounds, cal)
+    pf_static.scan_variant = variant
     static_ms = timed(lambda: pf_static(*args_of(x), out=out), reps)
-    return {"mode": "sweep", "config": f"{cfg}: {desc}", "scan_ms_by_chunk": scan_ms,
+    return {"mode": "sweep", "config": f"{cfg}: {desc}", "scan_variant": variant,
+            "scan_ms_by_chunk": scan_ms,
             "static_oracle_chunk": best, "rule_chunk": rule_chunk,
             "prefill_ms_rule": rule_ms, "prefill_ms_static_oracle": static_ms,
             "rule_vs_oracle": rule_ms / static_ms}
 
 
-def mix(reps):
+def mix(reps, variant="auto"):
     dev = torch.device("cuda", 0)
     dim, N = 2048, 16
     lengths = [512, 2048, 8192, 32768]
@@ -96,6 +100,7 @@ def mix(reps):
     res = {}
     for name, pol in policies.items():
         pf = Prefill(cl.HistogramSpec(), pol, bounds, cal)
+        pf.scan_variant = variant
         per_len, chunks = {}, {}
         for L in lengths:
             x = inputs[L]
@@ -103,7 +108,8 @@ def mix(reps):
             per_len[L] = timed(lambda: pf(*args_of(x), out=out), reps)
             chunks[L] = pf.decision().decision.chunk
         res[name] = {"total_ms": sum(per_len.values()), "ms_by_len": per_len, "chunk_by_len": chunks}
-    return {"mode": "mix", "workload": f"B=1 d_inner={dim} N={N}, one prefill per L in {lengths}",
+    return {"mode": "mix", "scan_variant": variant,
+            "workload": f"B=1 d_inner={dim} N={N}, one prefill per L in {lengths}",
             "policies": res}
 
 
@@ -112,8 +118,12 @@ def main():
     ap.add_argument("mode", choices=["sweep", "mix"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--variant", default="auto",
+                    help="scan kernel family: auto (by shape) or chained (the chunk is the "
+                         "scan's segment length on every shape)")
     a = ap.parse_args()
-    print(json.dumps(sweep(a.config, a.reps) if a.mode == "sweep" else mix(a.reps)))
+    print(json.dumps(sweep(a.config, a.reps, a.variant) if a.mode == "sweep"
+                     else mix(a.reps, a.variant)))
 
 
 if __name__ == "__main__":
