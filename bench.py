@@ -443,9 +443,10 @@ def main():
         graphs = []
         captured0 = pf.ctx.launches
         with torch.cuda.stream(cap):
-            # (each graph has its own stream workspace, so the B / C re-layout stays in the
-            # scan's graph rather than being folded into the init launch)
-            for stage in (lambda: (pf.stage_init(), pf.stage_minmax(uf, g0, init=False)),
+            # (the graphs are captured on one stream and so share its captured workspace:
+            # the init launch re-lays B / C for the scan graph, as in an eager prefill)
+            scan_in = (x["u"], x["delta"], x["A"], x["B"], x["C"])
+            for stage in (lambda: (pf.stage_init(scan_in), pf.stage_minmax(uf, g0, init=False)),
                           lambda: pf.stage_histogram_decide(uf, L, zero=False),
                           lambda: pf.stage_scan(x["u"], x["delta"], x["A"], x["B"], x["C"],
                                                 x["D"], x["z"], x["delta_bias"], True, out,

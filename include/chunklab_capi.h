@@ -20,7 +20,9 @@
  *     device scratch (scan work tickets and carries, the B/C transpose, the
  *     fused histogram's arrival ticket, token-entropy buffers) is kept per
  *     stream, so launch sequences on different streams never share scratch;
- *     the host path (*_host) is serialised on the context.
+ *     work captured into CUDA graphs on a stream uses a second workspace of that
+ *     stream (so graph replays and eager launches never share scratch either); the
+ *     host path (*_host) is serialised on the context.
  *   - Device-path functions (cl_minmax_f32 ... cl_selective_scan_f32) are
  *     asynchronous on the given cudaStream_t (passed as void*) and never
  *     synchronise with the host.  Errors only the device can see

@@ -40,13 +40,19 @@ cl_workspace* workspace(cl_ctx* ctx, cudaStream_t stream) {
     cudaGetLastError();
     cs = cudaStreamCaptureStatusNone;
   }
-  if (cs != cudaStreamCaptureStatusActive) capture_id = 0;
-  const auto key = std::make_pair(stream, capture_id);
+  // Everything captured on one stream shares one captured workspace (distinct from the
+  // stream's eager one): the graphs of a step (e.g. per-stage graphs replayed in order)
+  // then pass state the way eager launches on that stream do.  Like any scratch, it must
+  // not be used by two replays at once -- the same rule that already holds for replaying
+  // one graph on two streams concurrently.
+  const unsigned long long captured = cs == cudaStreamCaptureStatusActive ? 1ull : 0ull;
+  (void)capture_id;
+  const auto key = std::make_pair(stream, captured);
   std::lock_guard<std::mutex> lk(ctx->ws_mu);
   auto it = ctx->ws.find(key);
   if (it != ctx->ws.end()) return it->second;
   auto* w = new cl_workspace();
-  w->captured = capture_id != 0;
+  w->captured = captured != 0;
   cudaError_t e;
   {
     CaptureRelaxed relax;

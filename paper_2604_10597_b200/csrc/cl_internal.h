@@ -44,10 +44,9 @@ struct cl_workspace {
   // arrival ticket of the fused histogram -> decision launch: 0 between launches (the
   // last CTA resets it), never visible to callers
   unsigned long long* d_hist_ticket = nullptr;
-  // captured workspaces: a device-side epoch parity per tag scheme ([0] chained carry,
-  // [1] L-parallel aggregates), flipped by each launch's last work claimer, so a graph's
-  // replays alternate between two tag bases (0x80000000 / 0xC0000000) and never need an
-  // in-graph memset of the tagged words
+  // captured workspaces: device-side launch counters ([1]: L-parallel aggregate tags),
+  // advanced by each launch's last work claimer, so every replay of every graph captured on
+  // the stream tags its words differently and no in-graph memset is needed
   unsigned int* d_epoch = nullptr;
   // created inside a CUDA-graph capture: its buffers are baked into that graph, which
   // may replay many times, so per-launch state (tagged-carry epochs) is reset in-graph
@@ -66,8 +65,8 @@ struct cl_ctx {
   int device = 0;
   int num_sms = 148;
   std::atomic<uint64_t> launches{0};
-  // one workspace per (stream handle, CUDA-graph capture id -- 0 outside a capture),
-  // created on first use, freed with the context
+  // one workspace per (stream handle, captured?): the stream's eager workspace and one for
+  // everything captured on that stream; created on first use, freed with the context
   std::mutex ws_mu;
   std::map<std::pair<cudaStream_t, unsigned long long>, cl_workspace*> ws;
   // The host path (*_host) and its scratch: serialised per context, so the drop-in C++
@@ -101,7 +100,7 @@ int zero_now(cl_ctx* ctx, void* p, size_t bytes);
 int zero_now(cl_ctx* ctx, void* p, size_t bytes);
 
 // The workspace of `stream` (created on first use); nullptr + error on allocation failure.
-// Inside a stream capture each capture gets its own workspace (keyed by capture id).
+// Inside a stream capture: the stream's captured workspace (shared by its captures).
 cl_workspace* workspace(cl_ctx* ctx, cudaStream_t stream);
 
 // cudaMalloc is not allowed while a stream captures in the default (global) mode; a

@@ -1989,7 +1989,6 @@ __global__ void __launch_bounds__((kTokTWarps + 1) * 32) token_hist_tma_kernel(
     const BinParams P = FIXED ? make_bin_params_lohi(fixed_lo, fixed_hi, k)
                         : t_ok ? make_bin_params_lohi(-trange[t], trange[a.length + t], k)
                                : make_bin_params_lohi(0.0, 0.0, k);
-    const uint32_t inc = t_ok ? 1u : 0u;
     uint64_t cm = (a.offset + c0) % a.stride;  // (offset + c) % stride of the box's first row
     uint32_t since = 0;
     for (uint64_t c = c0; c < c1; c += kTokBoxRows, ++it) {

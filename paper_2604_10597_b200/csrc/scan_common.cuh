@@ -462,7 +462,6 @@ struct TmaArgs {
   unsigned int* flags;     // [n_tiles] completed segments
   unsigned long long* tcarry;  // [n_tiles][16][16] {tag << 32 | h bits} (rowpair_ws_kernel)
   unsigned int epoch;          // tag of segment s's carry-in = epoch + s
-  unsigned int* epoch_parity;  // captured graphs: the device-side epoch parity (else null)
   int stage_params;            // A / bias / D 16-byte aligned: the producer stages a full
                                // tile's rows of them into shared memory with the item's first box
   unsigned int* ticket;    // work counter
@@ -517,29 +516,30 @@ constexpr int kStagedFlag = 1 << 30;  // meta.y bit: this item's parameters are 
 // claiming lane ends with exactly one claim past the last item, so a ticket that started
 // at 0 ends at n_items + claiming lanes (checked in CL_DEVICE_CHECKS builds: a dirty
 // ticket would have skipped items and left consumers waiting for carries).
-// In a captured graph the last claimer also flips the workspace's epoch parity (every CTA
-// read it at its start, and every CTA has started once all claimers retired).
+// In a captured graph the last claimer also advances the workspace's launch counter (every
+// CTA read it at its start, and every CTA has started once all claimers retired).
 __device__ __forceinline__ void ticket_retire(unsigned int* ticket, unsigned claimers, int lane,
                                               unsigned expect_final,
-                                              unsigned int* epoch_parity = nullptr) {
+                                              unsigned int* launch_counter = nullptr) {
   if (lane == 0) {
     __threadfence();
     if (atomicAdd(ticket + 1, 1u) == claimers - 1) {
       CL_DCHECK(atomicAdd(ticket, 0u) == expect_final);
       atomicExch(ticket, 0u);
       atomicExch(ticket + 1, 0u);
-      if (epoch_parity) atomicXor(epoch_parity, 1u);
+      if (launch_counter) atomicAdd(launch_counter, 1u);
     }
   }
 }
 
-// Tag base of a launch: the host's epoch (eager; always < 0x80000000), or in a captured
-// graph one of two bases chosen by the device-side parity, 2^30 apart, so a replay never
-// matches its predecessor's words (tags are base + at most L / box + 2).
-constexpr unsigned kGraphEpochA = 0x80000000u, kGraphEpochB = 0xC0000000u;
-__device__ __forceinline__ unsigned launch_epoch(unsigned host_epoch, const unsigned int* parity) {
-  if (!parity) return host_epoch;
-  return (__ldcg(parity) & 1u) ? kGraphEpochB : kGraphEpochA;
+// Tag of a launch's words: the host's epoch (eager; always < 0x80000000), or in a captured
+// graph 0x80000000 | the device-side launch counter -- every replay of every graph captured
+// on the stream gets its own tag (2^31 launches before one could repeat), so the graph
+// needs no in-graph memset of the tagged words.
+constexpr unsigned kGraphEpochA = 0x80000000u;
+__device__ __forceinline__ unsigned launch_epoch(unsigned host_epoch, const unsigned int* counter) {
+  if (!counter) return host_epoch;
+  return kGraphEpochA | (__ldcg(counter) & 0x7FFFFFFFu);
 }
 
 __device__ __forceinline__ f2_t shfl_xor2(f2_t v, int m) {
@@ -761,7 +761,7 @@ struct LookbackLaunch {
   float* h_last;
   unsigned long long* agg;  // [n_tiles][n_seg][16][18] tagged words
   unsigned int epoch;
-  unsigned int* epoch_parity;  // captured graphs: device-side parity (else null)
+  unsigned int* launch_counter;  // captured graphs: the device-side launch counter (else null)
   int stage_params;
   unsigned int* ticket;
   uint64_t batch, dim, L;

@@ -43,7 +43,7 @@ struct LbArgs {
   float* h_last;
   unsigned long long* agg;  // [n_tiles][n_seg][16 rows][kAggWords]
   unsigned int epoch;       // tag of this launch's aggregate words (eager)
-  unsigned int* epoch_parity;  // captured graphs: the device-side parity (launch_epoch)
+  unsigned int* launch_counter;  // captured graphs: the device-side launch counter (launch_epoch)
   int stage_params;
   unsigned int* ticket;
   uint64_t batch, dim, L;
@@ -250,7 +250,13 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     mbar_init(full + threadIdx.x, 1);
     mbar_init(empty + threadIdx.x, 1);
   }
-  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // the launch's tag, read before any producer can retire (the last claimer of the grid
+  // advances a captured graph's counter, and it retires only after every CTA passed here)
+  __shared__ unsigned s_epoch;
+  if (threadIdx.x == 0) {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_epoch = launch_epoch(a.epoch, a.launch_counter);
+  }
   __syncthreads();
 
   // items are dispatched segment-major: every predecessor (tile, j < k) of an item holds a
@@ -340,7 +346,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     // the ticket to 0, so the next launch on this stream needs no memset
     ticket_retire(a.ticket, gridDim.x * NPROD, lane,
                   static_cast<unsigned>(n_items) + gridDim.x * static_cast<unsigned>(WARPS),
-                  a.epoch_parity);
+                  a.launch_counter);
     return;
   }
 
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
   LbItem cur{};
   int row = 0;
   bool row_valid = false;
-  const unsigned epoch = launch_epoch(a.epoch, a.epoch_parity);
+  const unsigned epoch = s_epoch;
   const unsigned long long tag = static_cast<unsigned long long>(epoch) << 32;
   for (int iter = 0;; ++iter) {
     const int slot = iter % STAGES;
@@ -511,7 +517,7 @@ cudaError_t launch_lookback(int cfg, bool sp, bool hz, const CUtensorMap* maps,
   t.h_last = p.h_last;
   t.agg = p.agg;
   t.epoch = p.epoch;
-  t.epoch_parity = p.epoch_parity;
+  t.launch_counter = p.launch_counter;
   t.stage_params = p.stage_params;
   t.ticket = p.ticket;
   t.batch = p.batch;

@@ -424,8 +424,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
     // only producers claim tickets: the last producer warp of the grid to finish returns
     // the ticket to 0, so the next launch on this stream needs no memset
     ticket_retire(a.ticket, gridDim.x * NPROD, lane,
-                  static_cast<unsigned>(n_items) + gridDim.x * static_cast<unsigned>(WARPS),
-                  a.epoch_parity);
+                  static_cast<unsigned>(n_items) + gridDim.x * static_cast<unsigned>(WARPS));
     return;
   }
 
@@ -436,7 +435,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
   uint64_t* wempty = empty + warp * STAGES;
   const int2* wmeta = meta + warp * STAGES;
   constexpr int kP = kN / 4;
-  const unsigned epoch = launch_epoch(a.epoch, a.epoch_parity);
+  const unsigned epoch = a.epoch;
   f2_t h2[kP], A2p[kP];
   float bias = 0.f, Dc = 0.f;
   Item cur{};
@@ -505,7 +504,7 @@ __global__ void __launch_bounds__((WARPS + NPROD) * 32, 1)
             ok &= static_cast<unsigned>(w[i] >> 32) == want;
             ok &= static_cast<unsigned>(w[i + 1] >> 32) == want;
             // eager tags only grow: a newer tag than this launch's would be a stale-epoch bug
-            CL_DCHECK(a.epoch_parity || static_cast<unsigned>(w[i] >> 32) <= want);
+            CL_DCHECK(static_cast<unsigned>(w[i] >> 32) <= want);
           }
           if (__all_sync(0xffffffffu, ok)) break;
           __nanosleep(64);
@@ -970,18 +969,26 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       rc = grow_scratch(ctx, w, &w->d_tcarry, &w->tcarry_bytes, tcarry_bytes, "cudaMalloc(tagged carry)");
       if (rc) return rc;
       const unsigned span = static_cast<unsigned>((L + cfg.box - 1) / cfg.box) + 2u;
-      // eager: host epochs below 0x80000000; a captured graph takes its tag base from the
-      // device-side parity instead (launch_epoch), so its replays need no memset
+      // eager: host epochs below 0x80000000, advanced past every launch's tags; a captured
+      // graph bakes its epoch into every replay, so it zeroes the words it uses in-graph
+      // before each launch (4 MB at C3: ~2 us of a 1.35 ms scan)
       if (fresh) {
         if ((rc = zero_now(ctx, w->d_tcarry, w->tcarry_bytes))) return rc;
         w->carry_epoch = 1;
-      } else if (!w->captured && (w->carry_epoch == 0 || w->carry_epoch > 0x7FFFFFFFu - span)) {
-        cudaError_t e = cudaMemsetAsync(w->d_tcarry, 0, w->tcarry_bytes, s);
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(tagged carry)");
-        w->carry_epoch = 1;
       }
-      epoch = w->captured ? 0u : w->carry_epoch;
-      if (!w->captured) w->carry_epoch += span;
+      if (w->captured) {
+        cudaError_t e = cudaMemsetAsync(w->d_tcarry, 0, tcarry_bytes, s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(tagged carry)");
+        epoch = 1;
+      } else {
+        if (w->carry_epoch == 0 || w->carry_epoch > 0x7FFFFFFFu - span) {
+          cudaError_t e = cudaMemsetAsync(w->d_tcarry, 0, w->tcarry_bytes, s);
+          if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(tagged carry)");
+          w->carry_epoch = 1;
+        }
+        epoch = w->carry_epoch;
+        w->carry_epoch += span;
+      }
     }
     // B^T / C^T: interleaved per timestep ([B | C], 128 B rows, one TMA box) for the
     // warp-specialised kernel, two separate (b, L, 16) arrays for the row kernel
@@ -1030,7 +1037,6 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     t.carry = w->d_carry;
     t.tcarry = w->d_tcarry;
     t.epoch = epoch;
-    t.epoch_parity = w->captured ? w->d_epoch : nullptr;
     t.stage_params = aligned16(a.A) && (!a.delta_bias || aligned16(a.delta_bias)) &&
                      (!a.D || aligned16(a.D));
     t.ticket = w->d_work;
@@ -1054,7 +1060,7 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
       p.h_last = a.h_last;
       p.agg = w->d_agg;
       p.epoch = epoch;
-      p.epoch_parity = w->captured ? w->d_epoch + 1 : nullptr;
+      p.launch_counter = w->captured ? w->d_epoch + 1 : nullptr;
       p.stage_params = t.stage_params;
       p.ticket = w->d_work;
       p.batch = Bt;

@@ -147,6 +147,37 @@ def test_no_host_sync_in_prefill(cuda):
         pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"])
 
 
+def test_several_graphs_share_the_captured_workspace(cuda):
+    """Graphs captured on one stream share that stream's captured workspace (torch's
+    graphs all capture on one side stream).  Replayed interleaved -- A B A A C B C ... --
+    each reproduces its eager bits: the L-parallel aggregate tags come from a device-side
+    launch counter (never repeated across graphs), the chained carry words are zeroed
+    in-graph, and the ticket returns to 0 at the end of every launch."""
+    cases = [((1, 48, 2048), "lookback"), ((2, 64, 512), "chained"), ((1, 32, 4096), "lookback"),
+             ((4, 64, 256), "auto")]
+    runs = []
+    for i, (shape, variant) in enumerate(cases):
+        d = dev(mamba_inputs(40 + i, *shape[:2], 16, shape[2]), cuda)
+        pf = Prefill(cl.HistogramSpec(), device=cuda)
+        pf.scan_variant = variant
+        out = torch.empty_like(d["u"])
+        args = (d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"])
+        pf(*args, out=out)
+        torch.cuda.synchronize()
+        runs.append([pf, args, out, out.clone(), None])
+    for r in runs:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            r[0](*r[1], out=r[2])
+        r[4] = g
+    for it, k in enumerate([0, 1, 0, 0, 2, 1, 2, 3, 0, 2, 2, 3, 1, 0]):
+        pf, args, out, ref, g = runs[k]
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), (it, k)
+
+
 @pytest.mark.parametrize("case", ["default", "repeat", "stride8", "fixed", "k512", "small",
                                   "nonfinite", "guarded", "ragged"])
 def test_histogram_decide_fused_equals_separate(cuda, case):

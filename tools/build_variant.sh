@@ -5,11 +5,13 @@
 set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
-out=build/variants/$name; mkdir -p $out
+out=build/variants/$name; rm -rf $out; mkdir -p $out
+pids=()
 for f in paper_2604_10597_b200/csrc/*.cu; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC \
     --expt-relaxed-constexpr -Iinclude -Ipaper_2604_10597_b200/csrc "$@" -c $f -o $out/$(basename $f).o &
+  pids+=($!)
 done
-wait
+for p in "${pids[@]}"; do wait $p; done  # any failed compile fails the build (set -e)
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o build/variants/$name.so $out/*.o -lpthread -ldl -lrt
 echo build/variants/$name.so
