@@ -77,6 +77,47 @@ __device__ __forceinline__ float exp2_elem(float x) {
 #endif
 }
 
+// ---- exponentials of the state transitions, dA = 2^(A log2e dt) ----
+// MUFU by default.  CL_STATE_POLY=m (0..4) computes the states s with ((s & 7) >> 1) < m
+// -- m of every lane's 4 state pairs -- on the FMA pipe instead: n = rint(x) by the
+// 1.5 * 2^23 magic add, f = x - n exactly, 2^f = 1 + f q(f) with q a degree-4 polynomial
+// (minimax relative error of 2^f with the constant term pinned to 1 so dA -> 1 exactly as
+// dt -> 0: 6.8e-8, 2.2e-7 after fp32 rounding; ex2.approx: 2.4e-7), 2^n added into the
+// exponent field, x clamped to [-125, 127] (NaN kept).  Every kernel picks the same
+// function for the same state, so all paths stay bitwise consistent.  A/B in
+// profiles/r2k_state_poly_ab.txt.
+#ifndef CL_STATE_POLY
+#define CL_STATE_POLY 0
+#endif
+constexpr float kSq1 = 0.6931465864181519f, kSq2 = 0.24022166430950165f,
+                kSq3 = 0.055510472506284714f, kSq4 = 0.009674952365458012f,
+                kSq5 = 0.0013202981790527701f;
+
+__device__ __forceinline__ float min_nan(float a, float b) {
+  float y;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(y) : "f"(a), "f"(b));
+  return y;
+}
+
+__device__ __forceinline__ bool state_on_fma(int s) { return ((s & 7) >> 1) < CL_STATE_POLY; }
+
+__device__ __forceinline__ float exp2_state_poly(float x) {
+  x = min_nan(max_nan(x, -125.f), 127.f);
+  const float t = __fadd_rn(x, 12582912.f);
+  const float f = __fadd_rn(x, -__fadd_rn(t, -12582912.f));
+  float q = fmaf(kSq5, f, kSq4);
+  q = fmaf(q, f, kSq3);
+  q = fmaf(q, f, kSq2);
+  q = fmaf(q, f, kSq1);
+  const float p = fmaf(q, f, 1.f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// dA of state s (scalar kernels: generic scan, decode)
+__device__ __forceinline__ float state_exp2(float x, int s) {
+  return state_on_fma(s) ? exp2_state_poly(x) : ex2_approx(x);
+}
+
 // ---- canonical elementwise math ----
 // Every Mamba-1 path (generic scan, TMA scans, decode) evaluates softplus, SiLU and, for
 // N = 16, C.h with exactly these operation sequences, so the paths agree bit for bit
@@ -188,7 +229,7 @@ __global__ void __launch_bounds__(128) generic_kernel(GenericArgs a) {
       float cv[16];
 #pragma unroll
       for (int s = 0; s < 16; ++s) {
-        const float dA = ex2_approx(A2[s] * dt);
+        const float dA = state_exp2(A2[s] * dt, s);
         h[s] = fmaf(dA, h[s], __fmul_rn(Bb[s * a.L + t], x));
         cv[s] = Cb[s * a.L + t];
       }
@@ -197,7 +238,7 @@ __global__ void __launch_bounds__(128) generic_kernel(GenericArgs a) {
 #pragma unroll
       for (int s = 0; s < (NS > 0 ? NS : 64); ++s) {
         if (s < N) {
-          const float dA = ex2_approx(A2[s] * dt);
+          const float dA = state_exp2(A2[s] * dt, s);
           h[s] = fmaf(dA, h[s], __fmul_rn(Bb[s * a.L + t], x));
           y = fmaf(Cb[s * a.L + t], h[s], y);
         }
@@ -247,7 +288,7 @@ __global__ void __launch_bounds__(128) decode_kernel(DecodeArgs a) {
     float h[16], cv[16];
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
-      const float dA = ex2_approx((a.A[c * 16 + s] * kLog2e) * dt);
+      const float dA = state_exp2((a.A[c * 16 + s] * kLog2e) * dt, s);
       h[s] = fmaf(dA, st[s], __fmul_rn(Bb[s], xx));
       cv[s] = Cb[s];
     }
@@ -256,7 +297,7 @@ __global__ void __launch_bounds__(128) decode_kernel(DecodeArgs a) {
     for (int s = 0; s < 16; ++s) st[s] = h[s];
   } else {
     for (int s = 0; s < N; ++s) {
-      const float dA = ex2_approx((a.A[c * N + s] * kLog2e) * dt);
+      const float dA = state_exp2((a.A[c * N + s] * kLog2e) * dt, s);
       const float h = fmaf(dA, st[s], __fmul_rn(Bb[s], xx));
       y = fmaf(Cb[s], h, y);
       st[s] = h;
@@ -415,6 +456,30 @@ __device__ __forceinline__ f2_t exp2_elem2(float xa, float xb) {
   return pk(__int_as_float(__float_as_int(pl) + (__float_as_int(tl) << 23)),
             __int_as_float(__float_as_int(ph) + (__float_as_int(th) << 23)));
 #endif
+}
+
+// dA of the state pair (s0, s0 + 1), s0 even, i = (s0 & 7) >> 1 (compile-time in the
+// unrolled pair loops); per lane the same operations as state_exp2
+__device__ __forceinline__ f2_t state_exp2_pair(f2_t x2, int i) {
+  float xa, xb;
+  upk(x2, xa, xb);
+  if (i >= CL_STATE_POLY) return pk(ex2_approx(xa), ex2_approx(xb));
+  const f2_t x = pk(min_nan(max_nan(xa, -125.f), 127.f), min_nan(max_nan(xb, -125.f), 127.f));
+  const f2_t t = add2(x, pk(12582912.f, 12582912.f));
+  const f2_t n = add2(t, pk(-12582912.f, -12582912.f));
+  float nl, nh;
+  upk(n, nl, nh);
+  const f2_t f = add2(x, pk(-nl, -nh));
+  f2_t q = fma2(pk(kSq5, kSq5), f, pk(kSq4, kSq4));
+  q = fma2(q, f, pk(kSq3, kSq3));
+  q = fma2(q, f, pk(kSq2, kSq2));
+  q = fma2(q, f, pk(kSq1, kSq1));
+  const f2_t p = fma2(q, f, pk(1.f, 1.f));
+  float pl, ph, tl, th;
+  upk(p, pl, ph);
+  upk(t, tl, th);
+  return pk(__int_as_float(__float_as_int(pl) + (__float_as_int(tl) << 23)),
+            __int_as_float(__float_as_int(ph) + (__float_as_int(th) << 23)));
 }
 
 __device__ __forceinline__ f2_t softplus2(f2_t x) {
@@ -587,9 +652,7 @@ __device__ __forceinline__ void pair_box(const unsigned char* st, float* ydst, i
       const f2_t dd = pk(dt[k], dt[k]);
 #pragma unroll
       for (int i = 0; i < kP; ++i) {
-        float al, ah;
-        upk(mul2(A2p[i], dd), al, ah);
-        dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+        dA[k][i] = state_exp2_pair(mul2(A2p[i], dd), i);
       }
     }
     float yp[4];
@@ -680,9 +743,7 @@ __device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* yd
       const f2_t dd = pk(dt[k], dt[k]);
 #pragma unroll
       for (int i = 0; i < kP; ++i) {
-        float al, ah;
-        upk(mul2(A2p[i], dd), al, ah);
-        dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+        dA[k][i] = state_exp2_pair(mul2(A2p[i], dd), i);
       }
     }
     float ndt[4], nxs[4];

@@ -92,9 +92,7 @@ __device__ __forceinline__ void agg_box(const unsigned char* st, int r, int hf, 
       const f2_t dd = pk(dt[k], dt[k]);
 #pragma unroll
       for (int i = 0; i < kP; ++i) {
-        float al, ah;
-        upk(mul2(A2p[i], dd), al, ah);
-        dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+        dA[k][i] = state_exp2_pair(mul2(A2p[i], dd), i);
       }
     }
 #pragma unroll
@@ -150,9 +148,7 @@ __device__ __forceinline__ void agg_box_pipe(const unsigned char* st, int r, int
       const f2_t dd = pk(dt[k], dt[k]);
 #pragma unroll
       for (int i = 0; i < kP; ++i) {
-        float al, ah;
-        upk(mul2(A2p[i], dd), al, ah);
-        dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+        dA[k][i] = state_exp2_pair(mul2(A2p[i], dd), i);
       }
     }
     float ndt[4], nxs[4];

@@ -210,9 +210,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         const f2_t dd = pk(dt[k], dt[k]);
 #pragma unroll
         for (int i = 0; i < kN / 2; ++i) {
-          float al, ah;
-          upk(mul2(A2p[i], dd), al, ah);
-          dA[k][i] = pk(ex2_approx(al), ex2_approx(ah));
+          dA[k][i] = state_exp2_pair(mul2(A2p[i], dd), i & 3);
         }
       }
       // phase B: recurrence h = dA*h + B*x and y = C.h, FFMA2 on state pairs
