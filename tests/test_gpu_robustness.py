@@ -69,7 +69,7 @@ def test_uncovered_dynamic_range_clamps_like_the_reference(cuda, port, n):
     d = torch.from_numpy(v).to(cuda)
     ctx = cl.Context.get(cuda.index)
     s = torch.cuda.current_stream(cuda).cuda_stream
-    for k in (256, 64):
+    for k in (256, 64, 100):  # power-of-two K: the one-LOP3 range check; 100: the compare
         spec = cl.HistogramSpec(bin_count=k)
         cs = spec.to_c()
         rng_buf = torch.tensor([-lo, hi, 0.0, 0.0], dtype=torch.float64, device=cuda)

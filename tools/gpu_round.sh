@@ -1,6 +1,4 @@
 mkdir -p gpurun_out
-for v in default poly1; do
-  if [ $v = default ]; then unset CHUNKLAB_LIB; else export CHUNKLAB_LIB=build/variants/$v.so; fi
-  timeout 300 python tools/profile_stages.py --config C3 --reps 1 > /dev/null 2>&1
-  timeout 600 ncu --set full --clock-control none -k regex:"rowpair_ws" -c 1 -o gpurun_out/k_$v python tools/profile_stages.py --config C3 --reps 1 > gpurun_out/k_ncu_$v.log 2>&1
-done
+./tools/micro/decide_lat > gpurun_out/r_decide_lat.txt 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q -k "entropy or hist or prefill or fullsize or robust or stress or lean or baseline or chunk or conv" > gpurun_out/r_tests.log 2>&1; echo rc=$? >> gpurun_out/r_tests.log
+for i in 1 2; do timeout 300 python tools/profile_stages.py --config C3 --reps 30 --median 2>&1 | grep cfg; done > gpurun_out/r_c3.txt
