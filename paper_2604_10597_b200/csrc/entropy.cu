@@ -380,6 +380,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+[[maybe_unused]] __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
   asm volatile(
@@ -1672,6 +1685,12 @@ constexpr int kTokHMaxPerFlush = 65000;     // u16 counters: flush before overfl
 #ifndef CL_TOK_TMA
 #define CL_TOK_TMA 1
 #endif
+#ifndef CL_TOK_QUAD
+#define CL_TOK_QUAD 1
+#endif
+#ifndef CL_TOK_PROD_SLEEP
+#define CL_TOK_PROD_SLEEP 0
+#endif
 
 __device__ __forceinline__ void tok_item_split(uint64_t item, uint64_t tiles, uint64_t splits,
                                                uint64_t channels, uint64_t* tile,
@@ -1984,7 +2003,15 @@ __global__ void __launch_bounds__((kTokTWarps + 1) * 32) token_hist_tma_kernel(
         const uint64_t c1 = umin64(a.channels, c0 + per_split);
         for (uint64_t c = c0; c < c1; c += kTokBoxRows, ++it) {
           const int st = it % kTokStages;
-          if (it >= static_cast<uint32_t>(kTokStages)) mbar_wait(empty + st, ((it / kTokStages) - 1) & 1);
+          if (it >= static_cast<uint32_t>(kTokStages)) {
+#if CL_TOK_PROD_SLEEP
+            // back off instead of spinning: the consumers are the bound, and a spinning
+            // producer takes issue slots from the consumer warps of its sub-partition
+            while (!mbar_test(empty + st, ((it / kTokStages) - 1) & 1)) __nanosleep(CL_TOK_PROD_SLEEP);
+#else
+            mbar_wait(empty + st, ((it / kTokStages) - 1) & 1);
+#endif
+          }
           mbar_expect_tx(full + st, kTokBoxBytes);
           tma_load_3d(ring + size_t(st) * kTokBoxBytes, &map, static_cast<int>(tile * 128),
                       static_cast<int>(c), 0, full + st);
@@ -2050,7 +2077,33 @@ __global__ void __launch_bounds__((kTokTWarps + 1) * 32) token_hist_tma_kernel(
       // u16 counters [bin][lane] (address = base + bin * 64: one IMAD; the lane pair sharing
       // a bank word conflicts only on different bins of equal parity -- this loop is
       // ALU-bound, not shared-memory-bound, ncu r2f)
-      if (__all_sync(0xffffffffu, smp == 0xFFFFu)) {
+      if (CL_TOK_QUAD && __all_sync(0xffffffffu, smp == 0xFFFFu)) {
+        // full box, every row sampled (stride 1): constant increments, four samples per
+        // read-modify-write round (all four loads, then the stores in sample order, each
+        // carrying the earlier samples of its bin: the last store to a bin holds the
+        // bin's whole multiplicity) -- the per-lane RMW chain is 4 rounds per box, not 8
+#pragma unroll
+        for (int g = 0; g < kTokBoxRows / 4; ++g) {
+          const int b0 = bin[4 * g], b1 = bin[4 * g + 1], b2 = bin[4 * g + 2], b3 = bin[4 * g + 3];
+          const uint32_t a0 = cbase + static_cast<uint32_t>(b0) * 64u;
+          const uint32_t a1 = cbase + static_cast<uint32_t>(b1) * 64u;
+          const uint32_t a2 = cbase + static_cast<uint32_t>(b2) * 64u;
+          const uint32_t a3 = cbase + static_cast<uint32_t>(b3) * 64u;
+          uint32_t v0, v1, v2, v3;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v0) : "r"(a0) : "memory");
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v1) : "r"(a1) : "memory");
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v2) : "r"(a2) : "memory");
+          asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v3) : "r"(a3) : "memory");
+          v0 += 1u;
+          v1 += 1u + (b0 == b1);
+          v2 += 1u + (b0 == b2) + (b1 == b2);
+          v3 += 1u + (b0 == b3) + (b1 == b3) + (b2 == b3);
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(a0), "h"(static_cast<uint16_t>(v0)) : "memory");
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(a1), "h"(static_cast<uint16_t>(v1)) : "memory");
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(a2), "h"(static_cast<uint16_t>(v2)) : "memory");
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(a3), "h"(static_cast<uint16_t>(v3)) : "memory");
+        }
+      } else if (__all_sync(0xffffffffu, smp == 0xFFFFu)) {
         // full box, every row sampled (stride 1): constant increments
 #pragma unroll
         for (int g = 0; g < kTokBoxRows / 2; ++g) {
@@ -2597,12 +2650,27 @@ cudaError_t launch_token_hist(const T* v, uint64_t channels, uint64_t length, ui
     if (!make_map(&map, reinterpret_cast<const float*>(v), length, channels, 1, 128, kTokBoxRows,
                   0))
       return cudaErrorInvalidValue;
-    uint64_t tiles, splits;
     const int resident = num_sms * 2;  // 2 blocks (64 KB counters + 40 KB ring) per SM
-    tok_lane_items(channels, length, 128, resident, &tiles, &splits);
-    // at least a few boxes per item
+    // channel splits: every item ends with a flush of its 128 x K counters (LDS + a global
+    // atomic per nonzero bin), and the items run in rounds of `resident` blocks, so pick the
+    // split count minimising rounds x (channels per item + flush cost in channel
+    // equivalents); at least a few boxes per item
+    const uint64_t tiles = (length + 127) / 128;
+    static const uint64_t flush_cost = [] {
+      const char* e = getenv("CL_TOK_FLUSH_COST");
+      return e ? static_cast<uint64_t>(atoi(e)) : uint64_t(256);
+    }();
     const uint64_t max_sp = (channels + 4 * kTokBoxRows - 1) / (4 * kTokBoxRows);
-    if (splits > max_sp) splits = max_sp < 1 ? 1 : max_sp;
+    const uint64_t hi_sp = (8 * static_cast<uint64_t>(resident) + tiles - 1) / tiles;
+    uint64_t splits = 1, best = ~0ull;
+    for (uint64_t sp = 1; sp <= hi_sp && sp <= (max_sp < 1 ? 1 : max_sp); ++sp) {
+      const uint64_t rounds = (tiles * sp + resident - 1) / resident;
+      const uint64_t cost = rounds * ((channels + sp - 1) / sp + flush_cost);
+      if (cost < best) {
+        best = cost;
+        splits = sp;
+      }
+    }
     const uint64_t items = tiles * splits;
     const unsigned grid = static_cast<unsigned>(items < static_cast<uint64_t>(resident) ? items : resident);
     const bool fixed = spec.range_mode == CL_RANGE_FIXED;

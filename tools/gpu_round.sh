@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-./tools/micro/decide_lat > gpurun_out/r_decide_lat.txt 2>&1
-timeout 600 python -m pytest tests -m gpu -x -q -k "entropy or hist or prefill or fullsize or robust or stress or lean or baseline or chunk or conv" > gpurun_out/r_tests.log 2>&1; echo rc=$? >> gpurun_out/r_tests.log
-for i in 1 2; do timeout 300 python tools/profile_stages.py --config C3 --reps 30 --median 2>&1 | grep cfg; done > gpurun_out/r_c3.txt
+for i in 1 2; do for f in 256 64 1024 4096; do
+  echo -n "F=$f "; CL_TOK_FLUSH_COST=$f timeout 300 python tools/profile_token.py --reps 10 2>&1 | tail -1
+done; done > gpurun_out/v_ab.txt
+timeout 600 python -m pytest tests -m gpu -x -q -k "token" > gpurun_out/v_tests.log 2>&1; echo rc=$? >> gpurun_out/v_tests.log
