@@ -402,16 +402,20 @@ def main():
                 ev[3].record()
         else:
             pf.stage_init((x["u"], x["delta"], x["A"], x["B"], x["C"]))
-            pf.stage_minmax(uf, g0, init=False)
-            if ev and fine:
-                ev[1].record()
             if FUSED_DECIDE:
-                # histogram + decision in one launch (its last CTA decides): stage
-                # "histogram" includes the decision, "decide" is the empty interval
-                pf.stage_histogram_decide(uf, L, zero=False)
+                # min/max (gathering the samples for strides >= 4), then histogram +
+                # decision in one launch (its last CTA decides): stage "histogram"
+                # includes the decision -- the single-GPU prefill's own sequence
+                pf.stage_entropy_minmax(uf)
+                if ev and fine:
+                    ev[1].record()
+                pf.stage_entropy_histogram(uf, L)
                 if ev and fine:
                     ev[2].record()
             else:
+                pf.stage_minmax(uf, g0, init=False)
+                if ev and fine:
+                    ev[1].record()
                 pf.stage_histogram(uf, g0, zero=False)
                 if ev and fine:
                     ev[2].record()
@@ -446,8 +450,8 @@ def main():
             # (the graphs are captured on one stream and so share its captured workspace:
             # the init launch re-lays B / C for the scan graph, as in an eager prefill)
             scan_in = (x["u"], x["delta"], x["A"], x["B"], x["C"])
-            for stage in (lambda: (pf.stage_init(scan_in), pf.stage_minmax(uf, g0, init=False)),
-                          lambda: pf.stage_histogram_decide(uf, L, zero=False),
+            for stage in (lambda: (pf.stage_init(scan_in), pf.stage_entropy_minmax(uf)),
+                          lambda: pf.stage_entropy_histogram(uf, L),
                           lambda: pf.stage_scan(x["u"], x["delta"], x["A"], x["B"], x["C"],
                                                 x["D"], x["z"], x["delta_bias"], True, out,
                                                 True)):
@@ -463,8 +467,7 @@ def main():
             g_ent = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g_ent, stream=cap):
                 pf.stage_init(scan_in)
-                pf.stage_minmax(uf, g0, init=False)
-                pf.stage_histogram_decide(uf, L, zero=False)
+                pf.stage_entropy(uf, L)
         torch.cuda.current_stream(device).wait_stream(cap)
         torch.cuda.synchronize()
 

@@ -150,6 +150,19 @@ int cl_minmax_f32(cl_ctx* ctx, const float* d_values, uint64_t n, uint64_t globa
                   uint64_t stride, double* d_range, void* stream);
 int cl_minmax_f64(cl_ctx* ctx, const double* d_values, uint64_t n, uint64_t global_offset,
                   uint64_t stride, double* d_range, void* stream);
+/* cl_minmax_f32 that also writes every sampled value, in index order, to d_samples:
+ * d_samples[j] = d_values[i] for the j-th i whose global index (global_offset + i) is a
+ * multiple of stride (capacity: cl_samples_in(global_offset, n, stride) floats).  A
+ * strided histogram of d_samples with stride 1 counts exactly what the strided
+ * histogram of d_values counts, reading n / stride values instead of n; cl_prefill_f32
+ * takes this path for stride >= 4. */
+#define CL_GATHER_MIN_STRIDE 4
+int cl_minmax_gather_f32(cl_ctx* ctx, const float* d_values, uint64_t n,
+                         uint64_t global_offset, uint64_t stride, double* d_range,
+                         float* d_samples, void* stream);
+/* Number of global indices in [global_offset, global_offset + n) that are multiples of
+ * stride (0 for stride 0). */
+uint64_t cl_samples_in(uint64_t global_offset, uint64_t n, uint64_t stride);
 
 /* Producer fusion (no reference counterpart -- the paper's u comes
  * out of mamba_ssm's causal_conv1d_fn):

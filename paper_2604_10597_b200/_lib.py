@@ -20,6 +20,7 @@ CL_RANGE_DYNAMIC, CL_RANGE_FIXED = 0, 1
 CL_SRC_GUARDED, CL_SRC_GUARDED_FALLBACK = 16, 32
 CL_SCAN_AUTO, CL_SCAN_ROWSEQ_TMA, CL_SCAN_GENERIC, CL_SCAN_LOOKBACK, CL_SCAN_CHAINED = range(5)
 CL_SCAN_CONFIG_BASE, CL_SCAN_LOOKBACK_BASE = 16, 64
+CL_GATHER_MIN_STRIDE = 4  # cl_prefill_f32 gathers the samples for sample_stride >= this
 CL_KERNEL_GENERIC, CL_KERNEL_CHAINED, CL_KERNEL_ROWSEQ, CL_KERNEL_LOOKBACK = range(4)
 KERNEL_NAMES = {0: "generic_kernel", 1: "rowpair_ws_kernel", 2: "rowseq_tma_kernel",
                 3: "lookback_ws_kernel"}
@@ -126,6 +127,8 @@ SIGNATURES = {
     "cl_validate_rule": (C.c_int, [_P, C.POINTER(cl_rule_spec)]),
     "cl_range_init": (C.c_int, [_P, _P, _P]),
     "cl_minmax_f32": (C.c_int, [_P, _P, _u64, _u64, _u64, _P, _P]),
+    "cl_minmax_gather_f32": (C.c_int, [_P, _P, _u64, _u64, _u64, _P, _P, _P]),
+    "cl_samples_in": (_u64, [_u64, _u64, _u64]),
     "cl_minmax_f64": (C.c_int, [_P, _P, _u64, _u64, _u64, _P, _P]),
     "cl_conv1d_f32": (C.c_int, [_P, _P, _P, _P, _P, _u64, _u64, _u64, C.c_int, C.c_int, _u64,
                                 _u64, _P, _P]),

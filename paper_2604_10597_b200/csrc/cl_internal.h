@@ -59,6 +59,9 @@ struct cl_workspace {
   size_t token_range_bytes = 0;
   unsigned int* d_token_counts = nullptr;
   size_t token_counts_bytes = 0;
+  // strided prefill: the sampled values gathered by cl_minmax_gather_f32
+  float* d_samples = nullptr;
+  size_t samples_bytes = 0;
 };
 
 struct cl_ctx {
@@ -136,6 +139,9 @@ cudaError_t launch_minmax_f32(const float* v, uint64_t n, uint64_t g0, uint64_t 
                               double* d_range, int num_sms, cudaStream_t s, int* launches);
 cudaError_t launch_minmax_f64(const double* v, uint64_t n, uint64_t g0, uint64_t stride,
                               double* d_range, int num_sms, cudaStream_t s, int* launches);
+cudaError_t launch_minmax_gather_f32(const float* v, uint64_t n, uint64_t g0, uint64_t stride,
+                                     double* d_range, float* d_samples, int num_sms,
+                                     cudaStream_t s, int* launches);
 // Histogram + decision in one launch (single-GPU prefill): the decision's inputs
 // beyond the histogram's own.
 struct HistFuse {

@@ -159,15 +159,26 @@ __device__ __forceinline__ bool sampled(uint64_t gi, uint64_t stride) {
   return gi % stride == 0;
 }
 
-template <int MODE>
+// GATHER: every sampled value is also written to gather[(g0 + i) / stride - first] (first =
+// the first sampled global index / stride), so a strided histogram reads n / stride values
+// instead of all n (cl_minmax_gather_f32)
+template <int MODE, bool GATHER = false>
 __global__ void __launch_bounds__(kThreads) minmax_f32_kernel(const float* __restrict__ v,
                                                               uint64_t n, uint64_t g0,
-                                                              uint64_t stride, double* range) {
+                                                              uint64_t stride, double* range,
+                                                              float* __restrict__ gather = nullptr,
+                                                              uint64_t first = 0) {
   range::Acc acc;
   const uint64_t head = umin64(n, ((16u - (reinterpret_cast<uintptr_t>(v) & 15u)) & 15u) / 4u);
   const uint64_t n4 = (n - head) / 4;
   const uint64_t tail0 = head + n4 * 4;
-  auto visit = [&](float x, uint64_t i) { acc.visit(x, sampled<MODE>(g0 + i, stride)); };
+  const int sh = MODE == 1 ? __ffsll(static_cast<long long>(stride)) - 1 : 0;
+  auto visit = [&](float x, uint64_t i) {
+    const bool smp = sampled<MODE>(g0 + i, stride);
+    acc.visit(x, smp);
+    if (GATHER && smp)
+      gather[(MODE == 1 ? (g0 + i) >> sh : (g0 + i) / stride) - first] = x;
+  };
   if (blockIdx.x == 0) {
     for (uint64_t i = threadIdx.x; i < head; i += blockDim.x) visit(v[i], i);
     for (uint64_t i = tail0 + threadIdx.x; i < n; i += blockDim.x) visit(v[i], i);
@@ -2289,6 +2300,27 @@ cudaError_t launch_minmax_f32(const float* v, uint64_t n, uint64_t g0, uint64_t 
     case 0: minmax_f32_kernel<0><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range); break;
     case 1: minmax_f32_kernel<1><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range); break;
     default: minmax_f32_kernel<2><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range); break;
+  }
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_minmax_gather_f32(const float* v, uint64_t n, uint64_t g0, uint64_t stride,
+                                     double* d_range, float* d_samples, int num_sms,
+                                     cudaStream_t s, int* launches) {
+  if (n == 0) return cudaSuccess;
+  const int grid = grid_for(n / 4 + 1, kThreads * 4, num_sms, CL_MM_CTAS_PER_SM);
+  const uint64_t first = (g0 + stride - 1) / stride;
+  switch (stride_mode(stride)) {
+    case 0:
+      minmax_f32_kernel<0, true><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range, d_samples, first);
+      break;
+    case 1:
+      minmax_f32_kernel<1, true><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range, d_samples, first);
+      break;
+    default:
+      minmax_f32_kernel<2, true><<<grid, kThreads, 0, s>>>(v, n, g0, stride, d_range, d_samples, first);
+      break;
   }
   ++*launches;
   return cudaGetLastError();

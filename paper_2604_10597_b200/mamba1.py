@@ -14,6 +14,7 @@ paper's Python hook, is gone).
 """
 from __future__ import annotations
 
+import copy as _copy
 import ctypes as C
 from dataclasses import dataclass
 from typing import Optional
@@ -266,6 +267,11 @@ class Prefill:
         # scan kernel family for __call__ / from_conv-free paths ("auto": by shape; "chained"
         # makes the decided chunk the scan's segment length on every shape -- chunk sweeps)
         self.scan_variant = "auto"
+        # strided sampling: the gathered samples and the stride-1 spec that bins them
+        self.samples = None
+        spec1 = _copy.copy(self.spec)
+        spec1.sample_stride = 1
+        self.cspec1 = spec1.to_c()
 
     # -- stages (exposed for the sharded path and for per-stage timing) --
     def stage_init(self, scan_inputs=None):
@@ -335,6 +341,41 @@ class Prefill:
                       C.byref(self.cspec), self.range.data_ptr(), self.counts.data_ptr(),
                       C.byref(self.rule), int(seq_len), self.decision_buf.data_ptr(), s)
 
+    def stage_entropy(self, u_flat: torch.Tensor, seq_len: int):
+        """The single-GPU entropy stages after stage_init, as cl_prefill_f32 runs them:
+        min/max, then histogram + decision in one launch; for sample_stride >=
+        CL_GATHER_MIN_STRIDE the min/max also gathers the sampled values
+        (cl_minmax_gather_f32) and the histogram reads only those."""
+        self.stage_entropy_minmax(u_flat)
+        self.stage_entropy_histogram(u_flat, seq_len)
+
+    def _gathers(self) -> bool:
+        return int(self.spec.sample_stride) >= _lib.CL_GATHER_MIN_STRIDE
+
+    def stage_entropy_minmax(self, u_flat: torch.Tensor):
+        """First half of stage_entropy (after stage_init)."""
+        if not self._gathers():
+            self.stage_minmax(u_flat, init=False)
+            return
+        st = int(self.spec.sample_stride)
+        m = int(self.ctx.lib.cl_samples_in(0, u_flat.numel(), st))
+        if self.samples is None or self.samples.numel() < m:
+            self.samples = torch.empty(max(m, 1), dtype=torch.float32, device=self.device)
+        self.ctx.call("cl_minmax_gather_f32", u_flat.data_ptr(), u_flat.numel(), 0, st,
+                      self.range.data_ptr(), self.samples.data_ptr(), _stream_ptr(self.device))
+
+    def stage_entropy_histogram(self, u_flat: torch.Tensor, seq_len: int):
+        """Second half of stage_entropy: histogram + decision (of the gathered samples
+        when stage_entropy_minmax gathered them)."""
+        if not self._gathers():
+            self.stage_histogram_decide(u_flat, seq_len, zero=False)
+            return
+        m = int(self.ctx.lib.cl_samples_in(0, u_flat.numel(), int(self.spec.sample_stride)))
+        self.ctx.call("cl_histogram_decide_f32", self.samples.data_ptr(), m,
+                      C.byref(self.cspec1), self.range.data_ptr(), self.counts.data_ptr(),
+                      C.byref(self.rule), int(seq_len), self.decision_buf.data_ptr(),
+                      _stream_ptr(self.device))
+
     def stage_decide(self, n_samples_total: int, seq_len: int):
         self.ctx.call("cl_decide", self.counts.data_ptr(), self.range.data_ptr(),
                       C.byref(self.cspec), int(n_samples_total), C.byref(self.rule),
@@ -361,8 +402,7 @@ class Prefill:
         else:
             uf = u.reshape(-1)
             self.stage_init((u, delta, A, B, C))
-            self.stage_minmax(uf, init=False)
-            self.stage_histogram_decide(uf, u.shape[-1], zero=False)
+            self.stage_entropy(uf, u.shape[-1])
         res = self.stage_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, out,
                               return_last_state, h0, variant=self.scan_variant)
         if return_last_state:

@@ -70,6 +70,8 @@ def test_enum_constants_match_the_header():
         m = re.search(rf"\b{name}\s*=\s*(\d+)", src)
         assert m, name
         assert getattr(_lib, name) == int(m.group(1)), name
+    m = re.search(r"#define\s+CL_GATHER_MIN_STRIDE\s+(\d+)", src)
+    assert m and _lib.CL_GATHER_MIN_STRIDE == int(m.group(1))
 
 
 def test_scan_variant_codes():
@@ -82,3 +84,15 @@ def test_scan_variant_codes():
     assert _variant_code("lb:2") == _lib.CL_SCAN_LOOKBACK_BASE + 2
     with pytest.raises(KeyError):
         _variant_code("nope")
+
+
+def test_samples_in_counts_multiples():
+    """cl_samples_in (pure host function): the number of global indices in
+    [offset, offset + n) that are multiples of stride."""
+    lib = _lib.load_library()
+    for off in (0, 1, 7, 8, 1000003):
+        for n in (0, 1, 5, 8, 999):
+            for st in (1, 3, 4, 8, 16):
+                want = sum(1 for g in range(off, off + n) if g % st == 0)
+                assert lib.cl_samples_in(off, n, st) == want, (off, n, st)
+    assert lib.cl_samples_in(5, 10, 0) == 0

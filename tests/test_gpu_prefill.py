@@ -215,3 +215,39 @@ def test_histogram_decide_fused_equals_separate(cuda, case):
         assert torch.equal(a.counts, b.counts)
         assert torch.equal(a.decision_buf, b.decision_buf)
         assert torch.equal(a.range, b.range)
+
+
+@pytest.mark.parametrize("stride", [4, 5, 8, 16])
+@pytest.mark.parametrize("n,offset", [(1 << 20, 0), (3 * 1000 * 997 + 13, 3), (4099, 1)])
+def test_gathered_strided_entropy_equals_full_read(cuda, stride, n, offset):
+    """For sample_stride >= CL_GATHER_MIN_STRIDE the single-GPU prefill gathers the sampled
+    values during min/max (cl_minmax_gather_f32) and histograms only those: range, counts
+    and the decision record equal the all-elements strided path bit for bit."""
+    g = torch.Generator().manual_seed(n % 97 + stride)
+    buf = torch.randn(n + offset, generator=g).to(cuda)
+    uf = buf[offset:]
+    spec = cl.HistogramSpec(sample_stride=stride)
+    a, b = Prefill(spec, device=cuda), Prefill(spec, device=cuda)
+    a.stage_init()
+    a.stage_minmax(uf, init=False)
+    a.stage_histogram_decide(uf, 2048, zero=False)
+    b.stage_init()
+    b.stage_entropy(uf, 2048)
+    torch.cuda.synchronize()
+    assert torch.equal(a.range, b.range)
+    assert torch.equal(a.counts, b.counts)
+    assert torch.equal(a.decision_buf, b.decision_buf)
+    assert int(b.counts.sum()) == (n + stride - 1) // stride
+
+
+def test_gathered_prefill_matches_oracle_decision(cuda, port):
+    """The whole strided prefill (gathered entropy -> decision -> scan) against the C
+    oracle's strided histogram and rule."""
+    x = mamba_inputs(31, 2, 64, 16, 1024)
+    d = dev(x, cuda)
+    spec = cl.HistogramSpec(sample_stride=8)
+    pf = Prefill(spec, device=cuda)
+    pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"])
+    torch.cuda.synchronize()
+    ref, *_ = port.histogram(x["u"].reshape(-1), 256, 1e-8, 8)
+    assert (pf.counts.cpu().numpy().astype(np.uint64) == ref).all()

@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-for i in 1 2; do for f in 256 64 1024 4096; do
-  echo -n "F=$f "; CL_TOK_FLUSH_COST=$f timeout 300 python tools/profile_token.py --reps 10 2>&1 | tail -1
-done; done > gpurun_out/v_ab.txt
-timeout 600 python -m pytest tests -m gpu -x -q -k "token" > gpurun_out/v_tests.log 2>&1; echo rc=$? >> gpurun_out/v_tests.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/w_tests.log 2>&1; echo rc=$? >> gpurun_out/w_tests.log
+timeout 500 python bench.py --config C4 --chunk-policy guarded --steps 20 --warmup 3 --no-producer --no-e2e --no-cpu > gpurun_out/w_bench_C4g.json 2>gpurun_out/w_bench.err
