@@ -177,17 +177,44 @@ int cl_prefill_sharded_f32(cl_ctx* ctx, const cl_mamba1_args* args, const cl_sha
   }
   if ((rc = cl_prefill_init_prepare_f32(ctx, d_range, d_counts, spec->bin_count, args, stream)))
     return rc;
-  for (const Segment& s : segs)
-    if ((rc = cl_minmax_f32(ctx, u + s.local_offset, s.numel, s.global_offset,
-                            spec->sample_stride, d_range, stream)))
+  const bool gather = spec->sample_stride >= CL_GATHER_MIN_STRIDE;
+  if (gather) {
+    // as cl_prefill_f32: min/max gathers every segment's samples (consecutively; the
+    // counts do not depend on their order) and the histogram reads only those
+    cl_workspace* w = workspace(ctx, static_cast<cudaStream_t>(stream));
+    if (!w) return CL_E_CUDA;
+    uint64_t m = 0;
+    for (const Segment& s : segs) m += cl_samples_in(s.global_offset, s.numel, spec->sample_stride);
+    if ((rc = grow_scratch(ctx, w, &w->d_samples, &w->samples_bytes, (m ? m : 1) * sizeof(float),
+                           "cudaMalloc(gathered samples)")))
       return rc;
-  if ((rc = hook(ctx, coll->allreduce_max_f64(d_range, 4, stream, coll->user),
-                 "allreduce_max_f64(range)")))
-    return rc;
-  for (const Segment& s : segs)
-    if ((rc = cl_histogram_f32(ctx, u + s.local_offset, s.numel, s.global_offset, spec, d_range,
-                               d_counts, stream)))
+    uint64_t at = 0;
+    for (const Segment& s : segs) {
+      if ((rc = cl_minmax_gather_f32(ctx, u + s.local_offset, s.numel, s.global_offset,
+                                     spec->sample_stride, d_range, w->d_samples + at, stream)))
+        return rc;
+      at += cl_samples_in(s.global_offset, s.numel, spec->sample_stride);
+    }
+    if ((rc = hook(ctx, coll->allreduce_max_f64(d_range, 4, stream, coll->user),
+                   "allreduce_max_f64(range)")))
       return rc;
+    cl_hist_spec s1 = *spec;
+    s1.sample_stride = 1;
+    if (m && (rc = cl_histogram_f32(ctx, w->d_samples, m, 0, &s1, d_range, d_counts, stream)))
+      return rc;
+  } else {
+    for (const Segment& s : segs)
+      if ((rc = cl_minmax_f32(ctx, u + s.local_offset, s.numel, s.global_offset,
+                              spec->sample_stride, d_range, stream)))
+        return rc;
+    if ((rc = hook(ctx, coll->allreduce_max_f64(d_range, 4, stream, coll->user),
+                   "allreduce_max_f64(range)")))
+      return rc;
+    for (const Segment& s : segs)
+      if ((rc = cl_histogram_f32(ctx, u + s.local_offset, s.numel, s.global_offset, spec, d_range,
+                                 d_counts, stream)))
+        return rc;
+  }
   if ((rc = hook(ctx,
                  coll->allreduce_sum_u64(d_counts, size_t(spec->bin_count), stream, coll->user),
                  "allreduce_sum_u64(counts)")))
