@@ -633,9 +633,9 @@ __device__ __forceinline__ void pair_box(const unsigned char* st, float* ydst, i
     if (4 * j >= valid) break;
     const int off = Geo<BOX>::swz(r, j);
     const float4 u4 = *reinterpret_cast<const float4*>(st + off);
-    const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
+    const float2 d2 = *reinterpret_cast<const float2*>(st + G::kTileBytes + off + 8 * hf);
     // softplus of timesteps (2hf, 2hf+1) here, the other pair from the partner lane
-    f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
+    f2_t mine = add2(pk(d2.x, d2.y), bias2);
     if (SP) mine = softplus2(mine);
     const f2_t other = shfl_xor2(mine, 1);
     const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
@@ -683,8 +683,8 @@ __device__ __forceinline__ void pair_box(const unsigned char* st, float* ydst, i
     const f2_t u2 = hf ? pk(u4.z, u4.w) : pk(u4.x, u4.y);
     f2_t yo = fma2(pk(Dc, Dc), u2, ysum);
     if (HZ) {
-      const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
-      yo = mul2(yo, silu2(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y)));
+      const float2 z2 = *reinterpret_cast<const float2*>(st + 2 * G::kTileBytes + off + 8 * hf);
+      yo = mul2(yo, silu2(pk(z2.x, z2.y)));
     }
     if (ydst) {
       float y0, y1;
@@ -716,8 +716,9 @@ __device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* yd
   auto prep = [&](int j, float (&dt)[4], float (&xs)[4], f2_t& u2, f2_t& g2) {
     const int off = Geo<BOX>::swz(r, j);
     const float4 u4 = *reinterpret_cast<const float4*>(st + off);
-    const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
-    f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
+    // this lane's delta pair (timesteps 2hf, 2hf + 1): an 8-byte load, no select
+    const float2 d2 = *reinterpret_cast<const float2*>(st + G::kTileBytes + off + 8 * hf);
+    f2_t mine = add2(pk(d2.x, d2.y), bias2);
     if (SP) mine = softplus2(mine);
     const f2_t other = shfl_xor2(mine, 1);
     const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
@@ -728,8 +729,8 @@ __device__ __forceinline__ void pair_box_pipe(const unsigned char* st, float* yd
     upk(x23, xs[2], xs[3]);
     u2 = hf ? pk(u4.z, u4.w) : pk(u4.x, u4.y);
     if (HZ) {
-      const float4 z4 = *reinterpret_cast<const float4*>(st + 2 * G::kTileBytes + off);
-      g2 = silu2(hf ? pk(z4.z, z4.w) : pk(z4.x, z4.y));
+      const float2 z2 = *reinterpret_cast<const float2*>(st + 2 * G::kTileBytes + off + 8 * hf);
+      g2 = silu2(pk(z2.x, z2.y));
     }
   };
   float dt[4], xs[4];

@@ -75,8 +75,9 @@ __device__ __forceinline__ void agg_box(const unsigned char* st, int r, int hf, 
     if (4 * j >= valid) break;
     const int off = Geo<BOX>::swz(r, j);
     const float4 u4 = *reinterpret_cast<const float4*>(st + off);
-    const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
-    f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
+    // this lane's delta pair (timesteps 2hf, 2hf + 1): an 8-byte load, no select
+    const float2 d2 = *reinterpret_cast<const float2*>(st + G::kTileBytes + off + 8 * hf);
+    f2_t mine = add2(pk(d2.x, d2.y), bias2);
     if (SP) mine = softplus2(mine);
     const f2_t other = shfl_xor2(mine, 1);
     const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;
@@ -127,8 +128,9 @@ __device__ __forceinline__ void agg_box_pipe(const unsigned char* st, int r, int
   auto prep = [&](int j, float (&dt)[4], float (&xs)[4]) {
     const int off = Geo<BOX>::swz(r, j);
     const float4 u4 = *reinterpret_cast<const float4*>(st + off);
-    const float4 d4 = *reinterpret_cast<const float4*>(st + G::kTileBytes + off);
-    f2_t mine = add2(hf ? pk(d4.z, d4.w) : pk(d4.x, d4.y), bias2);
+    // this lane's delta pair (timesteps 2hf, 2hf + 1): an 8-byte load, no select
+    const float2 d2 = *reinterpret_cast<const float2*>(st + G::kTileBytes + off + 8 * hf);
+    f2_t mine = add2(pk(d2.x, d2.y), bias2);
     if (SP) mine = softplus2(mine);
     const f2_t other = shfl_xor2(mine, 1);
     const f2_t dt01 = hf ? other : mine, dt23 = hf ? mine : other;

@@ -219,14 +219,19 @@ def test_histogram_decide_fused_equals_separate(cuda, case):
 
 @pytest.mark.parametrize("stride", [4, 5, 8, 16])
 @pytest.mark.parametrize("n,offset", [(1 << 20, 0), (3 * 1000 * 997 + 13, 3), (4099, 1)])
-def test_gathered_strided_entropy_equals_full_read(cuda, stride, n, offset):
+@pytest.mark.parametrize("kind", ["dynamic", "fixed", "k100"])
+def test_gathered_strided_entropy_equals_full_read(cuda, stride, n, offset, kind):
     """For sample_stride >= CL_GATHER_MIN_STRIDE the single-GPU prefill gathers the sampled
     values during min/max (cl_minmax_gather_f32) and histograms only those: range, counts
-    and the decision record equal the all-elements strided path bit for bit."""
+    and the decision record equal the all-elements strided path bit for bit (Dynamic and
+    Fixed range, power-of-two and other K)."""
     g = torch.Generator().manual_seed(n % 97 + stride)
     buf = torch.randn(n + offset, generator=g).to(cuda)
     uf = buf[offset:]
-    spec = cl.HistogramSpec(sample_stride=stride)
+    spec = {"dynamic": cl.HistogramSpec(sample_stride=stride),
+            "fixed": cl.HistogramSpec(sample_stride=stride, range_mode=cl.RangeMode.Fixed,
+                                      fixed_lo=-1.5, fixed_hi=2.0),
+            "k100": cl.HistogramSpec(sample_stride=stride, bin_count=100)}[kind]
     a, b = Prefill(spec, device=cuda), Prefill(spec, device=cuda)
     a.stage_init()
     a.stage_minmax(uf, init=False)
