@@ -391,19 +391,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-[[maybe_unused]] __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
   asm volatile(
@@ -1699,9 +1686,6 @@ constexpr int kTokHMaxPerFlush = 65000;     // u16 counters: flush before overfl
 #ifndef CL_TOK_QUAD
 #define CL_TOK_QUAD 1
 #endif
-#ifndef CL_TOK_PROD_SLEEP
-#define CL_TOK_PROD_SLEEP 0
-#endif
 
 __device__ __forceinline__ void tok_item_split(uint64_t item, uint64_t tiles, uint64_t splits,
                                                uint64_t channels, uint64_t* tile,
@@ -2014,15 +1998,8 @@ __global__ void __launch_bounds__((kTokTWarps + 1) * 32) token_hist_tma_kernel(
         const uint64_t c1 = umin64(a.channels, c0 + per_split);
         for (uint64_t c = c0; c < c1; c += kTokBoxRows, ++it) {
           const int st = it % kTokStages;
-          if (it >= static_cast<uint32_t>(kTokStages)) {
-#if CL_TOK_PROD_SLEEP
-            // back off instead of spinning: the consumers are the bound, and a spinning
-            // producer takes issue slots from the consumer warps of its sub-partition
-            while (!mbar_test(empty + st, ((it / kTokStages) - 1) & 1)) __nanosleep(CL_TOK_PROD_SLEEP);
-#else
-            mbar_wait(empty + st, ((it / kTokStages) - 1) & 1);
-#endif
-          }
+          // (a nanosleep backoff instead of this wait measured no different, r2n)
+          if (it >= static_cast<uint32_t>(kTokStages)) mbar_wait(empty + st, ((it / kTokStages) - 1) & 1);
           mbar_expect_tx(full + st, kTokBoxBytes);
           tma_load_3d(ring + size_t(st) * kTokBoxBytes, &map, static_cast<int>(tile * 128),
                       static_cast<int>(c), 0, full + st);
