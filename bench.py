@@ -55,12 +55,11 @@ CONFIGS = {
 
 
 def library_sha256():
-    import hashlib
-    from paper_2604_10597_b200 import _lib
-    h = hashlib.sha256()
-    with open(_lib.LIB_PATH, "rb") as f:
-        h.update(f.read())
-    return h.hexdigest()
+    """The library build's fingerprint (sources, headers, nvcc flags, toolkit version:
+    paper_2604_10597_b200.build.fingerprint); the .so bytes themselves are not
+    reproducible from build to build."""
+    from paper_2604_10597_b200 import build as _build
+    return _build.fingerprint()
 
 
 def cpu_model():

@@ -43,6 +43,25 @@ def headers():
                   glob.glob(os.path.join(INCLUDE, "*.h")))
 
 
+def fingerprint() -> str:
+    """sha256 of what determines the library's code: every source and header, the nvcc
+    flags and the toolkit's version file.  nvcc's output bytes are not reproducible from
+    build to build (embedded module ids), so measurements recorded against a build (the
+    scan's ncu DRAM traffic, profiles/scan_traffic.json) are keyed to this instead."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(" ".join(ARCH + NVCC_FLAGS[:-2]).encode())  # flags without the absolute -I paths
+    for f in sources() + headers():
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    ver = os.path.join(os.path.dirname(os.path.dirname(nvcc())), "version.json")
+    if os.path.exists(ver):
+        with open(ver, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def _newer(target, deps):
     if not os.path.exists(target):
         return True

@@ -9,8 +9,10 @@ On a GPU box:
 Here (or there):
     python tools/scan_traffic.py --record gpurun_out/traffic_C3.csv C3
 appends / replaces the record {config, kernel, kernel_family, lib_sha256, dram bytes} in
-profiles/scan_traffic.json.  bench.py uses a record only when config, kernel family and the
-sha256 of paper_2604_10597_b200/libchunklab_b200.so all match (else traffic = null).
+profiles/scan_traffic.json.  lib_sha256 is the build fingerprint (sha256 of the library's
+sources, headers and nvcc flags: paper_2604_10597_b200.build.fingerprint -- nvcc's output
+bytes differ from build to build).  bench.py uses a record only when config, kernel family
+and the fingerprint all match (else traffic = null).
 """
 import argparse
 import csv
