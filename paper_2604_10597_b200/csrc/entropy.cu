@@ -25,6 +25,10 @@
 #ifndef CL_DEVICE_CHECKS
 #define CL_DEVICE_CHECKS 0
 #endif
+// lane_count_u8 counts with shared-memory reductions (1) or read-modify-write pairs (0)
+#ifndef CL_HIST_ATOMS
+#define CL_HIST_ATOMS 1
+#endif
 #include "conv_common.cuh"
 #include "range.cuh"
 #include "tma_map.cuh"
@@ -346,7 +350,7 @@ __device__ __forceinline__ uint32_t cofs(uint32_t b) {
 // magic-number rounded t = n + 1.5*2^23 (bits 0x4B400000 + n, 0 <= n < 256, so n's bits
 // are the low byte and the exponent bits lie above it): (n & ~3)*32 + (n & 3) plus the
 // lane's word and the warp's block (wl = warp*8192 + lane*4) -- LOP3, LOP3, IMAD.
-__device__ __forceinline__ uint32_t cofs_from_tbits(uint32_t tb, uint32_t wl) {
+[[maybe_unused]] __device__ __forceinline__ uint32_t cofs_from_tbits(uint32_t tb, uint32_t wl) {
   uint32_t o;
   asm("{\n"
       ".reg .b32 hi, lo;\n"
@@ -544,6 +548,20 @@ __device__ __forceinline__ void lane_count_u8(const float (&val)[NS], const BinP
   // the counter block starts at dynamic shared offset 0, so an offset is an address
   // and the loads / stores below are LDS/STS [R + UR(base)] with no add
   const uint32_t wl = static_cast<uint32_t>(warp) * (kLaneBins * 32) + lane * 4u;
+#if CL_HIST_ATOMS
+  // one shared-memory reduction per sample on the lane's own word (byte n & 3 of word
+  // (n >> 2, lane)): no read-modify-write chain, same-bin samples need no special case;
+  // a byte never carries into its neighbour (<= 246 increments between flushes)
+  const uint32_t base = smem_u32(cblk);
+#pragma unroll
+  for (int e = 0; e < NS; ++e) {
+    const uint32_t w = base + (tb[e] & 0xFCu) * 32u + wl;
+    const uint32_t inc = 1u << ((tb[e] & 3u) << 3);
+    // volatile, no memory clobber: the reductions stay in program order among themselves
+    // and behind the flush's __syncwarp, without pinning the surrounding loads
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(w), "r"(inc));
+  }
+#else
 #pragma unroll
   for (int g = 0; g < NS / 2; ++g) {
     // plain accesses: the offsets may alias, so the compiler keeps this order
@@ -554,6 +572,7 @@ __device__ __forceinline__ void lane_count_u8(const float (&val)[NS], const BinP
     cblk[o0] = static_cast<unsigned char>(v0 + 1u);
     cblk[o1] = static_cast<unsigned char>(v1 + 1u + (o0 == o1 ? 1u : 0u));
   }
+#endif
 }
 
 template <int MODE, bool FIXED>
