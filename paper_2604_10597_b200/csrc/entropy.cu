@@ -1705,6 +1705,9 @@ constexpr int kTokHMaxPerFlush = 65000;     // u16 counters: flush before overfl
 #ifndef CL_TOK_QUAD
 #define CL_TOK_QUAD 1
 #endif
+#ifndef CL_TOK_RED
+#define CL_TOK_RED 1
+#endif
 
 __device__ __forceinline__ void tok_item_split(uint64_t item, uint64_t tiles, uint64_t splits,
                                                uint64_t channels, uint64_t* tile,
@@ -2084,7 +2087,23 @@ __global__ void __launch_bounds__((kTokTWarps + 1) * 32) token_hist_tma_kernel(
       // u16 counters [bin][lane] (address = base + bin * 64: one IMAD; the lane pair sharing
       // a bank word conflicts only on different bins of equal parity -- this loop is
       // ALU-bound, not shared-memory-bound, ncu r2f)
-      if (CL_TOK_QUAD && __all_sync(0xffffffffu, smp == 0xFFFFu)) {
+      if (CL_TOK_RED) {
+        // one shared-memory reduction per sample on the 32-bit word the lane shares with
+        // its neighbour: this lane's u16 half is 1 << 16 * (lane & 1) (<= 65000 counts
+        // between flushes, so a half never carries); no read-modify-write chain
+        const uint32_t wbase = cbase & ~3u;
+        const uint32_t inc1 = 1u << ((lane & 1) * 16);
+        if (__all_sync(0xffffffffu, smp == 0xFFFFu)) {
+#pragma unroll
+          for (int r = 0; r < kTokBoxRows; ++r)
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(wbase + static_cast<uint32_t>(bin[r]) * 64u), "r"(inc1));
+        } else {
+#pragma unroll
+          for (int r = 0; r < kTokBoxRows; ++r)
+            if ((smp >> r) & 1u)
+              asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(wbase + static_cast<uint32_t>(bin[r]) * 64u), "r"(inc1));
+        }
+      } else if (CL_TOK_QUAD && __all_sync(0xffffffffu, smp == 0xFFFFu)) {
         // full box, every row sampled (stride 1): constant increments, four samples per
         // read-modify-write round (all four loads, then the stores in sample order, each
         // carrying the earlier samples of its bin: the last store to a bin holds the
@@ -2145,7 +2164,17 @@ __global__ void __launch_bounds__((kTokTWarps + 1) * 32) token_hist_tma_kernel(
         // this warp's 32 positions into counts [L][K], counters cleared (warp-local)
         __syncwarp();
         if (t_ok) {
-          for (int b = 0; b < k; ++b) {
+          // four counters in flight per step (the loads no longer wait on each other)
+          int b = 0;
+          for (; b + 4 <= k; b += 4) {
+            uint32_t v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = tcnt[(warp * 256 + b + q) * 32 + lane];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (v[q]) atomicAdd(counts + t * k + b + q, v[q]);
+          }
+          for (; b < k; ++b) {
             const uint32_t v = tcnt[(warp * 256 + b) * 32 + lane];
             if (v) atomicAdd(counts + t * k + b, v);
           }
