@@ -446,10 +446,10 @@ def main():
         graphs = []
         captured0 = pf.ctx.launches
         with torch.cuda.stream(cap):
-            # (the graphs are captured on one stream and so share its captured workspace:
-            # the init launch re-lays B / C for the scan graph, as in an eager prefill)
-            scan_in = (x["u"], x["delta"], x["A"], x["B"], x["C"])
-            for stage in (lambda: (pf.stage_init(scan_in), pf.stage_entropy_minmax(uf)),
+            # (the graphs are captured on one stream and share its captured workspace; the
+            # scan graph re-lays B / C itself -- a hand-off from another graph's init launch
+            # would depend on replay order, so the library only takes it within one capture)
+            for stage in (lambda: (pf.stage_init(), pf.stage_entropy_minmax(uf)),
                           lambda: pf.stage_entropy_histogram(uf, L),
                           lambda: pf.stage_scan(x["u"], x["delta"], x["A"], x["B"], x["C"],
                                                 x["D"], x["z"], x["delta_bias"], True, out,
@@ -465,7 +465,7 @@ def main():
             # untimed stage breakdown
             g_ent = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g_ent, stream=cap):
-                pf.stage_init(scan_in)
+                pf.stage_init()
                 pf.stage_entropy(uf, L)
         torch.cuda.current_stream(device).wait_stream(cap)
         torch.cuda.synchronize()

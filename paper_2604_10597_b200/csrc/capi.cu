@@ -33,6 +33,16 @@ int zero_now(cl_ctx* ctx, void* p, size_t bytes) {
   return e == cudaSuccess ? CL_OK : cuda_fail(ctx, e, "zero scratch");
 }
 
+unsigned long long capture_id_of(cudaStream_t stream) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  if (cudaStreamGetCaptureInfo(stream, &cs, &id) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return cs == cudaStreamCaptureStatusActive ? id : 0;
+}
+
 cl_workspace* workspace(cl_ctx* ctx, cudaStream_t stream) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   unsigned long long capture_id = 0;

@@ -33,10 +33,13 @@ struct cl_workspace {
   // d_bct already holds the interleaved [B | C] re-layout of these inputs, written by
   // cl_prefill_init_prepare_f32 earlier on this stream; the next scan with the same B, C,
   // batch and L consumes it (and clears it) instead of launching its own transpose
+  // (in a captured workspace only within the same capture: a graph's replays cannot know
+  // what another graph's replays left in d_bct)
   bool bct_ready = false;
   const float* bct_B = nullptr;
   const float* bct_C = nullptr;
   uint64_t bct_batch = 0, bct_L = 0;
+  unsigned long long bct_capture = 0;  // capture id of the prepare (0: eager)
   // L-parallel scan: per-(tile, segment) aggregates {tag, h~_end[16], sum dt} words
   unsigned long long* d_agg = nullptr;
   size_t agg_bytes = 0;
@@ -105,6 +108,8 @@ int zero_now(cl_ctx* ctx, void* p, size_t bytes);
 // The workspace of `stream` (created on first use); nullptr + error on allocation failure.
 // Inside a stream capture: the stream's captured workspace (shared by its captures).
 cl_workspace* workspace(cl_ctx* ctx, cudaStream_t stream);
+// id of the capture in progress on the stream, 0 when the stream is not capturing
+unsigned long long capture_id_of(cudaStream_t stream);
 
 // cudaMalloc is not allowed while a stream captures in the default (global) mode; a
 // library may switch the calling thread to relaxed mode around its own allocations.

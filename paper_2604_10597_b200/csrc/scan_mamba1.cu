@@ -907,6 +907,7 @@ int scan_prepare_with_init(cl_ctx* ctx, const cl_mamba1_args& a, double* d_range
   if (e != cudaSuccess) return cuda_fail(ctx, e, "init_transpose_kernel launch");
   ++ctx->launches;
   w->bct_ready = ws;
+  w->bct_capture = capture_id_of(s);
   w->bct_B = a.B;
   w->bct_C = a.C;
   w->bct_batch = Bt;
@@ -1015,7 +1016,8 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(scan work)");
     w->ticket_dirty = !ws;  // the row kernel leaves its ticket and flags behind
     const bool prepared = ws && w->bct_ready && w->bct_B == a.B && w->bct_C == a.C &&
-                          w->bct_batch == Bt && w->bct_L == L;
+                          w->bct_batch == Bt && w->bct_L == L &&
+                          w->bct_capture == capture_id_of(s);
     w->bct_ready = false;  // consumed (or stale) either way
     if (!prepared) {
       const dim3 tgrid(static_cast<unsigned>((L + 31) / 32), static_cast<unsigned>(Bt), 2);

@@ -256,3 +256,35 @@ def test_gathered_prefill_matches_oracle_decision(cuda, port):
     torch.cuda.synchronize()
     ref, *_ = port.histogram(x["u"].reshape(-1), 256, 1e-8, 8)
     assert (pf.counts.cpu().numpy().astype(np.uint64) == ref).all()
+
+
+def test_bc_relayout_handoff_is_per_capture(cuda):
+    """The init launch's B / C re-layout (cl_prefill_init_prepare_f32) is consumed by the
+    scan only within one capture: a scan graph captured separately from its init graph
+    re-lays B / C itself, so replaying another prefill's graph in between cannot leave it
+    reading a stale re-layout."""
+    xa = dev(mamba_inputs(50, 2, 64, 16, 1024), cuda)
+    xb = dev(mamba_inputs(51, 2, 64, 16, 1024), cuda)
+    pa, pb = Prefill(cl.HistogramSpec(), device=cuda), Prefill(cl.HistogramSpec(), device=cuda)
+    pa.scan_variant = pb.scan_variant = "chained"
+    args_a = (xa["u"], xa["delta"], xa["A"], xa["B"], xa["C"], xa["D"], xa["z"], xa["delta_bias"])
+    args_b = (xb["u"], xb["delta"], xb["A"], xb["B"], xb["C"], xb["D"], xb["z"], xb["delta_bias"])
+    ref_a = pa(*args_a).out.clone()
+    ref_b = pb(*args_b).out.clone()
+    torch.cuda.synchronize()
+    out_a, out_b = torch.empty_like(ref_a), torch.empty_like(ref_b)
+    g_init, g_scan, g_b = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_init):
+        pa.stage_init(args_a[:5])
+        pa.stage_entropy(xa["u"].reshape(-1), 1024)
+    with torch.cuda.graph(g_scan):
+        pa.stage_scan(*args_a, True, out_a, variant="chained")
+    with torch.cuda.graph(g_b):
+        pb(*args_b, out=out_b)
+    for _ in range(3):
+        g_init.replay()
+        g_b.replay()      # another prefill's re-layout lands in the shared captured scratch
+        g_scan.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out_a, ref_a)
+        assert torch.equal(out_b, ref_b)
