@@ -1099,6 +1099,14 @@ int scan_mamba1(cl_ctx* ctx, const cl_mamba1_args& a, const cl_decision* d_decis
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     ++ctx->launches;
+    if (!ws && w->captured) {
+      // the row kernel leaves its ticket and flags behind; a captured graph cannot hand
+      // that state to later graphs through the host flag (their replay order is not
+      // known at capture), so it restores the clean ticket in-graph
+      e = cudaMemsetAsync(w->d_work, 0, work_bytes, s);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMemsetAsync(scan work)");
+      w->ticket_dirty = false;
+    }
     return CL_OK;
   }
   if (a.d_state < 1 || a.d_state > 64)

@@ -152,9 +152,10 @@ def test_several_graphs_share_the_captured_workspace(cuda):
     graphs all capture on one side stream).  Replayed interleaved -- A B A A C B C ... --
     each reproduces its eager bits: the L-parallel aggregate tags come from a device-side
     launch counter (never repeated across graphs), the chained carry words are zeroed
-    in-graph, and the ticket returns to 0 at the end of every launch."""
+    in-graph, and the work ticket is 0 again at the end of every launch (the row kernel's
+    graph restores it in-graph)."""
     cases = [((1, 48, 2048), "lookback"), ((2, 64, 512), "chained"), ((1, 32, 4096), "lookback"),
-             ((4, 64, 256), "auto")]
+             ((4, 64, 256), "auto"), ((2, 64, 512), "cfg:1")]  # cfg:1: the row kernel
     runs = []
     for i, (shape, variant) in enumerate(cases):
         d = dev(mamba_inputs(40 + i, *shape[:2], 16, shape[2]), cuda)
@@ -170,7 +171,7 @@ def test_several_graphs_share_the_captured_workspace(cuda):
         with torch.cuda.graph(g):
             r[0](*r[1], out=r[2])
         r[4] = g
-    for it, k in enumerate([0, 1, 0, 0, 2, 1, 2, 3, 0, 2, 2, 3, 1, 0]):
+    for it, k in enumerate([0, 1, 0, 0, 2, 1, 2, 3, 0, 2, 2, 3, 1, 0, 4, 1, 4, 0, 4, 3]):
         pf, args, out, ref, g = runs[k]
         out.zero_()
         g.replay()
