@@ -315,7 +315,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-producer", action="store_true",
                     help="skip the side measurements (conv1d producer fusion, token entropy)")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="timed e2e steps (0: enough for ~40 ms of PCIe traffic, at least 8)")
     ap.add_argument("--pipelined", action="store_true",
                     help="also measure two batches in flight (entropy of call i+1 in the lean "
                          "kernels under call i's scan); measured slower on B200, see DESIGN.md")
@@ -652,8 +653,14 @@ def main():
             def run_prefill(d, o):
                 pf(d["u"], d["delta"], d["A"], d["B"], d["C"], d["D"], d["z"], d["delta_bias"],
                    True, out=o)
+        e2e_steps = args.e2e_steps
+        if e2e_steps <= 0:
+            # the three-stream pipeline fills and drains around the timed steps: size the
+            # run to ~40 ms of uploads at ~50 GB/s so small configs reach steady state
+            step_s = sum(v.numel() * 4 for v in x.values()) / 50e9
+            e2e_steps = int(min(256, max(8, 0.04 / step_s)))
         result["e2e"] = e2e_measure(torch, dist, world, device, x, run_prefill, L, global_batch,
-                                    args.e2e_steps)
+                                    e2e_steps)
     del x, out
     torch.cuda.empty_cache()
 
