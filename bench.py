@@ -74,6 +74,9 @@ def cpu_model():
     return platform.processor() or "unknown"
 
 
+HBM_SPEC_GBS = 8000.0  # B200 HBM3e data-sheet bandwidth (report both)
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -589,6 +592,7 @@ def main():
                      "frac": scan_gbs / peak, "traffic": traffic, "traffic_source": traffic_note,
                      "kernel": "rowpair_ws_kernel",
                      "peak_kind": peak_kind,
+                     "spec_peak": HBM_SPEC_GBS, "spec_frac": scan_gbs / HBM_SPEC_GBS,
                      "algorithmic_bytes_per_launch": ab["scan"]},
         "stage_ms": ({k: statistics.mean(v) for k, v in stage_ms.items()} if world == 1 else
                      {"entropy_allreduce_decide": statistics.mean(stage_ms["entropy"]),
