@@ -108,7 +108,8 @@ class ClockSampler:
     def __init__(self, device_index=0):
         self.proc = None
         self.nvml = None
-        self.samples = []  # (time, sm_mhz, max_mhz, set of reasons)
+        self.samples = []  # (time, sm_mhz, max_mhz, set of reasons, power W or None)
+        self.power_limit_w = None
         self.dev = device_index
         self.stop = False
 
@@ -122,6 +123,10 @@ class ClockSampler:
                     "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
                     "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
             mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            try:
+                self.power_limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(h) / 1000.0
+            except Exception:
+                self.power_limit_w = None
             self.nvml = (pynvml, h, bits, mx)
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
@@ -145,7 +150,12 @@ class ClockSampler:
             try:
                 sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
                 r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((time.time(), sm, mx, {n for n, b in bits.items() if r & b}))
+                try:
+                    pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                except Exception:
+                    pw = None
+                self.samples.append((time.time(), sm, mx, {n for n, b in bits.items() if r & b},
+                                     pw))
             except Exception:
                 pass
             time.sleep(0.002)
@@ -160,7 +170,11 @@ class ClockSampler:
             except ValueError:
                 continue
             reasons = {n for n, v in zip(self.NAMES, parts[5:9]) if v.lower().startswith("active")}
-            self.samples.append((time.time(), sm, mx, reasons))
+            try:
+                pw = float(parts[3])
+            except ValueError:
+                pw = None
+            self.samples.append((time.time(), sm, mx, reasons, pw))
 
     def mark(self, which):
         setattr(self, which, time.time())
@@ -175,17 +189,27 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         t0, t1 = getattr(self, "t_start", 0.0), getattr(self, "t_stop", 1e30)
-        for ts, s_mhz, m_mhz, rs in list(self.samples):
+        for ts, s_mhz, m_mhz, rs, p_w in list(self.samples):
             if not (t0 <= ts <= t1 + 0.002):
                 continue
             sm.append(s_mhz)
             mx = m_mhz
             reasons |= rs
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm),
-                "source": "nvml" if self.nvml else "nvidia-smi"}
+            if p_w is not None:
+                pw.append(p_w)
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+               "reasons": sorted(reasons), "samples": len(sm),
+               "source": "nvml" if self.nvml else "nvidia-smi"}
+        if sm:
+            out["sm_mhz_min"] = min(sm)
+        if pw:  # board power during the timed region (sw_power_cap: at the enforced limit)
+            out["power_w_median"] = statistics.median(pw)
+            out["power_w_max"] = max(pw)
+        if self.power_limit_w:
+            out["power_limit_w"] = self.power_limit_w
+        return out
 
 
 # ----------------------------------------------------------------- data
