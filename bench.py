@@ -659,9 +659,11 @@ def main():
         pf(x["u"], x["delta"], x["A"], x["B"], x["C"], x["D"], x["z"], x["delta_bias"], True,
            out=out)  # the serial reference output of batch 0 (same decision buffers)
         torch.cuda.synchronize()
-        result["pipelined"] = pipelined_measure(
-            torch, device, x, pf, out, max(args.steps // 2, 6),
-            lambda seed: make_inputs(torch, device, batch, dim, L, N, seed))
+        mk = lambda seed: make_inputs(torch, device, batch, dim, L, N, seed)  # noqa: E731
+        result["pipelined"] = pipelined_measure(torch, device, x, pf, out,
+                                                max(args.steps // 2, 6), mk, lean=False)
+        result["pipelined_lean"] = pipelined_measure(torch, device, x, pf, out,
+                                                     max(args.steps // 2, 6), mk, lean=True)
 
     # ---- producer fusion (conv1d + SiLU with the min/max epilogue), side measurement
     if not args.no_producer and world == 1:
@@ -802,10 +804,10 @@ def producer_fusion_measure(torch, device, x, pf, reps=20):
     return res
 
 
-def pipelined_measure(torch, device, x, pf, out_serial, steps, make):
+def pipelined_measure(torch, device, x, pf, out_serial, steps, make, lean=True):
     """Steady-state throughput with two independent batches in flight: call i+1's entropy
-    (cl_entropy_lean_f32: lean kernels sized to share SMs with a scan CTA) on one stream
-    while call i's scan runs on another.  Every call still does all of its own work
+    (lean=True: cl_entropy_lean_f32, lean kernels sized to share SMs with a scan CTA;
+    lean=False: the regular stages) on one stream while call i's scan runs on another.  Every call still does all of its own work
     (min/max, histogram, device decision, scan); outputs are checked against the serial
     step bit for bit.  A separately labelled figure beside the single-call latency."""
     import paper_2604_10597_b200 as cl
@@ -824,7 +826,11 @@ def pipelined_measure(torch, device, x, pf, out_serial, steps, make):
         with torch.cuda.stream(s_ent):
             if scanned[j]:
                 s_ent.wait_event(scan_done[j])  # its buffers are read by that scan
-            pfs[j].stage_entropy_lean(sets[j]["u"].reshape(-1), L)
+            if lean:
+                pfs[j].stage_entropy_lean(sets[j]["u"].reshape(-1), L)
+            else:
+                pfs[j].stage_init()
+                pfs[j].stage_entropy(sets[j]["u"].reshape(-1), L)
             ent_done[j].record(s_ent)
 
     def scan(j):
@@ -858,9 +864,10 @@ def pipelined_measure(torch, device, x, pf, out_serial, steps, make):
     same_dec = bool(torch.equal(pfs[0].decision_buf, pf.decision_buf))
     res = {"ms_per_step": ms, "value": batch * L / (ms / 1e3), "unit": "tokens/s",
            "steps": steps, "matches_serial_bitwise": same and same_dec,
-           "workload": "two independent batches in flight: entropy(i+1) [lean kernels, stream "
-                       "2] under scan(i) [stream 1]; every call's own min/max + histogram + "
-                       "device decision + scan"}
+           "workload": "two independent batches in flight: entropy(i+1) [" +
+                       ("lean" if lean else "regular") + " kernels, stream 2] under scan(i) "
+                       "[stream 1]; every call's own min/max + histogram + device decision + "
+                       "scan"}
     del xb, outs, sets
     return res
 
