@@ -180,7 +180,10 @@ __device__ __forceinline__ void agg_box_pipe(const unsigned char* st, int r, int
 // Carry-in fold over segments [j0, j1) of one tile: h = exp2(A2 S_j) h + h~_j in segment
 // order.  The aggregate words are loaded kBatch segments at a time (independent loads in
 // flight), then polled only where a tag was not yet current.
-constexpr int kFoldBatch = 4;
+#ifndef CL_LB_FOLD_BATCH
+#define CL_LB_FOLD_BATCH 4
+#endif
+constexpr int kFoldBatch = CL_LB_FOLD_BATCH;  // segments per batch of loads: 2 and 4 tie, 8 is 5% slower (C1/C2)
 
 template <int NB>
 __device__ __forceinline__ void fold_batch(const unsigned long long* base, int j0, int r, int hf,
